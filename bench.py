@@ -1,0 +1,356 @@
+"""Benchmark: batched offline WFST beam-search decode on B200 (BASELINE.json
+configs[1]: Conformer-CTC-Large-shaped log-probs, 129 BPE+blank, 40 ms
+frames, 10 s utterances = 250 frames, synthetic 3-gram TLG of ~4.5M arcs,
+batch 512 per GPU, beam 17, max_active 10k).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A *step* decodes one batch of 512 utterances end to end (seed lanes,
+250-frame chunk, best path). metric = decode RTFx = audio s / decode s.
+* value: inputs already resident in HBM (one (512, 250, 129) f32 tensor),
+  timed with CUDA events around each step, L2 flushed between steps.
+* e2e:   the same public call (decode_batch) fed from PINNED HOST memory:
+  the H2D copy of the log-probs and the D2H of the transcripts are inside
+  the timed region.
+* cpu_baseline: the unmodified reference (oracle/_ref, compiled from
+  /root/reference) decoding a bounded sample of the same utterances on all
+  host cores, rank 0, N=1 only; its transcripts are also compared with ours.
+N>1 (torchrun): every rank decodes its own 512 utterances on its own graph
+replica (weak scaling, no collective on the data path); value = total audio
+over the max step time across ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FRAME_S = 0.04
+C2 = dict(num_units=129, blank_id=128, num_words=4000, order=3, seed=1, min_pron=1, max_pron=4,
+          followers=40, tri_contexts=0.3, tri_followers=8)
+LP = dict(delta=6.0, sigma=1.5)
+BEAM, MAX_ACTIVE = 17.0, 10_000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=512)
+    ap.add_argument("--frames", type=int, default=250)
+    ap.add_argument("--cpu-sample", type=int, default=24, help="utterances in the CPU baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--small", action="store_true", help="tiny graph smoke run (not a bench number)")
+    return ap.parse_args()
+
+
+def system(small: bool):
+    from paper_2311_04996_b200 import synth
+
+    spec = dict(C2)
+    if small:
+        spec.update(num_words=300, followers=10)
+    return synth.build_system(synth.SystemSpec(**spec))
+
+
+def workload(s, n, frames, rank):
+    from paper_2311_04996_b200 import synth
+
+    return synth.conformer_logprobs(s, n, frames, seed=1000 + rank, dtype=np.float32, **LP)
+
+
+# ------------------------------------------------------------ clocks ------
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md recipe)."""
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------- reference (CPU) ---
+
+
+def ref_module():
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    import ctcwfst  # the unmodified reference, compiled by oracle/build_ref.py
+
+    assert ctcwfst.KERNEL_NAME == "compiled"
+    return ctcwfst
+
+
+def ref_flatgraph(ctcwfst, fg):
+    """A reference FlatGraph built directly from our CSR arrays:
+    decode_batch accepts a FlatGraph, so no reference code changes."""
+    from ctcwfst.decoder import FlatGraph
+
+    r = FlatGraph.__new__(FlatGraph)
+    for k in ("num_states", "start", "off", "eps_end", "ilabel", "olabel", "weight", "nextstate", "final",
+              "max_ilabel", "max_olabel"):
+        setattr(r, k, getattr(fg, k))
+    return r
+
+
+def cpu_decode(utts, fg, cores):
+    ctcwfst = ref_module()
+    rfg = ref_flatgraph(ctcwfst, fg)
+    cfg = ctcwfst.DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE)
+    t0 = time.perf_counter()
+    hyps = ctcwfst.decode_batch(rfg, cfg, [u.astype(np.float64) for u in utts], workers=cores)
+    return hyps, time.perf_counter() - t0
+
+
+def cores_available():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------- main -------
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def reference_arm(args):
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    s = system(args.small)
+    n = args.cpu_sample
+    utts = list(workload(s, n, args.frames, 0))
+    cores = cores_available()
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_decode(utts[: max(1, cores)], s.graph, cores)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_decode(utts, s.graph, cores)
+        times.append(dt)
+    audio = n * args.frames * FRAME_S
+    value = audio * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": "decode RTFx (audio s / decode s)", "value": value, "unit": "x realtime",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2: 3-gram TLG %d states / %d arcs, V=129, 250-frame utts (10 s), beam 17, "
+                               "max_active 10k; CPU sample of %d utts per step" % (s.graph.num_states,
+                                                                                  s.graph.num_arcs, n)},
+        "cpu_baseline": {"value": value, "unit": "x realtime", "cores": cores, "kind": "reference",
+                         "sample": f"{n} utterances x {args.frames} frames per step", "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "x realtime", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+
+    world, rank, local = dist_setup(args)
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    from paper_2311_04996_b200 import DecoderConfig, Hypothesis, decode_batch
+
+    s = system(args.small)
+    fg = s.graph
+    cfg = DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE)
+    n, F, V = args.batch, args.frames, s.num_units
+    host = torch.from_numpy(workload(s, n, F, rank)).pin_memory()
+    host_np = host.numpy()
+    dev_ll = host.to(f"cuda:{dev}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    pool = fg.device_graph(dev).pool(cfg, fg.num_states)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        out = decode_batch(fg, cfg, dev_ll, device=dev)
+    assert all(isinstance(h, Hypothesis) for h in out), [h for h in out if not isinstance(h, Hypothesis)][:2]
+
+    # ---- value: inputs resident in HBM ----
+    pool.reset_stats()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(dev) as clk:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record()
+            out = decode_batch(fg, cfg, dev_ll, device=dev)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    st = pool.stats()
+    ms = sum(step_ms) / len(step_ms)
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    audio_total = world * n * F * FRAME_S
+    value = audio_total / (ms_max / 1e3)
+
+    # ---- e2e: pinned host input, transcripts back on the host ----
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        ev2[i][0].record()
+        out_e2e = decode_batch(fg, cfg, host_np, device=dev)
+        ev2[i][1].record()
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    assert [h.words for h in out_e2e] == [h.words for h in out]
+    words_bytes = sum(len(h.words) for h in out_e2e) * 4 + n * (8 + 8 + 4)
+
+    # ---- roofline of the frame kernel (k_decode_chunk) ----
+    launches = max(1, st["decode_launches"])
+    algo_bytes = (28 * st["arcs"] + 24 * st["src_tokens"]) / launches
+    kernel_ms = st["decode_ms"] / launches
+    achieved = algo_bytes / (kernel_ms / 1e3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+        except ValueError:
+            traffic = None
+
+    if rank != 0:
+        return
+    line = {
+        "metric": "decode RTFx (audio s / decode s)", "value": value, "unit": "x realtime", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2: synthetic 3-gram TLG (%d states, %d arcs), Conformer-CTC-shaped log-probs "
+                               "V=129 (blank 128), %d utts x %d frames (40 ms) per GPU, beam 17, max_active 10k"
+                               % (fg.num_states, fg.num_arcs, n, F),
+                   "global_batch": world * n, "frames": F, "parallelism": f"utterance-sharded x{world}",
+                   "l2": "flushed (256 MiB write) before every step"},
+        "utterances_per_s": world * n / (ms_max / 1e3),
+        "e2e": {"value": audio_total / (e2e_ms / 1e3), "unit": "x realtime",
+                "h2d_bytes_per_step": int(host_np.nbytes), "d2h_bytes_per_step": int(words_bytes)},
+        "gpu_launches": int(st["launches"]),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "k_decode_chunk",
+                     "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms_per_launch": kernel_ms,
+                     "bytes_model": "28*E_emit + 24*N_src (SURVEY 8(d))",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
+        "workload_stats": {"emitting_arcs_per_lane_frame": st["arcs"] / max(1, st["frames"]),
+                           "tokens_per_lane_frame": st["src_tokens"] / max(1, st["frames"]),
+                           "max_slots": st["max_slots"], "wall_s_timed": t_wall},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        k = min(args.cpu_sample, n)
+        cores = cores_available()
+        hyps, dt = cpu_decode([host_np[i] for i in range(k)], fg, cores)
+        cpu_rtfx = k * F * FRAME_S / dt
+        line["cpu_baseline"] = {"value": cpu_rtfx, "unit": "x realtime", "cores": cores, "kind": "reference",
+                                "sample": f"first {k} of the {n} utterances, reference decode_batch(workers={cores})",
+                                "cpu": cpu_model()}
+        same = all(getattr(h, "words", None) == g.words for h, g in zip(hyps, out[:k]))
+        rel = max(abs(h.total_cost - g.total_cost) / max(1.0, abs(h.total_cost)) for h, g in zip(hyps, out[:k]))
+        line["parity"] = {"utterances": k, "words_identical": bool(same), "max_cost_rel_diff": rel}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

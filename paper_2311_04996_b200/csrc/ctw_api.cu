@@ -1,0 +1,1109 @@
+// ctw_api.cu -- host side of libctcwfst_b200.so: the C-ABI declared in
+// include/ctcwfst_b200.h. Owns HBM allocations (graph, lanes), staging of
+// log-likelihood chunks, the grow-and-rerun protocol of chunk-atomic lanes,
+// and the export of histories in the reference layout.
+//
+// Reference call sites this layer stands behind (pkg/src/ctcwfst/):
+//   FlatGraph / flatten                      decoder.py:70-138
+//   DecodeState seeding / set_boost          decoder.py:173-238
+//   DecodeState.advance_frames               decoder.py:264-341
+//   best_path                                decoder.py:377-415
+//   history_records / active_tokens          decoder.py:240-260
+//   kernel plug-in contract                  _pykernel.py:28-248
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/ctcwfst_b200.h"
+#include "ctw_common.h"
+
+extern "C" int ctw_launch_decode(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
+                                 const double*, const void*, int, int, const long long*, const int*,
+                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, cudaStream_t);
+extern "C" int ctw_launch_seed(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
+                               const double*, const int*, int, int, const CtwDecodeCfg*, CtwLaneOut*,
+                               cudaStream_t);
+extern "C" int ctw_launch_best(const CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
+                               const double*, const int*, int, int32_t*, const long long*, const int*,
+                               int*, double*, int*, cudaStream_t);
+extern "C" int ctw_launch_clear(CtwTok*, uint32_t, cudaStream_t);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(-100 - (int)e_, std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  return cudaMalloc((void**)p, n * sizeof(T));
+}
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree((void*)p);
+  p = nullptr;
+}
+
+uint32_t ceil_log2(uint64_t x) {
+  uint32_t r = 0;
+  while ((1ull << r) < x) ++r;
+  return r;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ graph --
+
+struct ctw_graph {
+  int device = 0;
+  int64_t S = 0, A = 0, start = 0, max_il = 0, max_ol = 0;
+  CtwStateRange* ranges = nullptr;
+  CtwArc* arcs = nullptr;
+  int32_t* olabel = nullptr;
+  double* final_w = nullptr;
+  std::vector<double> h_final;
+};
+
+// ------------------------------------------------------------------ lanes --
+
+struct ctw_lanes {
+  ctw_graph* g = nullptr;
+  ctw_config cfg{};
+  CtwDecodeCfg dcfg{};
+  int n = 0, cap = 0;
+  CtwLane* h = nullptr;  // pinned host mirror
+  CtwLane* d = nullptr;  // device copy
+  std::vector<double*> boost_buf;
+  std::vector<int64_t> boost_cap;
+  std::vector<char> seeded;
+  std::vector<double> surv_ema;  // survivors per frame estimate, for history sizing
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // scratch
+  int* d_ids = nullptr;
+  int* d_nframes = nullptr;
+  long long* d_lloff = nullptr;
+  CtwLaneOut* d_out = nullptr;
+  int scratch_cap = 0;
+  int* h_ids = nullptr;
+  int* h_nframes = nullptr;
+  long long* h_lloff = nullptr;
+  CtwLaneOut* h_out = nullptr;
+  char* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  // best-path scratch
+  int32_t* d_words = nullptr;
+  size_t words_cap = 0;
+  long long* d_woff = nullptr;
+  int* d_wcap = nullptr;
+  int* d_nwords = nullptr;
+  double* d_tcost = nullptr;
+  int* d_bstatus = nullptr;
+  long long* h_woff = nullptr;
+  int* h_wcap = nullptr;
+  int* h_nwords = nullptr;
+  double* h_tcost = nullptr;
+  int* h_bstatus = nullptr;
+  int best_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // stats
+  int64_t launches = 0, decode_launches = 0, arcs = 0, srcs = 0, frames = 0, max_slots = 0;
+  double decode_ms = 0.0;
+  std::mutex mu;
+};
+
+namespace {
+
+int sync_lane(ctw_lanes* l, int i) {
+  CUDA_TRY(cudaMemcpyAsync(&l->d[i], &l->h[i], sizeof(CtwLane), cudaMemcpyHostToDevice, l->stream));
+  return 0;
+}
+
+void free_lane(CtwLane& L) {
+  dfree(L.table);
+  dfree(L.slots);
+  dfree(L.front);
+  for (auto& s : L.src) dfree(s);
+  dfree(L.pend);
+  dfree(L.rec_link);
+  dfree(L.rec_state);
+  dfree(L.rec_cost);
+  dfree(L.frame_base);
+  dfree(L.pool);
+}
+
+// (Re)allocate the table-sized buffers of lane i at capacity 1 << tlog2,
+// preserving the committed sources (and their pending chains).
+int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
+  CtwLane& L = l->h[i];
+  const uint64_t tcap = 1ull << tlog2;
+  const uint64_t scap = tcap / 2 + 1;
+  CtwTok* table;
+  uint32_t *slots, *front;
+  CtwSrc* src[3];
+  int32_t* pend;
+  CUDA_TRY(dalloc(&table, tcap));
+  CUDA_TRY(dalloc(&slots, tcap));
+  CUDA_TRY(dalloc(&front, 2 * tcap));
+  for (int b = 0; b < 3; ++b) CUDA_TRY(dalloc(&src[b], scap));
+  CUDA_TRY(dalloc(&pend, scap));
+  if (ctw_launch_clear(table, (uint32_t)tcap, l->stream)) return fail(-1, "clear kernel launch failed");
+  if (L.table) {
+    if (L.n_src > 0) {
+      CUDA_TRY(cudaMemcpyAsync(src[L.src_buf], L.src[L.src_buf], (size_t)L.n_src * sizeof(CtwSrc),
+                               cudaMemcpyDeviceToDevice, l->stream));
+      CUDA_TRY(cudaMemcpyAsync(pend, L.pend, (size_t)L.n_src * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                               l->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    dfree(L.table);
+    dfree(L.slots);
+    dfree(L.front);
+    for (auto& s : L.src) dfree(s);
+    dfree(L.pend);
+  }
+  L.table = table;
+  L.slots = slots;
+  L.front = front;
+  for (int b = 0; b < 3; ++b) L.src[b] = src[b];
+  L.pend = pend;
+  L.tlog2 = tlog2;
+  return sync_lane(l, i);
+}
+
+template <class T>
+int grow_keep(cudaStream_t st, T*& p, int64_t keep, int64_t ncap) {
+  T* np;
+  CUDA_TRY(dalloc(&np, (size_t)ncap));
+  if (p && keep > 0) CUDA_TRY(cudaMemcpyAsync(np, p, (size_t)keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  dfree(p);
+  p = np;
+  return 0;
+}
+
+int grow_hist(ctw_lanes* l, int i, int64_t need) {
+  CtwLane& L = l->h[i];
+  if (need <= L.rcap) return 0;
+  int64_t ncap = std::max<int64_t>(need, L.rcap + L.rcap / 2);
+  if (int r = grow_keep(l->stream, L.rec_link, L.n_rec, ncap)) return r;
+  if (int r = grow_keep(l->stream, L.rec_state, L.n_rec, ncap)) return r;
+  if (int r = grow_keep(l->stream, L.rec_cost, L.n_rec, ncap)) return r;
+  L.rcap = ncap;
+  return sync_lane(l, i);
+}
+
+int grow_frames(ctw_lanes* l, int i, int64_t need) {
+  CtwLane& L = l->h[i];
+  if (need <= L.fcap) return 0;
+  int64_t ncap = std::max<int64_t>(need, 2 * (int64_t)L.fcap);
+  if (ncap > INT32_MAX) return fail(-1, "frame count exceeds 2^31");
+  if (int r = grow_keep(l->stream, L.frame_base, L.frame_count, ncap)) return r;
+  L.fcap = (int32_t)ncap;
+  return sync_lane(l, i);
+}
+
+int grow_pool(ctw_lanes* l, int i, int64_t need) {
+  CtwLane& L = l->h[i];
+  if (need <= L.pcap) return 0;
+  int64_t ncap = std::max<int64_t>(need, 2 * (int64_t)L.pcap);
+  if (ncap > INT32_MAX) return fail(-1, "olabel pool exceeds 2^31");
+  if (int r = grow_keep(l->stream, L.pool, L.pool_used, ncap)) return r;
+  L.pcap = (int32_t)ncap;
+  return sync_lane(l, i);
+}
+
+int init_lane(ctw_lanes* l, int i) {
+  CtwLane& L = l->h[i];
+  std::memset(&L, 0, sizeof(L));
+  const uint64_t S = (uint64_t)std::max<int64_t>(l->g->S, 1);
+  const uint32_t tlog2 = std::min<uint32_t>(std::max<uint32_t>(6, ceil_log2(2 * S + 2)), 16);
+  if (int r = alloc_table(l, i, tlog2)) return r;
+  L.rcap = 1 << 12;
+  L.fcap = 256;
+  L.pcap = 1 << 10;
+  CUDA_TRY(dalloc(&L.rec_link, (size_t)L.rcap));
+  CUDA_TRY(dalloc(&L.rec_state, (size_t)L.rcap));
+  CUDA_TRY(dalloc(&L.rec_cost, (size_t)L.rcap));
+  CUDA_TRY(dalloc(&L.frame_base, (size_t)L.fcap));
+  CUDA_TRY(dalloc(&L.pool, (size_t)L.pcap));
+  return sync_lane(l, i);
+}
+
+int ensure_scratch(ctw_lanes* l, int n) {
+  if (n <= l->scratch_cap) return 0;
+  int c = std::max(n, 2 * l->scratch_cap);
+  dfree(l->d_ids);
+  dfree(l->d_nframes);
+  dfree(l->d_lloff);
+  dfree(l->d_out);
+  if (l->h_ids) cudaFreeHost(l->h_ids);
+  if (l->h_nframes) cudaFreeHost(l->h_nframes);
+  if (l->h_lloff) cudaFreeHost(l->h_lloff);
+  if (l->h_out) cudaFreeHost(l->h_out);
+  CUDA_TRY(dalloc(&l->d_ids, c));
+  CUDA_TRY(dalloc(&l->d_nframes, c));
+  CUDA_TRY(dalloc(&l->d_lloff, c));
+  CUDA_TRY(dalloc(&l->d_out, c));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_ids, c * sizeof(int)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_nframes, c * sizeof(int)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_lloff, c * sizeof(long long)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_out, c * sizeof(CtwLaneOut)));
+  l->scratch_cap = c;
+  return 0;
+}
+
+int reserve_lanes(ctw_lanes* l, int n) {
+  if (n <= l->n) return 0;
+  if (n > l->cap) {
+    int c = std::max(n, 2 * l->cap);
+    CtwLane* nh;
+    CtwLane* nd;
+    CUDA_TRY(cudaMallocHost((void**)&nh, c * sizeof(CtwLane)));
+    CUDA_TRY(dalloc(&nd, c));
+    if (l->h) {
+      std::memcpy(nh, l->h, l->n * sizeof(CtwLane));
+      cudaFreeHost(l->h);
+    }
+    if (l->d) {
+      CUDA_TRY(cudaMemcpyAsync(nd, l->d, l->n * sizeof(CtwLane), cudaMemcpyDeviceToDevice, l->stream));
+      CUDA_TRY(cudaStreamSynchronize(l->stream));
+      dfree(l->d);
+    }
+    l->h = nh;
+    l->d = nd;
+    l->cap = c;
+  }
+  for (int i = l->n; i < n; ++i) {
+    if (int r = init_lane(l, i)) return r;
+  }
+  l->boost_buf.resize(n, nullptr);
+  l->boost_cap.resize(n, 0);
+  l->seeded.resize(n, 0);
+  l->surv_ema.resize(n, -1.0);
+  l->n = n;
+  CUDA_TRY(cudaStreamSynchronize(l->stream));
+  return 0;
+}
+
+void update_from_out(CtwLane& L, const CtwLaneOut& o) {
+  L.n_src = o.n_src;
+  L.src_buf = o.src_buf;
+  L.frame_count = o.frame_count;
+  L.pool_used = o.pool_used;
+  L.n_rec = o.n_rec;
+  L.pend_valid = o.pend_valid;
+}
+
+int check_ids(ctw_lanes* l, const int32_t* ids, int n) {
+  std::vector<char> seen(l->n, 0);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= l->n) return fail(-1, "lane id out of range");
+    if (seen[ids[i]]) return fail(-1, "duplicate lane id in one batch");
+    seen[ids[i]] = 1;
+  }
+  return 0;
+}
+
+// Run the seed kernel on `ids`, growing tables / pools and re-running lanes
+// that ask for it. st[i] gets the per-lane CTW status.
+int run_seed(ctw_lanes* l, std::vector<int> ids, std::vector<int>& st) {
+  ctw_graph* g = l->g;
+  std::vector<int> pos(l->n, -1);
+  for (size_t i = 0; i < ids.size(); ++i) pos[ids[i]] = (int)i;
+  st.assign(ids.size(), CTW_OK);
+  std::vector<int> todo = ids;
+  for (int round = 0; !todo.empty(); ++round) {
+    if (round > 40) return fail(-1, "seed: grow loop did not converge");
+    const int n = (int)todo.size();
+    if (int r = ensure_scratch(l, n)) return r;
+    for (int i = 0; i < n; ++i) l->h_ids[i] = todo[i];
+    CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+    if (ctw_launch_seed(l->d, g->ranges, g->arcs, g->olabel, g->final_w, l->d_ids, n, (int)g->start,
+                        &l->dcfg, l->d_out, l->stream))
+      return fail(-1, std::string("seed launch: ") + cudaGetErrorString(cudaGetLastError()));
+    l->launches++;
+    CUDA_TRY(cudaMemcpyAsync(l->h_out, l->d_out, n * sizeof(CtwLaneOut), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    std::vector<int> again;
+    for (int i = 0; i < n; ++i) {
+      const int lane = todo[i];
+      const CtwLaneOut& o = l->h_out[i];
+      CtwLane& L = l->h[lane];
+      if (o.status == CTW_GROW_TABLE) {
+        if (int r = alloc_table(l, lane, L.tlog2 + 1)) return r;
+        again.push_back(lane);
+      } else if (o.status == CTW_GROW_POOL) {
+        if (int r = grow_pool(l, lane, 2 * (int64_t)L.pcap)) return r;
+        again.push_back(lane);
+      } else {
+        update_from_out(L, o);
+        st[pos[lane]] = o.status;
+      }
+    }
+    todo.swap(again);
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctw_abi_version(void) { return CTW_ABI_VERSION; }
+
+const char* ctw_last_error(void) { return g_err.c_str(); }
+
+int ctw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* ilabel,
+                     const int32_t* olabel, const double* weight, const int32_t* nextstate,
+                     const double* final_w, int64_t num_states, int64_t num_arcs, int64_t start,
+                     int32_t device, ctw_graph** out) {
+  *out = nullptr;
+  if (num_states <= 0) return fail(-1, "empty graph");
+  if (num_arcs < 0 || num_arcs >= 0x7FFFFFFFLL) return fail(-1, "arc count must be < 2^31");
+  if (num_states >= 0x7FFFFFFFLL) return fail(-1, "state count must be < 2^31");
+  if (start < 0 || start >= num_states) return fail(-1, "start state out of range");
+  if (off[0] != 0 || off[num_states] != num_arcs) return fail(-1, "off[] does not span the arcs");
+  std::vector<CtwStateRange> r((size_t)num_states);
+  int64_t max_il = 0, max_ol = 0;
+  for (int64_t s = 0; s < num_states; ++s) {
+    if (off[s + 1] < off[s] || eps_end[s] < off[s] || eps_end[s] > off[s + 1])
+      return fail(-1, "inconsistent CSR offsets");
+    r[s] = CtwStateRange{(uint32_t)off[s], (uint32_t)eps_end[s], (uint32_t)off[s + 1], 0u};
+  }
+  std::vector<CtwArc> arcs((size_t)std::max<int64_t>(num_arcs, 1));
+  for (int64_t s = 0; s < num_states; ++s) {
+    for (int64_t a = off[s]; a < off[s + 1]; ++a) {
+      const bool eps = a < eps_end[s];
+      if ((ilabel[a] == 0) != eps) return fail(-1, "arcs are not ilabel-sorted with epsilons first");
+      if (nextstate[a] < 0 || nextstate[a] >= num_states) return fail(-1, "nextstate out of range");
+      if (olabel[a] < 0 || ilabel[a] < 0) return fail(-1, "negative label");
+      arcs[a] = CtwArc{weight[a], nextstate[a], ilabel[a]};
+      max_il = std::max<int64_t>(max_il, ilabel[a]);
+      max_ol = std::max<int64_t>(max_ol, olabel[a]);
+    }
+  }
+  ctw_graph* g = new ctw_graph();
+  g->device = device;
+  g->S = num_states;
+  g->A = num_arcs;
+  g->start = start;
+  g->max_il = max_il;
+  g->max_ol = max_ol;
+  g->h_final.assign(final_w, final_w + num_states);
+  auto bail = [&](int code) {
+    ctw_graph_destroy(g);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(fail(-2, "cudaSetDevice failed"));
+  if (dalloc(&g->ranges, (size_t)num_states) || dalloc(&g->arcs, arcs.size()) ||
+      dalloc(&g->olabel, (size_t)std::max<int64_t>(num_arcs, 1)) || dalloc(&g->final_w, (size_t)num_states))
+    return bail(fail(-3, "graph allocation failed"));
+  if (cudaMemcpy(g->ranges, r.data(), r.size() * sizeof(CtwStateRange), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->arcs, arcs.data(), (size_t)num_arcs * sizeof(CtwArc), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->olabel, olabel, (size_t)num_arcs * sizeof(int32_t), cudaMemcpyHostToDevice) ||
+      cudaMemcpy(g->final_w, final_w, (size_t)num_states * sizeof(double), cudaMemcpyHostToDevice))
+    return bail(fail(-3, "graph upload failed"));
+  *out = g;
+  return 0;
+}
+
+void ctw_graph_destroy(ctw_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  dfree(g->ranges);
+  dfree(g->arcs);
+  dfree(g->olabel);
+  dfree(g->final_w);
+  delete g;
+}
+
+int ctw_graph_info(const ctw_graph* g, int64_t* num_states, int64_t* num_arcs, int64_t* max_ilabel,
+                   int64_t* max_olabel, int64_t* bytes) {
+  if (num_states) *num_states = g->S;
+  if (num_arcs) *num_arcs = g->A;
+  if (max_ilabel) *max_ilabel = g->max_il;
+  if (max_olabel) *max_olabel = g->max_ol;
+  if (bytes) *bytes = g->S * (int64_t)(sizeof(CtwStateRange) + sizeof(double)) + g->A * (int64_t)(sizeof(CtwArc) + 4);
+  return 0;
+}
+
+int ctw_lanes_create(ctw_graph* g, int32_t n_lanes, const ctw_config* cfg, void* stream, ctw_lanes** out) {
+  *out = nullptr;
+  if (!g) return fail(-1, "null graph");
+  if (n_lanes < 0) return fail(-1, "negative lane count");
+  if (!(cfg->beam > 0) || cfg->max_active < 1 || !(cfg->acoustic_scale > 0))
+    return fail(-1, "invalid decoder config");
+  CUDA_TRY(cudaSetDevice(g->device));
+  ctw_lanes* l = new ctw_lanes();
+  l->g = g;
+  l->cfg = *cfg;
+  l->dcfg = CtwDecodeCfg{cfg->beam, cfg->acoustic_scale, cfg->relax_eps, (long long)cfg->max_active,
+                         (long long)cfg->max_ne_iters};
+  if (stream) {
+    l->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete l;
+      return fail(-2, "stream creation failed");
+    }
+    l->own_stream = true;
+  }
+  cudaEventCreate(&l->ev0);
+  cudaEventCreate(&l->ev1);
+  if (int r = reserve_lanes(l, n_lanes)) {
+    ctw_lanes_destroy(l);
+    return r;
+  }
+  *out = l;
+  return 0;
+}
+
+void ctw_lanes_destroy(ctw_lanes* l) {
+  if (!l) return;
+  cudaSetDevice(l->g->device);
+  cudaStreamSynchronize(l->stream);
+  for (int i = 0; i < l->n; ++i) {
+    free_lane(l->h[i]);
+    dfree(l->boost_buf[i]);
+  }
+  if (l->h) cudaFreeHost(l->h);
+  dfree(l->d);
+  dfree(l->d_ids);
+  dfree(l->d_nframes);
+  dfree(l->d_lloff);
+  dfree(l->d_out);
+  dfree(l->d_stage);
+  dfree(l->d_words);
+  dfree(l->d_woff);
+  dfree(l->d_wcap);
+  dfree(l->d_nwords);
+  dfree(l->d_tcost);
+  dfree(l->d_bstatus);
+  for (void* p : {(void*)l->h_ids, (void*)l->h_nframes, (void*)l->h_lloff, (void*)l->h_out, (void*)l->h_woff,
+                  (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus})
+    if (p) cudaFreeHost(p);
+  if (l->ev0) cudaEventDestroy(l->ev0);
+  if (l->ev1) cudaEventDestroy(l->ev1);
+  if (l->own_stream) cudaStreamDestroy(l->stream);
+  delete l;
+}
+
+int ctw_lanes_reserve(ctw_lanes* l, int32_t n) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (int r = reserve_lanes(l, n)) return r;
+  return l->n;
+}
+
+int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const double* const* boosts,
+                   const int64_t* boost_lens, int32_t* status) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (int r = check_ids(l, lane_ids, n)) return r;
+  std::vector<int> ids(lane_ids, lane_ids + n);
+  for (int i = 0; i < n; ++i) {
+    const int lane = ids[i];
+    CtwLane& L = l->h[lane];
+    const double* b = boosts ? boosts[i] : nullptr;
+    if (b) {
+      const int64_t len = boost_lens[i];
+      if (len < l->g->max_ol + 1) return fail(-1, "boost vector shorter than max_olabel + 1");
+      if (l->boost_cap[lane] < len) {
+        dfree(l->boost_buf[lane]);
+        CUDA_TRY(dalloc(&l->boost_buf[lane], (size_t)len));
+        l->boost_cap[lane] = len;
+      }
+      CUDA_TRY(cudaMemcpyAsync(l->boost_buf[lane], b, (size_t)len * sizeof(double), cudaMemcpyHostToDevice,
+                               l->stream));
+      L.boost = l->boost_buf[lane];
+      L.boost_len = (int32_t)len;
+    } else {
+      L.boost = nullptr;
+      L.boost_len = 0;
+    }
+    L.n_src = 0;
+    L.src_buf = 0;
+    L.frame_count = 0;
+    L.pool_used = 0;
+    L.n_rec = 0;
+    L.pend_valid = 0;
+    if (int r = sync_lane(l, lane)) return r;
+  }
+  std::vector<int> st;
+  if (int r = run_seed(l, ids, st)) return r;
+  for (int i = 0; i < n; ++i) {
+    status[i] = st[i];
+    l->seeded[ids[i]] = st[i] == CTW_OK;
+  }
+  return 0;
+}
+
+int ctw_lane_set_boost(ctw_lanes* l, int32_t lane, const double* boost, int64_t boost_len) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (lane < 0 || lane >= l->n) return fail(-1, "lane id out of range");
+  CtwLane& L = l->h[lane];
+  if (boost) {
+    if (boost_len < l->g->max_ol + 1) return fail(-1, "boost vector shorter than max_olabel + 1");
+    if (l->boost_cap[lane] < boost_len) {
+      CUDA_TRY(cudaStreamSynchronize(l->stream));
+      dfree(l->boost_buf[lane]);
+      CUDA_TRY(dalloc(&l->boost_buf[lane], (size_t)boost_len));
+      l->boost_cap[lane] = boost_len;
+    }
+    CUDA_TRY(cudaMemcpyAsync(l->boost_buf[lane], boost, (size_t)boost_len * sizeof(double),
+                             cudaMemcpyHostToDevice, l->stream));
+    L.boost = l->boost_buf[lane];
+    L.boost_len = (int32_t)boost_len;
+  } else {
+    L.boost = nullptr;
+    L.boost_len = 0;
+  }
+  if (int r = sync_lane(l, lane)) return r;
+  CUDA_TRY(cudaStreamSynchronize(l->stream));
+  return 0;
+}
+
+int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
+                int32_t* status, int32_t* err_frame) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  ctw_graph* g = l->g;
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n <= 0) return 0;
+  if (int r = check_ids(l, lane_ids, n)) return r;
+  if (dtype != 0 && dtype != 1) return fail(-1, "dtype must be 0 (f32) or 1 (f64)");
+  if (width < g->max_il) return fail(-1, "frame width smaller than the graph's max input label");
+  const size_t esz = dtype ? 8 : 4;
+  for (int i = 0; i < n; ++i) {
+    if (!l->seeded[lane_ids[i]]) return fail(-1, "lane not seeded (call ctw_lane_reset first)");
+    if (frames[i] < 0) return fail(-1, "negative frame count");
+  }
+  // stage host rows into HBM (one copy when the chunks are contiguous)
+  const char* dev_ll = (const char*)loglik;
+  if (int r = ensure_scratch(l, n)) return r;
+  if (location == 0) {
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int i = 0; i < n; ++i) {
+      if (frames[i] == 0) continue;
+      lo = std::min<int64_t>(lo, ll_offsets[i]);
+      hi = std::max<int64_t>(hi, ll_offsets[i] + (int64_t)frames[i] * width);
+    }
+    if (lo == INT64_MAX) lo = hi = 0;
+    const size_t bytes = (size_t)(hi - lo) * esz;
+    if (bytes > l->stage_bytes) {
+      dfree(l->d_stage);
+      CUDA_TRY(dalloc(&l->d_stage, bytes + bytes / 4));
+      l->stage_bytes = bytes + bytes / 4;
+    }
+    if (bytes)
+      CUDA_TRY(cudaMemcpyAsync(l->d_stage, (const char*)loglik + lo * esz, bytes, cudaMemcpyHostToDevice,
+                               l->stream));
+    dev_ll = l->d_stage - lo * (int64_t)esz;
+  }
+  // pre-size per-lane frame / history capacity
+  for (int i = 0; i < n; ++i) {
+    const int lane = lane_ids[i];
+    CtwLane& L = l->h[lane];
+    if (int r = grow_frames(l, lane, (int64_t)L.frame_count + frames[i])) return r;
+    double est = l->surv_ema[lane];
+    if (est < 0) est = (double)std::min<int64_t>(l->cfg.max_active, 2048);
+    const int64_t need = L.n_rec + (int64_t)std::ceil(est * 1.25 * frames[i]) + 64;
+    if (need > L.rcap)
+      if (int r = grow_hist(l, lane, need)) return r;
+  }
+  std::vector<int> pos(l->n, -1);
+  for (int i = 0; i < n; ++i) pos[lane_ids[i]] = i;
+  std::vector<int> todo(lane_ids, lane_ids + n);
+  for (int round = 0; !todo.empty(); ++round) {
+    if (round > 60) return fail(-1, "advance: grow loop did not converge");
+    const int m = (int)todo.size();
+    for (int k = 0; k < m; ++k) {
+      const int i = pos[todo[k]];
+      l->h_ids[k] = todo[k];
+      l->h_nframes[k] = frames[i];
+      l->h_lloff[k] = (long long)ll_offsets[i];
+    }
+    CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(l->d_nframes, l->h_nframes, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(l->d_lloff, l->h_lloff, m * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
+    CUDA_TRY(cudaEventRecord(l->ev0, l->stream));
+    if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
+                          l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, l->stream))
+      return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
+    CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
+    l->launches++;
+    l->decode_launches++;
+    CUDA_TRY(cudaMemcpyAsync(l->h_out, l->d_out, m * sizeof(CtwLaneOut), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, l->ev0, l->ev1);
+    l->decode_ms += ms;
+    std::vector<int> again;
+    for (int k = 0; k < m; ++k) {
+      const int lane = todo[k];
+      const int i = pos[lane];
+      const CtwLaneOut& o = l->h_out[k];
+      CtwLane& L = l->h[lane];
+      l->max_slots = std::max<int64_t>(l->max_slots, o.n_slots_max);
+      if (o.status == CTW_GROW_TABLE) {
+        if (int r = alloc_table(l, lane, L.tlog2 + 1)) return r;
+        again.push_back(lane);
+      } else if (o.status == CTW_GROW_HIST) {
+        const int64_t per = (o.rec_need - L.n_rec) / std::max(1, o.err_frame + 1) + 1;
+        if (int r = grow_hist(l, lane, L.n_rec + (int64_t)(per * 1.5 * frames[i]) + 64)) return r;
+        again.push_back(lane);
+      } else if (o.status == CTW_GROW_POOL) {
+        if (int r = grow_pool(l, lane, 2 * (int64_t)L.pcap)) return r;
+        again.push_back(lane);
+      } else {
+        const int64_t before = L.n_rec;
+        update_from_out(L, o);
+        status[i] = o.status;
+        err_frame[i] = o.err_frame;
+        if (o.status == CTW_OK) {
+          l->arcs += o.arcs_expanded;
+          l->srcs += o.src_total;
+          l->frames += frames[i];
+          if (frames[i] > 0) {
+            const double per = (double)(L.n_rec - before) / frames[i];
+            l->surv_ema[lane] = l->surv_ema[lane] < 0 ? per : 0.5 * (l->surv_ema[lane] + per);
+          }
+        }
+      }
+    }
+    todo.swap(again);
+  }
+  return 0;
+}
+
+int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* words, int64_t words_cap,
+                  int64_t* word_off, double* total_cost, int64_t* frame_count, int32_t* status) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  ctw_graph* g = l->g;
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n <= 0) {
+    word_off[0] = 0;
+    return 0;
+  }
+  for (int i = 0; i < n; ++i)
+    if (lane_ids[i] < 0 || lane_ids[i] >= l->n) return fail(-1, "lane id out of range");
+  if (n > l->best_cap) {
+    const int c = std::max(n, 2 * l->best_cap);
+    dfree(l->d_woff);
+    dfree(l->d_wcap);
+    dfree(l->d_nwords);
+    dfree(l->d_tcost);
+    dfree(l->d_bstatus);
+    for (void* p : {(void*)l->h_woff, (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus})
+      if (p) cudaFreeHost(p);
+    CUDA_TRY(dalloc(&l->d_woff, c));
+    CUDA_TRY(dalloc(&l->d_wcap, c));
+    CUDA_TRY(dalloc(&l->d_nwords, c));
+    CUDA_TRY(dalloc(&l->d_tcost, c));
+    CUDA_TRY(dalloc(&l->d_bstatus, c));
+    CUDA_TRY(cudaMallocHost((void**)&l->h_woff, c * sizeof(long long)));
+    CUDA_TRY(cudaMallocHost((void**)&l->h_wcap, c * sizeof(int)));
+    CUDA_TRY(cudaMallocHost((void**)&l->h_nwords, c * sizeof(int)));
+    CUDA_TRY(cudaMallocHost((void**)&l->h_tcost, c * sizeof(double)));
+    CUDA_TRY(cudaMallocHost((void**)&l->h_bstatus, c * sizeof(int)));
+    l->best_cap = c;
+  }
+  if (int r = ensure_scratch(l, n)) return r;
+  // capacity guess: one word per frame is generous for word-level graphs
+  std::vector<int> caps(n);
+  for (int i = 0; i < n; ++i) caps[i] = l->h[lane_ids[i]].frame_count + 8;
+  for (int round = 0; round < 2; ++round) {
+    long long tot = 0;
+    for (int i = 0; i < n; ++i) {
+      l->h_woff[i] = tot;
+      l->h_wcap[i] = caps[i];
+      l->h_ids[i] = lane_ids[i];
+      tot += caps[i];
+    }
+    if ((size_t)tot > l->words_cap) {
+      dfree(l->d_words);
+      CUDA_TRY(dalloc(&l->d_words, (size_t)tot + tot / 2));
+      l->words_cap = (size_t)tot + tot / 2;
+    }
+    CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(l->d_woff, l->h_woff, n * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(l->d_wcap, l->h_wcap, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+    if (ctw_launch_best(l->d, g->ranges, g->arcs, g->olabel, g->final_w, l->d_ids, n, l->d_words, l->d_woff,
+                        l->d_wcap, l->d_nwords, l->d_tcost, l->d_bstatus, l->stream))
+      return fail(-1, std::string("best-path launch: ") + cudaGetErrorString(cudaGetLastError()));
+    l->launches++;
+    CUDA_TRY(cudaMemcpyAsync(l->h_nwords, l->d_nwords, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(l->h_tcost, l->d_tcost, n * sizeof(double), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(l->h_bstatus, l->d_bstatus, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    bool redo = false;
+    for (int i = 0; i < n; ++i)
+      if (l->h_nwords[i] > caps[i]) {
+        caps[i] = l->h_nwords[i];
+        redo = true;
+      }
+    if (!redo) break;
+  }
+  int64_t need = 0;
+  for (int i = 0; i < n; ++i) {
+    const CtwLane& L = l->h[lane_ids[i]];
+    word_off[i] = need;
+    frame_count[i] = L.frame_count;
+    if (L.frame_count == 0) {
+      status[i] = 2;
+      total_cost[i] = INFINITY;
+      continue;
+    }
+    status[i] = l->h_bstatus[i];
+    total_cost[i] = l->h_tcost[i];
+    if (status[i] == 0) need += l->h_nwords[i];
+  }
+  word_off[n] = need;
+  if (need > words_cap) return -2;
+  for (int i = 0; i < n; ++i) {
+    if (status[i] != 0 || l->h_nwords[i] == 0) continue;
+    CUDA_TRY(cudaMemcpyAsync(words + word_off[i], l->d_words + l->h_woff[i], l->h_nwords[i] * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, l->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(l->stream));
+  return 0;
+}
+
+int ctw_lane_info(ctw_lanes* l, int32_t lane, int64_t* frame_count, int64_t* n_tokens, int64_t* n_records) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  if (lane < 0 || lane >= l->n) return fail(-1, "lane id out of range");
+  const CtwLane& L = l->h[lane];
+  if (frame_count) *frame_count = L.frame_count;
+  if (n_tokens) *n_tokens = L.n_src;
+  if (n_records) *n_records = L.n_rec;
+  return 0;
+}
+
+void ctw_export_free(ctw_export* e) {
+  if (!e) return;
+  free(e->counts);
+  free(e->rec_prev);
+  free(e->rec_state);
+  free(e->rec_cost);
+  free(e->rec_olab_off);
+  free(e->rec_olab_pool);
+  free(e->tok_state);
+  free(e->tok_cost);
+  free(e->tok_bp);
+  free(e->tok_chain_off);
+  free(e->tok_chain_pool);
+  std::memset(e, 0, sizeof(*e));
+}
+
+}  // extern "C"
+
+namespace {
+template <class T>
+T* cmalloc(size_t n) {
+  return (T*)malloc(std::max<size_t>(n, 1) * sizeof(T));
+}
+
+void expand_code(const std::vector<int32_t>& pool, int32_t code, std::vector<int32_t>& out) {
+  if (code > 0) out.push_back(code);
+  else if (code < 0) {
+    const int64_t off = -(int64_t)code - 1;
+    const int32_t m = pool[off];
+    for (int32_t j = 0; j < m; ++j) out.push_back(pool[off + 1 + j]);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ctw_lane_export(ctw_lanes* l, int32_t lane, int64_t frame_from, int64_t base, const int64_t* ext_bp,
+                    int64_t n_ext, ctw_export* out) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  std::memset(out, 0, sizeof(*out));
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (lane < 0 || lane >= l->n) return fail(-1, "lane id out of range");
+  const CtwLane& L = l->h[lane];
+  const int64_t F = L.frame_count, R = L.n_rec;
+  if (frame_from < 0 || frame_from > F) return fail(-1, "frame_from out of range");
+  std::vector<int64_t> fb((size_t)F);
+  std::vector<int2> link((size_t)R);
+  std::vector<int32_t> st((size_t)R), pool((size_t)L.pool_used);
+  std::vector<double> cost((size_t)R);
+  std::vector<CtwSrc> src((size_t)L.n_src);
+  std::vector<int32_t> pend((size_t)(L.pend_valid ? L.n_src : 0));
+  if (F) CUDA_TRY(cudaMemcpyAsync(fb.data(), L.frame_base, F * 8, cudaMemcpyDeviceToHost, l->stream));
+  if (R) {
+    CUDA_TRY(cudaMemcpyAsync(link.data(), L.rec_link, R * sizeof(int2), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(st.data(), L.rec_state, R * 4, cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(cost.data(), L.rec_cost, R * 8, cudaMemcpyDeviceToHost, l->stream));
+  }
+  if (L.pool_used)
+    CUDA_TRY(cudaMemcpyAsync(pool.data(), L.pool, L.pool_used * 4, cudaMemcpyDeviceToHost, l->stream));
+  if (L.n_src)
+    CUDA_TRY(cudaMemcpyAsync(src.data(), L.src[L.src_buf], L.n_src * sizeof(CtwSrc), cudaMemcpyDeviceToHost,
+                             l->stream));
+  if (!pend.empty())
+    CUDA_TRY(cudaMemcpyAsync(pend.data(), L.pend, pend.size() * 4, cudaMemcpyDeviceToHost, l->stream));
+  CUDA_TRY(cudaStreamSynchronize(l->stream));
+  // per frame: order by state; global index = base + rank
+  std::vector<int64_t> gidx((size_t)R);
+  std::vector<int64_t> order;
+  order.reserve((size_t)R);
+  for (int64_t f = 0; f < F; ++f) {
+    const int64_t b = fb[f], e = (f + 1 < F) ? fb[f + 1] : R;
+    const size_t o0 = order.size();
+    for (int64_t r = b; r < e; ++r) order.push_back(r);
+    std::sort(order.begin() + o0, order.end(), [&](int64_t x, int64_t y) { return st[x] < st[y]; });
+    for (size_t k = o0; k < order.size(); ++k) gidx[order[k]] = base + (int64_t)k;
+  }
+  auto map_prev = [&](int32_t p) -> int64_t {
+    if (p >= 0) return gidx[p];
+    if (p == -1) return -1;
+    const int64_t x = -2 - (int64_t)p;
+    return (ext_bp && x < n_ext) ? ext_bp[x] : -1;
+  };
+  const int64_t r0 = frame_from < F ? fb[frame_from] : R;
+  const int64_t nr = R - r0;
+  out->n_frames = F - frame_from;
+  out->n_records = nr;
+  out->counts = cmalloc<int64_t>(out->n_frames);
+  for (int64_t f = frame_from; f < F; ++f) out->counts[f - frame_from] = ((f + 1 < F) ? fb[f + 1] : R) - fb[f];
+  out->rec_prev = cmalloc<int64_t>(nr);
+  out->rec_state = cmalloc<int32_t>(nr);
+  out->rec_cost = cmalloc<double>(nr);
+  out->rec_olab_off = cmalloc<int64_t>(nr + 1);
+  std::vector<int32_t> labs;
+  out->rec_olab_off[0] = 0;
+  for (int64_t k = 0; k < nr; ++k) {
+    const int64_t r = order[(size_t)(r0 + k)];
+    out->rec_prev[k] = map_prev(link[r].x);
+    out->rec_state[k] = st[r];
+    out->rec_cost[k] = cost[r];
+    expand_code(pool, link[r].y, labs);
+    out->rec_olab_off[k + 1] = (int64_t)labs.size();
+  }
+  out->n_olab = (int64_t)labs.size();
+  out->rec_olab_pool = cmalloc<int32_t>(labs.size());
+  std::copy(labs.begin(), labs.end(), out->rec_olab_pool);
+  // active tokens, state-ascending
+  std::vector<int64_t> to((size_t)L.n_src);
+  std::iota(to.begin(), to.end(), 0);
+  std::sort(to.begin(), to.end(), [&](int64_t x, int64_t y) { return src[x].state < src[y].state; });
+  out->n_tok = L.n_src;
+  out->tok_state = cmalloc<int32_t>(L.n_src);
+  out->tok_cost = cmalloc<double>(L.n_src);
+  out->tok_bp = cmalloc<int64_t>(L.n_src);
+  out->tok_chain_off = cmalloc<int64_t>(L.n_src + 1);
+  std::vector<int32_t> ch;
+  out->tok_chain_off[0] = 0;
+  for (int64_t k = 0; k < L.n_src; ++k) {
+    const CtwSrc& t = src[to[k]];
+    out->tok_state[k] = t.state;
+    out->tok_cost[k] = t.cost;
+    out->tok_bp[k] = map_prev(t.bp);
+    if (!pend.empty()) expand_code(pool, pend[to[k]], ch);
+    out->tok_chain_off[k + 1] = (int64_t)ch.size();
+  }
+  out->n_chain = (int64_t)ch.size();
+  out->tok_chain_pool = cmalloc<int32_t>(ch.size());
+  std::copy(ch.begin(), ch.end(), out->tok_chain_pool);
+  return 0;
+}
+
+int ctw_lanes_stats(ctw_lanes* l, int64_t* launches, int64_t* decode_launches, double* decode_ms, int64_t* arcs,
+                    int64_t* src_tokens, int64_t* frames, int64_t* max_slots) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  if (launches) *launches = l->launches;
+  if (decode_launches) *decode_launches = l->decode_launches;
+  if (decode_ms) *decode_ms = l->decode_ms;
+  if (arcs) *arcs = l->arcs;
+  if (src_tokens) *src_tokens = l->srcs;
+  if (frames) *frames = l->frames;
+  if (max_slots) *max_slots = l->max_slots;
+  return 0;
+}
+
+int ctw_lanes_reset_stats(ctw_lanes* l) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  l->launches = l->decode_launches = l->arcs = l->srcs = l->frames = l->max_slots = 0;
+  l->decode_ms = 0.0;
+  return 0;
+}
+
+void* ctw_lanes_stream(ctw_lanes* l) { return (void*)l->stream; }
+
+// ------------------------------------------------------------- compat ----
+}  // extern "C"
+
+namespace {
+struct CompatCache {
+  uint64_t hash = 0;
+  int64_t S = -1, A = -1;
+  int device = -1;
+  ctw_graph* g = nullptr;
+  ctw_lanes* l = nullptr;
+};
+std::mutex g_compat_mu;
+CompatCache g_compat;
+
+uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const unsigned char* c = (const unsigned char*)p;
+  for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  return h;
+}
+}  // namespace
+
+extern "C" {
+
+int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const int32_t* ilabel,
+                             const int32_t* olabel, const double* weight, const int32_t* nextstate,
+                             int64_t num_states, int64_t num_arcs, const int32_t* act_state,
+                             const double* act_cost, const int64_t* act_bp, const int64_t* act_chain_off,
+                             const int32_t* act_chain_pool, int64_t n_src, const double* loglik,
+                             int64_t num_frames, int64_t width, double acoustic_scale, double beam,
+                             int64_t max_active, double relax_eps, int64_t max_ne_iters, const double* boost,
+                             int64_t boost_len, int64_t base, int32_t device, int64_t* err_frame,
+                             ctw_export* out) {
+  std::lock_guard<std::mutex> lk(g_compat_mu);
+  std::memset(out, 0, sizeof(*out));
+  *err_frame = -1;
+  // the reference kernel derives finals nowhere; use +inf (best path is not part of the contract)
+  uint64_t h = 1469598103934665603ull;
+  h = fnv(h, off, (size_t)(num_states + 1) * 8);
+  h = fnv(h, eps_end, (size_t)num_states * 8);
+  h = fnv(h, ilabel, (size_t)num_arcs * 4);
+  h = fnv(h, olabel, (size_t)num_arcs * 4);
+  h = fnv(h, weight, (size_t)num_arcs * 8);
+  h = fnv(h, nextstate, (size_t)num_arcs * 4);
+  CompatCache& c = g_compat;
+  if (!(c.g && c.hash == h && c.S == num_states && c.A == num_arcs && c.device == device)) {
+    if (c.l) ctw_lanes_destroy(c.l);
+    if (c.g) ctw_graph_destroy(c.g);
+    c = CompatCache();
+    std::vector<double> fin((size_t)num_states, INFINITY);
+    if (int r = ctw_graph_create(off, eps_end, ilabel, olabel, weight, nextstate, fin.data(), num_states, num_arcs,
+                                 0, device, &c.g))
+      return r;
+    ctw_config cfg{beam, max_active, acoustic_scale, relax_eps, max_ne_iters};
+    if (int r = ctw_lanes_create(c.g, 1, &cfg, nullptr, &c.l)) return r;
+    c.hash = h;
+    c.S = num_states;
+    c.A = num_arcs;
+    c.device = device;
+  }
+  ctw_lanes* l = c.l;
+  if (!(beam > 0) || max_active < 1 || !(acoustic_scale > 0)) return fail(-1, "invalid decoder config");
+  l->cfg = ctw_config{beam, max_active, acoustic_scale, relax_eps, max_ne_iters};
+  l->dcfg = CtwDecodeCfg{beam, acoustic_scale, relax_eps, (long long)max_active, (long long)max_ne_iters};
+  CUDA_TRY(cudaSetDevice(device));
+  CtwLane& L = l->h[0];
+  // table must hold the external sources
+  while ((int64_t)((1ull << L.tlog2) / 2) < n_src)
+    if (int r = alloc_table(l, 0, L.tlog2 + 1)) return r;
+  if (boost && boost_len < c.g->max_ol + 1) return fail(-1, "boost vector shorter than max_olabel + 1");
+  // load sources (bp = -2 - i refers back to act_bp[i]) and their pending chains
+  std::vector<CtwSrc> srcs((size_t)n_src);
+  std::vector<int32_t> pend((size_t)n_src, 0), pool;
+  bool any_pend = false;
+  for (int64_t i = 0; i < n_src; ++i) {
+    srcs[i] = CtwSrc{act_state[i], (int32_t)(-2 - i), act_cost[i]};
+    const int64_t a0 = act_chain_off[i], a1 = act_chain_off[i + 1];
+    if (a1 - a0 == 1) pend[i] = act_chain_pool[a0];
+    else if (a1 - a0 > 1) {
+      pend[i] = -(int32_t)pool.size() - 1;
+      pool.push_back((int32_t)(a1 - a0));
+      for (int64_t k = a0; k < a1; ++k) pool.push_back(act_chain_pool[k]);
+    }
+    any_pend |= a1 > a0;
+    if (act_state[i] < 0 || act_state[i] >= num_states) return fail(-1, "active state out of range");
+  }
+  if (int r = grow_pool(l, 0, (int64_t)pool.size() + 1)) return r;
+  if (n_src) {
+    CUDA_TRY(cudaMemcpyAsync(L.src[0], srcs.data(), n_src * sizeof(CtwSrc), cudaMemcpyHostToDevice, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(L.pend, pend.data(), n_src * 4, cudaMemcpyHostToDevice, l->stream));
+  }
+  if (!pool.empty())
+    CUDA_TRY(cudaMemcpyAsync(L.pool, pool.data(), pool.size() * 4, cudaMemcpyHostToDevice, l->stream));
+  double* dboost = nullptr;
+  if (boost) {
+    if (l->boost_cap[0] < boost_len) {
+      dfree(l->boost_buf[0]);
+      CUDA_TRY(dalloc(&l->boost_buf[0], (size_t)boost_len));
+      l->boost_cap[0] = boost_len;
+    }
+    CUDA_TRY(cudaMemcpyAsync(l->boost_buf[0], boost, boost_len * 8, cudaMemcpyHostToDevice, l->stream));
+    dboost = l->boost_buf[0];
+  }
+  auto load_state = [&]() -> int {
+    L.n_src = (int32_t)n_src;
+    L.src_buf = 0;
+    L.frame_count = 0;
+    L.pool_used = (int32_t)pool.size();
+    L.n_rec = 0;
+    L.pend_valid = any_pend ? 1 : 0;
+    L.boost = dboost;
+    L.boost_len = (int32_t)boost_len;
+    l->seeded[0] = 1;
+    return sync_lane(l, 0);
+  };
+  if (int r = load_state()) return r;
+  int32_t lane = 0, st = 0, ef = -1;
+  const int64_t zero = 0;
+  int32_t nf = (int32_t)num_frames;
+  if (num_frames > 0) {
+    if (int r = ctw_advance(l, &lane, 1, loglik, 1, 0, &zero, &nf, (int32_t)width, &st, &ef)) return r;
+    if (st != CTW_OK && ef > 0) {
+      // the contract returns the frames completed before the failure: redo them
+      if (int r = load_state()) return r;
+      int32_t st2 = 0, ef2 = -1, nf2 = ef;
+      if (int r = ctw_advance(l, &lane, 1, loglik, 1, 0, &zero, &nf2, (int32_t)width, &st2, &ef2)) return r;
+      if (st2 != CTW_OK) return fail(-1, "compat: replay of completed frames failed");
+    }
+  }
+  *err_frame = (st == CTW_OK) ? -1 : ef;
+  if (st == CTW_OK || ef > 0) {
+    if (int r = ctw_lane_export(l, 0, 0, base, act_bp, n_src, out)) return r;
+  } else {
+    out->counts = cmalloc<int64_t>(0);
+    out->rec_prev = cmalloc<int64_t>(0);
+    out->rec_state = cmalloc<int32_t>(0);
+    out->rec_cost = cmalloc<double>(0);
+    out->rec_olab_off = cmalloc<int64_t>(1);
+    out->rec_olab_off[0] = 0;
+    out->rec_olab_pool = cmalloc<int32_t>(0);
+  }
+  // leave the cached lane empty of history
+  L.n_rec = 0;
+  L.frame_count = 0;
+  return st;
+}
+
+}  // extern "C"

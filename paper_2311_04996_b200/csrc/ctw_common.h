@@ -1,0 +1,111 @@
+// ctw_common.h -- data layout shared by the host C-ABI layer and the sm_100a
+// kernels of the batched WFST beam-search decoder.
+//
+// Reference being replaced: the per-channel frame kernel
+// /root/reference/pkg/src/ctcwfst/_kernel.pyx:115-502 (== _pykernel.py:28-248)
+// and the CSR graph view decoder.py:70-127. See DESIGN.md for the layout
+// rationale and the per-unit byte counts used by the roofline.
+#pragma once
+#include <stdint.h>
+
+// Kernel/lane status words. 0..2 mirror the reference codes
+// (_pykernel.py:22-25); 3 mirrors C_ERR_OOM (_kernel.pyx:22). 16..18 are
+// internal "grow and re-run the chunk" requests handled by the host layer.
+enum {
+  CTW_OK = 0,
+  CTW_ERR_EPS_ITERS = 1,
+  CTW_ERR_NO_SURVIVORS = 2,
+  CTW_ERR_OOM = 3,
+  CTW_GROW_TABLE = 16,
+  CTW_GROW_HIST = 17,
+  CTW_GROW_POOL = 18,
+};
+
+// Per-state arc ranges (16 B, one vector load): epsilon arcs occupy
+// [eps_beg, emit_beg), emitting arcs [emit_beg, emit_end) -- the
+// FlatGraph invariant of decoder.py:108-116.
+struct __align__(16) CtwStateRange {
+  uint32_t eps_beg, emit_beg, emit_end, pad;
+};
+
+// One arc (16 B, one vector load). Output labels live in a separate int32
+// array: they are read only for winners (records) and when a boost vector is
+// attached.
+struct __align__(16) CtwArc {
+  double weight;
+  int32_t nextstate;
+  int32_t ilabel;
+};
+
+// Token-table entry (32 B = one L2 sector). `key`+`tb` are updated together
+// by a 128-bit CAS; `key` is the order-preserving bit pattern of the f64 cost
+// and `tb` the tie-break: the winning arc index (emitting arcs) or
+// EPS_BIT|arc (epsilon arcs, which lose exact ties to emitting winners as in
+// the reference's strict '<', _kernel.pyx:273/:332). `aux` is the source
+// token index (emitting winner) or the predecessor state (epsilon winner).
+struct __align__(32) CtwTok {
+  unsigned long long key;
+  uint32_t tb;
+  uint32_t aux;
+  uint32_t state;  // hash key; CTW_EMPTY when free
+  uint32_t stamp;  // epsilon-frontier dedupe epoch
+  uint32_t pad0, pad1;
+};
+
+#define CTW_EMPTY 0xFFFFFFFFu
+#define CTW_EPS_BIT 0x80000000u
+#define CTW_SEED_TB 0x7FFFFFFFu
+
+// Active token (16 B): the frame's sources / survivors.
+struct __align__(16) CtwSrc {
+  int32_t state;
+  int32_t bp;  // record index in this lane's history, -1 root, <= -2: external (compat)
+  double cost;
+};
+
+// Device-side descriptor of one lane (= one decoding channel). The host owns
+// the authoritative copy; kernels read it and write the committed fields back.
+struct CtwLane {
+  // token hash table: capacity 1 << tlog2
+  CtwTok* table;
+  uint32_t* slots;   // [tcap]  table index of each slot, discovery order
+  uint32_t* front;   // [2 * tcap] epsilon frontier ping-pong
+  CtwSrc* src[3];    // [tcap/2 + 1] each: committed + two working buffers
+  int32_t* pend;     // [tcap/2 + 1] pending olabel segment of seeded sources
+  int2* rec_link;    // [rcap] {prev record, olabel code}
+  int32_t* rec_state;
+  double* rec_cost;
+  int64_t* frame_base;  // [fcap] first record of each frame
+  int32_t* pool;        // [pcap] multi-label olabel segments: [n, l1..ln]
+  const double* boost;  // dense f64[boost_len] or null
+  uint32_t tlog2;
+  int32_t boost_len;
+  int64_t rcap;
+  int32_t fcap, pcap;
+  // committed channel state
+  int32_t n_src, src_buf, frame_count, pool_used;
+  int64_t n_rec;
+  int32_t pend_valid;  // committed sources carry pending olabel chains
+  int32_t pad;
+};
+
+// Per-launch result of one lane.
+struct CtwLaneOut {
+  int32_t status;
+  int32_t err_frame;   // chunk-relative
+  int32_t n_src, src_buf, frame_count, pool_used;
+  int64_t n_rec;
+  int32_t pend_valid;
+  int32_t n_slots_max;  // diagnostics: max slots seen in a frame
+  int64_t arcs_expanded;  // diagnostics: emitting arcs relaxed (E_emit)
+  int64_t src_total;      // diagnostics: sum of sources over frames (N_src)
+  int64_t rec_need;       // CTW_GROW_HIST: records needed through the failing frame
+};
+
+struct CtwDecodeCfg {
+  double beam;
+  double acoustic_scale;
+  double relax_eps;
+  long long max_active;
+  long long max_ne_iters;
+};

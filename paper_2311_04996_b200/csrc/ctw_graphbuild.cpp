@@ -1,0 +1,244 @@
+// ctw_graphbuild.cpp -- native offline graph construction for the synthetic
+// benchmark graphs: composition, trim and arc sort over CSR-form FSTs.
+//
+// Off the decode path (the reference builds graphs offline in pure Python,
+// pkg/src/ctcwfst/wfst.py:294-410 + graph.py:9-17, which takes ~35 s per
+// 2.5M arcs). Semantics follow the reference exactly so a TLG built here is
+// state-for-state identical to build_tlg's output for the same T, L, G
+// (pinned by tests/test_graphbuild.py):
+//   compose  wfst.py:307-366  BFS state numbering from the start pair; per
+//            state: a's arcs in order (eps-output arcs advance a alone,
+//            otherwise matched with b's arcs of that input label in b's
+//            order), then b's eps-input arcs advance b alone
+//   connect  wfst.py:369-410  accessible (DFS) & coaccessible, ids kept in
+//            increasing old order
+//   arc_sort wfst.py:294-304  stable by ilabel
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <unordered_map>
+#include <vector>
+
+extern "C" {
+
+typedef struct {
+  int64_t num_states, num_arcs, start;
+  int64_t* off;  // [num_states + 1]
+  int32_t* ilabel;
+  int32_t* olabel;
+  double* weight;
+  int32_t* nextstate;
+  double* final_w;  // +inf = non-final
+} ctw_fst;
+
+void ctw_fst_free(ctw_fst* f) {
+  if (!f) return;
+  free(f->off);
+  free(f->ilabel);
+  free(f->olabel);
+  free(f->weight);
+  free(f->nextstate);
+  free(f->final_w);
+  std::memset(f, 0, sizeof(*f));
+}
+}
+
+namespace {
+
+struct Arcs {
+  std::vector<int64_t> src;
+  std::vector<int32_t> il, ol, ns;
+  std::vector<double> w;
+  void add(int64_t s, int32_t i, int32_t o, double wt, int32_t n) {
+    src.push_back(s);
+    il.push_back(i);
+    ol.push_back(o);
+    w.push_back(wt);
+    ns.push_back(n);
+  }
+};
+
+template <class T>
+T* dup(const std::vector<T>& v) {
+  T* p = (T*)malloc(std::max<size_t>(v.size(), 1) * sizeof(T));
+  if (!v.empty()) std::memcpy(p, v.data(), v.size() * sizeof(T));
+  return p;
+}
+
+// arcs are appended grouped by source state in increasing order
+void emit(ctw_fst* out, int64_t n, int64_t start, const Arcs& a, const std::vector<double>& fin) {
+  std::vector<int64_t> off(n + 1, 0);
+  for (int64_t s : a.src) off[s + 1]++;
+  for (int64_t s = 0; s < n; ++s) off[s + 1] += off[s];
+  out->num_states = n;
+  out->num_arcs = (int64_t)a.il.size();
+  out->start = start;
+  out->off = dup(off);
+  out->ilabel = dup(a.il);
+  out->olabel = dup(a.ol);
+  out->weight = dup(a.w);
+  out->nextstate = dup(a.ns);
+  out->final_w = dup(fin);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctw_fst_compose(const ctw_fst* a, const ctw_fst* b, ctw_fst* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (a->num_states == 0 || b->num_states == 0) {
+    emit(out, 0, -1, Arcs(), {});
+    return 0;
+  }
+  // b's arcs grouped by (state, ilabel), preserving order
+  std::vector<int64_t> border;  // arc indices of b sorted by (state, ilabel) stably
+  border.resize((size_t)b->num_arcs);
+  std::iota(border.begin(), border.end(), 0);
+  std::vector<int64_t> bsrc((size_t)b->num_arcs);
+  for (int64_t s = 0; s < b->num_states; ++s)
+    for (int64_t k = b->off[s]; k < b->off[s + 1]; ++k) bsrc[k] = s;
+  std::stable_sort(border.begin(), border.end(), [&](int64_t x, int64_t y) {
+    if (bsrc[x] != bsrc[y]) return bsrc[x] < bsrc[y];
+    return b->ilabel[x] < b->ilabel[y];
+  });
+  auto brange = [&](int64_t qb, int32_t lab, int64_t& lo, int64_t& hi) {
+    // within [off[qb], off[qb+1]) positions of border, find ilabel == lab
+    const int64_t* beg = border.data() + b->off[qb];
+    const int64_t* end = border.data() + b->off[qb + 1];
+    auto cmp1 = [&](int64_t x, int32_t v) { return b->ilabel[x] < v; };
+    auto cmp2 = [&](int32_t v, int64_t x) { return v < b->ilabel[x]; };
+    lo = std::lower_bound(beg, end, lab, cmp1) - border.data();
+    hi = std::upper_bound(beg, end, lab, cmp2) - border.data();
+  };
+  std::unordered_map<uint64_t, int32_t> ids;
+  ids.reserve(1 << 20);
+  std::vector<std::pair<int32_t, int32_t>> queue;
+  auto state_of = [&](int64_t qa, int64_t qb) -> int32_t {
+    const uint64_t key = ((uint64_t)qa << 32) | (uint64_t)qb;
+    auto it = ids.find(key);
+    if (it != ids.end()) return it->second;
+    const int32_t id = (int32_t)queue.size();
+    ids.emplace(key, id);
+    queue.emplace_back((int32_t)qa, (int32_t)qb);
+    return id;
+  };
+  state_of(a->start, b->start);
+  Arcs arcs;
+  std::vector<double> fin;
+  for (size_t head = 0; head < queue.size(); ++head) {
+    const int64_t qa = queue[head].first, qb = queue[head].second;
+    const int64_t src = (int64_t)head;
+    const double fa = a->final_w[qa], fb = b->final_w[qb];
+    fin.push_back((std::isfinite(fa) && std::isfinite(fb)) ? fa + fb : INFINITY);
+    for (int64_t k = a->off[qa]; k < a->off[qa + 1]; ++k) {
+      if (a->olabel[k] == 0) {
+        const int32_t d = state_of(a->nextstate[k], qb);
+        arcs.add(src, a->ilabel[k], 0, a->weight[k], d);
+      } else {
+        int64_t lo, hi;
+        brange(qb, a->olabel[k], lo, hi);
+        for (int64_t p = lo; p < hi; ++p) {
+          const int64_t j = border[p];
+          const int32_t d = state_of(a->nextstate[k], b->nextstate[j]);
+          arcs.add(src, a->ilabel[k], b->olabel[j], a->weight[k] + b->weight[j], d);
+        }
+      }
+    }
+    int64_t lo, hi;
+    brange(qb, 0, lo, hi);
+    for (int64_t p = lo; p < hi; ++p) {
+      const int64_t j = border[p];
+      const int32_t d = state_of(qa, b->nextstate[j]);
+      arcs.add(src, 0, b->olabel[j], b->weight[j], d);
+    }
+  }
+  emit(out, (int64_t)queue.size(), 0, arcs, fin);
+  return 0;
+}
+
+int ctw_fst_connect(const ctw_fst* g, ctw_fst* out) {
+  std::memset(out, 0, sizeof(*out));
+  const int64_t n = g->num_states;
+  if (n == 0 || g->start < 0) {
+    emit(out, 0, -1, Arcs(), {});
+    return 0;
+  }
+  std::vector<char> acc(n, 0), coacc(n, 0);
+  std::vector<int64_t> stack{g->start};
+  acc[g->start] = 1;
+  while (!stack.empty()) {
+    const int64_t s = stack.back();
+    stack.pop_back();
+    for (int64_t k = g->off[s]; k < g->off[s + 1]; ++k) {
+      const int32_t d = g->nextstate[k];
+      if (!acc[d]) {
+        acc[d] = 1;
+        stack.push_back(d);
+      }
+    }
+  }
+  // reverse adjacency (CSR)
+  std::vector<int64_t> roff(n + 1, 0);
+  for (int64_t k = 0; k < g->num_arcs; ++k) roff[g->nextstate[k] + 1]++;
+  for (int64_t s = 0; s < n; ++s) roff[s + 1] += roff[s];
+  std::vector<int64_t> rsrc((size_t)g->num_arcs), fillp(roff.begin(), roff.end() - 1);
+  for (int64_t s = 0; s < n; ++s)
+    for (int64_t k = g->off[s]; k < g->off[s + 1]; ++k) rsrc[fillp[g->nextstate[k]]++] = s;
+  for (int64_t s = 0; s < n; ++s)
+    if (acc[s] && std::isfinite(g->final_w[s])) {
+      coacc[s] = 1;
+      stack.push_back(s);
+    }
+  while (!stack.empty()) {
+    const int64_t s = stack.back();
+    stack.pop_back();
+    for (int64_t k = roff[s]; k < roff[s + 1]; ++k) {
+      const int64_t p = rsrc[k];
+      if (!coacc[p]) {
+        coacc[p] = 1;
+        stack.push_back(p);
+      }
+    }
+  }
+  if (!coacc[g->start]) {
+    emit(out, 0, -1, Arcs(), {});
+    return 0;
+  }
+  std::vector<int32_t> remap(n, -1);
+  int32_t m = 0;
+  for (int64_t s = 0; s < n; ++s)
+    if (acc[s] && coacc[s]) remap[s] = m++;
+  Arcs arcs;
+  std::vector<double> fin(m, INFINITY);
+  for (int64_t s = 0; s < n; ++s) {
+    if (remap[s] < 0) continue;
+    for (int64_t k = g->off[s]; k < g->off[s + 1]; ++k) {
+      const int32_t d = remap[g->nextstate[k]];
+      if (d >= 0) arcs.add(remap[s], g->ilabel[k], g->olabel[k], g->weight[k], d);
+    }
+    fin[remap[s]] = g->final_w[s];
+  }
+  emit(out, m, remap[g->start], arcs, fin);
+  return 0;
+}
+
+int ctw_fst_arcsort_ilabel(const ctw_fst* g, ctw_fst* out) {
+  std::memset(out, 0, sizeof(*out));
+  Arcs arcs;
+  std::vector<int64_t> idx;
+  for (int64_t s = 0; s < g->num_states; ++s) {
+    idx.resize((size_t)(g->off[s + 1] - g->off[s]));
+    std::iota(idx.begin(), idx.end(), g->off[s]);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t x, int64_t y) { return g->ilabel[x] < g->ilabel[y]; });
+    for (int64_t k : idx) arcs.add(s, g->ilabel[k], g->olabel[k], g->weight[k], g->nextstate[k]);
+  }
+  std::vector<double> fin(g->final_w, g->final_w + g->num_states);
+  emit(out, g->num_states, g->start, arcs, fin);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,857 @@
+// ctw_kernels.cu -- sm_100a kernels of the batched WFST beam-search decoder.
+//
+// One CTA owns one lane (= one decoding channel) for a whole chunk of frames
+// and loops over the frames itself: emitting expansion -> epsilon fixpoint ->
+// beam / max-active prune -> records + next sources -> table reset, with only
+// __syncthreads between stages. There is no host round trip and no grid-wide
+// sync inside a chunk; the batch of lanes is the grid.
+//
+// Reference semantics (all paths under /root/reference/pkg/src/ctcwfst/):
+//   expansion arithmetic  ((c + (-scale*ll[f, il-1])) + w) (+ boost[ol])
+//                                                       _kernel.pyx:249-253
+//   recombination: min cost per state, ties -> first arc in (source state,
+//     arc) order == lowest global CSR arc index          _kernel.pyx:243-285
+//   epsilon relaxation to a fixpoint, stop when improvements <= relax_eps,
+//     cap max_ne_iters passes -> ERR_EPS_ITERS           _kernel.pyx:292-355
+//   no slots -> ERR_NO_SURVIVORS; keep cost <= min+beam, then the
+//     max_active smallest (cost, state)                  _kernel.pyx:357-390
+//   records (prev, olabels oldest-first, state, cost)    _kernel.pyx:392-427
+//   seeding closure                                      decoder.py:173-229
+//   best-path token choice + backtrace                   decoder.py:377-415
+// See DESIGN.md for the deviations that are inherent to a parallel fixpoint
+// (exact epsilon ties and sub-relax_eps improvements; none observed in tests).
+#include <cuda_runtime.h>
+#include <cub/block/block_scan.cuh>
+#include <stdint.h>
+
+#include "ctw_common.h"
+
+#define CTW_BS 256
+#define CTW_MAX_SMEM_WIDTH 4096
+
+namespace {
+
+struct GraphDev {
+  const CtwStateRange* ranges;
+  const CtwArc* arcs;
+  const int32_t* olabel;
+  const double* final_w;
+};
+
+// ---------------------------------------------------------------- helpers --
+
+__device__ __forceinline__ unsigned long long d2key(double x) {
+  x = __dadd_rn(x, 0.0);  // -0.0 -> +0.0 (they compare equal in the reference)
+  long long b = __double_as_longlong(x);
+  return (unsigned long long)(b ^ ((b >> 63) | (long long)0x8000000000000000ULL));
+}
+
+__device__ __forceinline__ double key2d(unsigned long long k) {
+  long long b = (k & 0x8000000000000000ULL) ? (long long)(k ^ 0x8000000000000000ULL) : (long long)~k;
+  return __longlong_as_double(b);
+}
+
+__device__ __forceinline__ void cas128(void* addr, unsigned long long clo, unsigned long long chi,
+                                       unsigned long long nlo, unsigned long long nhi,
+                                       unsigned long long& olo, unsigned long long& ohi) {
+  asm volatile(
+      "{\n\t.reg .b128 c, n, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.relaxed.gpu.global.cas.b128 o, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(olo), "=l"(ohi)
+      : "l"(clo), "l"(chi), "l"(nlo), "l"(nhi), "l"(addr)
+      : "memory");
+}
+
+// An atomic 128-bit snapshot: CAS with a compare value no live entry can hold
+// (key 0 is the sortable image of a negative NaN, never stored).
+__device__ __forceinline__ void snap128(void* addr, unsigned long long& lo, unsigned long long& hi) {
+  cas128(addr, 0ULL, ~0ULL, 0ULL, ~0ULL, lo, hi);
+}
+
+__device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
+  return (s * 0x9E3779B1u) >> shift;
+}
+
+// Find-or-insert `d` in the lane's open-addressing table (linear probing).
+// Returns the table index or CTW_EMPTY when the table is full.
+__device__ __forceinline__ uint32_t tok_insert(CtwTok* T, uint32_t mask, uint32_t shift, uint32_t d,
+                                               bool& is_new) {
+  uint32_t h = tok_hash(d, shift);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    uint32_t k = __ldcg(&T[h].state);
+    if (k == d) return h;
+    if (k == CTW_EMPTY) {
+      uint32_t old = atomicCAS(&T[h].state, CTW_EMPTY, d);
+      if (old == CTW_EMPTY) {
+        is_new = true;
+        return h;
+      }
+      if (old == d) return h;
+    }
+    h = (h + 1) & mask;
+  }
+  return CTW_EMPTY;
+}
+
+__device__ __forceinline__ uint32_t tok_find(const CtwTok* T, uint32_t mask, uint32_t shift, uint32_t d) {
+  uint32_t h = tok_hash(d, shift);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    uint32_t k = __ldcg(&T[h].state);
+    if (k == d) return h;
+    if (k == CTW_EMPTY) return CTW_EMPTY;
+    h = (h + 1) & mask;
+  }
+  return CTW_EMPTY;
+}
+
+// Lexicographic (key, tb) atomic min on the entry's first 16 bytes. Returns
+// true when our value was installed; *old_key gets the replaced key.
+__device__ __forceinline__ bool tok_min(CtwTok* e, unsigned long long key, uint32_t tb, uint32_t aux,
+                                        unsigned long long* old_key) {
+  unsigned long long ck = __ldcg(&e->key);  // single-copy atomic 64-bit read
+  if (key > ck) return false;               // keys only decrease within a frame
+  unsigned long long clo, chi;
+  if (key == ck) {
+    snap128(e, clo, chi);  // exact tie: need an untorn tie-break
+  } else {
+    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(e));
+    clo = v.x;
+    chi = v.y;
+  }
+  const unsigned long long nhi = ((unsigned long long)aux << 32) | tb;
+  for (;;) {
+    if (key > clo || (key == clo && tb >= (uint32_t)chi)) return false;
+    unsigned long long olo, ohi;
+    cas128(e, clo, chi, key, nhi, olo, ohi);
+    if (olo == clo && ohi == chi) {
+      *old_key = clo;
+      return true;
+    }
+    clo = olo;
+    chi = ohi;
+  }
+}
+
+__device__ __forceinline__ void tok_clear(CtwTok* e) {
+  ulonglong2* p = reinterpret_cast<ulonglong2*>(e);
+  __stcg(p, make_ulonglong2(~0ULL, 0xFFFFFFFFULL));                                 // key, tb, aux=0
+  __stcg(p + 1, make_ulonglong2((unsigned long long)CTW_EMPTY, 0ULL));            // state, stamp=0
+}
+
+// --------------------------------------------------------- shared memory --
+
+struct __align__(16) Smem {
+  typedef cub::BlockScan<int, CTW_BS> Scan;
+  typename Scan::TempStorage scan;
+  int off[CTW_BS];
+  uint32_t beg[CTW_BS];
+  double cost[CTW_BS];
+  uint32_t hist[256];
+  unsigned long long min_key;
+  unsigned long long sel_hi;  // radix-select prefix (cost-key digits)
+  uint32_t sel_lo;            // radix-select prefix (state digits)
+  int sel_depth;              // digits fixed; survivor iff top digits <= prefix
+  int sel_need;
+  int sel_done;
+  int n_slots;
+  int n_next;
+  int status;
+  int cnt;
+  int pool_used;
+  int hop_fail;
+  unsigned long long arcs;
+};
+
+struct LaneCtx {
+  CtwTok* T;
+  uint32_t mask, shift, tcap;
+  uint32_t* slots;
+  int pool_cap;
+  int32_t* pool;
+};
+
+// Append a newly inserted table index to the slot list (always, so the table
+// can be reset even on overflow); request a bigger table past half load.
+__device__ __forceinline__ void slot_append(Smem& sm, const LaneCtx& L, uint32_t h) {
+  int s = atomicAdd(&sm.n_slots, 1);
+  if ((uint32_t)s < L.tcap) L.slots[s] = h;
+  if ((uint32_t)s >= (L.tcap >> 1)) atomicMax(&sm.status, CTW_GROW_TABLE);
+}
+
+// ------------------------------------------------------- epsilon fixpoint --
+
+// Parallel label-correcting fixpoint over epsilon arcs, frontier by frontier.
+// Frontier 0 = every slot in [0, n_slots) (all states reached this frame).
+// A state is re-queued when it is new or improved by more than relax_eps,
+// mirroring the Gauss-Seidel stop rule (_kernel.pyx:331, :346, :351).
+// Returns CTW_OK or CTW_ERR_EPS_ITERS (pass count > max_ne_iters).
+__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t* front,
+                            const double* boost, double relax_eps, long long max_ne_iters) {
+  const int tid = threadIdx.x;
+  const uint32_t* cur = L.slots;
+  int n_cur = sm.n_slots;
+  int which = 0;
+  long long iters = 0;
+  for (;;) {
+    ++iters;
+    if (iters > max_ne_iters) return CTW_ERR_EPS_ITERS;
+    if (tid == 0) sm.n_next = 0;
+    __syncthreads();
+    const uint32_t epoch = (uint32_t)iters;
+    uint32_t* nxt = front + (size_t)which * L.tcap;
+    for (int i = tid; i < n_cur; i += CTW_BS) {
+      const uint32_t h = cur[i];
+      const uint32_t s = __ldcg(&L.T[h].state);
+      const CtwStateRange r = g.ranges[s];
+      if (r.eps_beg == r.emit_beg) continue;
+      const unsigned long long k = __ldcg(&L.T[h].key);
+      const double c = key2d(k);
+      for (uint32_t a = r.eps_beg; a < r.emit_beg; ++a) {
+        const CtwArc arc = g.arcs[a];
+        double nc = __dadd_rn(c, arc.weight);
+        if (boost) {
+          const int32_t ol = g.olabel[a];
+          if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+        }
+        if (!(nc < __longlong_as_double(0x7FF0000000000000LL))) continue;
+        bool is_new = false;
+        const uint32_t d = tok_insert(L.T, L.mask, L.shift, (uint32_t)arc.nextstate, is_new);
+        if (d == CTW_EMPTY) {
+          atomicMax(&sm.status, CTW_GROW_TABLE);
+          continue;
+        }
+        if (is_new) slot_append(sm, L, d);
+        unsigned long long oldk;
+        if (tok_min(&L.T[d], d2key(nc), CTW_EPS_BIT | a, s, &oldk)) {
+          const bool push = is_new || oldk == ~0ULL || (key2d(oldk) - nc) > relax_eps;
+          if (push && atomicExch(&L.T[d].stamp, epoch) != epoch) {
+            int p = atomicAdd(&sm.n_next, 1);
+            if ((uint32_t)p < L.tcap) nxt[p] = d;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int n_next = sm.n_next;
+    if (sm.status >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
+    if (n_next == 0) return CTW_OK;
+    cur = nxt;
+    n_cur = n_next;
+    which ^= 1;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- records ----
+
+// Walk a survivor's winner chain back to its emitting arc (or the seed),
+// collecting output labels. Labels come newest-first; the record stores
+// them oldest-first: [pending chain of the source] + emitting olabel +
+// epsilon olabels in path order (_kernel.pyx:400-416).
+struct WalkEnd {
+  int32_t bp;
+  int32_t pend;  // olabel code of the source's pending chain
+  int n;         // labels found on the walk (excluding pend)
+  int32_t last;  // the single label when n == 1
+  bool ok;
+};
+
+__device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, uint32_t h,
+                                        const CtwSrc* src, const int32_t* pend, int hop_cap) {
+  WalkEnd w{-1, 0, 0, 0, true};
+  for (int hop = 0; hop < hop_cap; ++hop) {
+    const uint32_t tb = __ldcg(&L.T[h].tb);
+    const uint32_t aux = __ldcg(&L.T[h].aux);
+    if (tb == CTW_SEED_TB) return w;
+    const uint32_t a = tb & ~CTW_EPS_BIT;
+    const int32_t ol = g.olabel[a];
+    if (ol != 0) {
+      ++w.n;
+      w.last = ol;
+    }
+    if (!(tb & CTW_EPS_BIT)) {
+      w.bp = src[aux].bp;
+      w.pend = pend ? pend[aux] : 0;
+      return w;
+    }
+    h = tok_find(L.T, L.mask, L.shift, aux);
+    if (h == CTW_EMPTY) break;
+  }
+  w.ok = false;
+  return w;
+}
+
+__device__ __forceinline__ int code_len(const int32_t* pool, int32_t code) {
+  return code == 0 ? 0 : (code > 0 ? 1 : pool[-code - 1]);
+}
+
+// Olabel code of a record: 0 none, >0 one label, <0 pool segment
+// -(offset+1) holding [n, l1..ln].
+__device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t h,
+                               const WalkEnd& w) {
+  const int np = code_len(L.pool, w.pend);
+  const int n = np + w.n;
+  if (n == 0) return 0;
+  if (n == 1) return np ? w.pend : w.last;
+  const int off = atomicAdd(&sm.pool_used, n + 1);
+  if (off + n + 1 > L.pool_cap) {
+    atomicMax(&sm.status, CTW_GROW_POOL);
+    return 0;
+  }
+  int32_t* seg = L.pool + off;
+  seg[0] = n;
+  if (np == 1) seg[1] = w.pend;
+  else
+    for (int i = 0; i < np; ++i) seg[1 + i] = L.pool[-w.pend - 1 + 1 + i];
+  // walk again, writing newest-first labels from the back
+  int pos = n;
+  for (int hop = 0; hop < 1 << 20; ++hop) {
+    const uint32_t tb = __ldcg(&L.T[h].tb);
+    const uint32_t aux = __ldcg(&L.T[h].aux);
+    if (tb == CTW_SEED_TB) break;
+    const uint32_t a = tb & ~CTW_EPS_BIT;
+    const int32_t ol = g.olabel[a];
+    if (ol != 0) seg[pos--] = ol;
+    if (!(tb & CTW_EPS_BIT)) break;
+    h = tok_find(L.T, L.mask, L.shift, aux);
+    if (h == CTW_EMPTY) break;
+  }
+  return -(off + 1);
+}
+
+// ------------------------------------------------------------- prune ------
+
+__device__ __forceinline__ int digit_of(unsigned long long key, uint32_t state, int d) {
+  return d < 8 ? (int)((key >> (56 - 8 * d)) & 255) : (int)((state >> (24 - 8 * (d - 8))) & 255);
+}
+
+// Compare the top `depth` 8-bit digits of (key, state) with the prefix.
+__device__ __forceinline__ int cmp_prefix(unsigned long long key, uint32_t state, int depth,
+                                          unsigned long long ph, uint32_t pl) {
+  if (depth <= 8) {
+    if (depth == 0) return 0;
+    const unsigned long long x = key >> (64 - 8 * depth);
+    return x < ph ? -1 : (x > ph ? 1 : 0);
+  }
+  if (key != ph) return key < ph ? -1 : 1;
+  const uint32_t x = state >> (32 - 8 * (depth - 8));
+  return x < pl ? -1 : (x > pl ? 1 : 0);
+}
+
+// Exact top-k by (cost, state) among in-beam slots: MSD radix select over the
+// 96-bit (sortable cost, state) key, 8 bits per pass, stopping as soon as the
+// prefix bucket is taken whole. Leaves (sel_hi, sel_lo, sel_depth).
+__device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned long long cut_key,
+                             long long k) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm.sel_hi = 0;
+    sm.sel_lo = 0;
+    sm.sel_depth = 0;
+    sm.sel_need = (int)k;
+    sm.sel_done = 0;
+  }
+  __syncthreads();
+  for (int d = 0; d < 12; ++d) {
+    for (int i = tid; i < 256; i += CTW_BS) sm.hist[i] = 0;
+    __syncthreads();
+    const unsigned long long ph = sm.sel_hi;
+    const uint32_t pl = sm.sel_lo;
+    for (int i = tid; i < n_slots; i += CTW_BS) {
+      const CtwTok* e = &L.T[L.slots[i]];
+      const unsigned long long key = __ldcg(&e->key);
+      if (key > cut_key) continue;
+      const uint32_t st = __ldcg(&e->state);
+      if (cmp_prefix(key, st, d, ph, pl) != 0) continue;
+      atomicAdd(&sm.hist[digit_of(key, st, d)], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      // warp 0: locate the bucket holding the need-th smallest
+      uint32_t c[8];
+      uint32_t sum = 0;
+      for (int j = 0; j < 8; ++j) {
+        c[j] = sm.hist[tid * 8 + j];
+        sum += c[j];
+      }
+      uint32_t incl = sum;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (tid >= o) incl += t;
+      }
+      const uint32_t excl = incl - sum;
+      const uint32_t need = (uint32_t)sm.sel_need;
+      const bool mine = excl < need && need <= incl;
+      if (mine) {
+        uint32_t run = excl;
+        int b = 0;
+        for (int j = 0; j < 8; ++j) {
+          if (run + c[j] >= need) {
+            b = tid * 8 + j;
+            break;
+          }
+          run += c[j];
+        }
+        const uint32_t rem = need - run;
+        if (d < 8) sm.sel_hi = (sm.sel_hi << 8) | (unsigned long long)b;
+        else sm.sel_lo = (sm.sel_lo << 8) | (uint32_t)b;
+        sm.sel_depth = d + 1;
+        sm.sel_need = (int)rem;
+        if (sm.hist[b] == rem) sm.sel_done = 1;
+      }
+    }
+    __syncthreads();
+    if (sm.sel_done) break;
+  }
+}
+
+// --------------------------------------------------------- frame kernel ---
+
+struct ChunkArgs {
+  const void* loglik;       // [*, width] rows, f32 or f64, device
+  const long long* ll_off;  // per batch entry: element offset of frame 0
+  const int* nframes;       // per batch entry
+  const int* lane_ids;      // per batch entry
+  int width;
+  int is_f64;
+  CtwDecodeCfg cfg;
+};
+
+__global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a,
+                                                          CtwLaneOut* out) {
+  extern __shared__ double nll_s[];
+  __shared__ Smem sm;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x;
+  CtwLane& lane = lanes[a.lane_ids[b]];
+  LaneCtx L;
+  L.T = lane.table;
+  L.tcap = 1u << lane.tlog2;
+  L.mask = L.tcap - 1;
+  L.shift = 32 - lane.tlog2;
+  L.slots = lane.slots;
+  L.pool = lane.pool;
+  L.pool_cap = lane.pcap;
+  const int F = a.nframes[b];
+  const double* boost = lane.boost;
+  const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
+  const double neg_scale = -a.cfg.acoustic_scale;
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+
+  int n_src = lane.n_src;
+  int cur_buf = lane.src_buf;
+  int w0 = (cur_buf + 1) % 3, w1 = (cur_buf + 2) % 3;
+  const int committed = cur_buf;
+  long long n_rec = lane.n_rec;
+  int pend_valid = lane.pend_valid;
+  int status = CTW_OK;
+  int err_frame = -1;
+  int f = 0;
+  int n_slots_max = 0;
+  long long arcs_total = 0, src_total = 0, rec_need = 0;
+  if (tid == 0) {
+    sm.status = CTW_OK;
+    sm.pool_used = lane.pool_used;
+    sm.arcs = 0;
+  }
+  __syncthreads();
+
+  for (f = 0; f < F; ++f) {
+    const CtwSrc* src = lane.src[cur_buf];
+    const int32_t* pend = pend_valid ? lane.pend : nullptr;
+    const int nxt_buf = (f & 1) ? w1 : w0;
+    CtwSrc* nsrc = lane.src[nxt_buf];
+    if (tid == 0) {
+      sm.n_slots = 0;
+      sm.min_key = ~0ULL;
+      sm.cnt = 0;
+      sm.hop_fail = 0;
+    }
+    // frame row -> -scale * ll (the reference's (-acoustic_scale * ll) term)
+    const long long row0 = a.ll_off[b] + (long long)f * a.width;
+    if (smem_ll) {
+      for (int v = tid; v < a.width; v += CTW_BS) {
+        const double x = a.is_f64 ? ((const double*)a.loglik)[row0 + v]
+                                  : (double)((const float*)a.loglik)[row0 + v];
+        nll_s[v] = __dmul_rn(neg_scale, x);
+      }
+    }
+    __syncthreads();
+    src_total += n_src;
+
+    // ---- emitting expansion (load-balanced over out-degree) ----
+    for (int tile = 0; tile < n_src; tile += CTW_BS) {
+      const int i = tile + tid;
+      int deg = 0;
+      if (i < n_src) {
+        const CtwSrc t = src[i];
+        const CtwStateRange r = g.ranges[t.state];
+        deg = (int)(r.emit_end - r.emit_beg);
+        sm.beg[tid] = r.emit_beg;
+        sm.cost[tid] = t.cost;
+      }
+      int excl, total;
+      Smem::Scan(sm.scan).ExclusiveSum(deg, excl, total);
+      sm.off[tid] = excl;
+      __syncthreads();
+      const int nt = min(CTW_BS, n_src - tile);
+      for (int k = tid; k < total; k += CTW_BS) {
+        int lo = 0, hi = nt - 1;  // last j with off[j] <= k
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.off[mid] <= k) lo = mid;
+          else hi = mid - 1;
+        }
+        const uint32_t arc_i = sm.beg[lo] + (uint32_t)(k - sm.off[lo]);
+        const CtwArc arc = g.arcs[arc_i];
+        double ac;
+        if (smem_ll) ac = nll_s[arc.ilabel - 1];
+        else {
+          const long long idx = row0 + arc.ilabel - 1;
+          const double x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+          ac = __dmul_rn(neg_scale, x);
+        }
+        double nc = __dadd_rn(__dadd_rn(sm.cost[lo], ac), arc.weight);
+        if (boost) {
+          const int32_t ol = g.olabel[arc_i];
+          if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+        }
+        if (!(nc < INF)) continue;
+        bool is_new = false;
+        const uint32_t d = tok_insert(L.T, L.mask, L.shift, (uint32_t)arc.nextstate, is_new);
+        if (d == CTW_EMPTY) {
+          atomicMax(&sm.status, CTW_GROW_TABLE);
+          continue;
+        }
+        if (is_new) slot_append(sm, L, d);
+        unsigned long long oldk;
+        tok_min(&L.T[d], d2key(nc), arc_i, (uint32_t)(tile + lo), &oldk);
+      }
+      if (tid == 0) arcs_total += total;
+      __syncthreads();
+    }
+
+    // ---- epsilon closure ----
+    int st = CTW_OK;
+    if (sm.status < CTW_GROW_TABLE)
+      st = eps_fixpoint(sm, L, g, lane.front, boost, a.cfg.relax_eps, a.cfg.max_ne_iters);
+    __syncthreads();
+    const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
+    n_slots_max = max(n_slots_max, n_slots);
+    if (st != CTW_OK) status = st;
+    else if (sm.status >= CTW_GROW_TABLE) status = sm.status;
+    else if (n_slots == 0) status = CTW_ERR_NO_SURVIVORS;
+
+    if (status == CTW_OK) {
+      // ---- prune: frame minimum, beam cutoff, exact max_active ----
+      unsigned long long mk = ~0ULL;
+      for (int i = tid; i < n_slots; i += CTW_BS) mk = min(mk, __ldcg(&L.T[L.slots[i]].key));
+      for (int o = 16; o; o >>= 1) mk = min(mk, __shfl_xor_sync(0xFFFFFFFFu, mk, o));
+      if ((tid & 31) == 0) atomicMin(&sm.min_key, mk);
+      __syncthreads();
+      const double cutoff = __dadd_rn(key2d(sm.min_key), a.cfg.beam);
+      const unsigned long long cut_key = d2key(cutoff);
+      int c = 0;
+      for (int i = tid; i < n_slots; i += CTW_BS) c += (__ldcg(&L.T[L.slots[i]].key) <= cut_key);
+      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+      if ((tid & 31) == 0) atomicAdd(&sm.cnt, c);
+      __syncthreads();
+      const int in_beam = sm.cnt;
+      const bool select = (long long)in_beam > a.cfg.max_active;
+      const int n_surv = select ? (int)a.cfg.max_active : in_beam;
+      if (select) radix_select(sm, L, n_slots, cut_key, a.cfg.max_active);
+      else if (tid == 0) sm.sel_depth = 0;
+      __syncthreads();
+      if (n_rec + n_surv > lane.rcap) {
+        status = CTW_GROW_HIST;
+        rec_need = n_rec + n_surv;
+      } else {
+        // ---- records + next sources, compacted in slot order ----
+        const int depth = sm.sel_depth;
+        const unsigned long long ph = sm.sel_hi;
+        const uint32_t pl = sm.sel_lo;
+        const int hop_cap = n_slots + 2;
+        int run = 0;
+        for (int tile = 0; tile < n_slots; tile += CTW_BS) {
+          const int i = tile + tid;
+          int keep = 0;
+          uint32_t h = 0;
+          unsigned long long key = 0;
+          uint32_t st2 = 0;
+          if (i < n_slots) {
+            h = L.slots[i];
+            key = __ldcg(&L.T[h].key);
+            st2 = __ldcg(&L.T[h].state);
+            keep = key <= cut_key && (!select || cmp_prefix(key, st2, depth, ph, pl) <= 0);
+          }
+          int pos, tot;
+          Smem::Scan(sm.scan).ExclusiveSum(keep, pos, tot);
+          if (keep) {
+            const WalkEnd w = walk(L, g, h, src, pend, hop_cap);
+            if (!w.ok) sm.hop_fail = 1;
+            const int32_t code = record_code(sm, L, g, h, w);
+            const long long r = n_rec + run + pos;
+            lane.rec_link[r] = make_int2(w.bp, code);
+            lane.rec_state[r] = (int32_t)st2;
+            const double cost = key2d(key);
+            lane.rec_cost[r] = cost;
+            CtwSrc ns;
+            ns.state = (int32_t)st2;
+            ns.bp = (int32_t)r;
+            ns.cost = cost;
+            nsrc[run + pos] = ns;
+          }
+          run += tot;
+          __syncthreads();
+        }
+        if (tid == 0) lane.frame_base[lane.frame_count + f] = n_rec;
+        n_rec += run;
+        n_src = run;
+        __syncthreads();
+        if (sm.status >= CTW_GROW_TABLE) status = sm.status;
+        else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
+      }
+    }
+
+    // ---- reset every touched table entry (also on failure) ----
+    for (int i = tid; i < n_slots; i += CTW_BS) tok_clear(&L.T[L.slots[i]]);
+    __syncthreads();
+    if (status != CTW_OK) {
+      err_frame = f;
+      break;
+    }
+    cur_buf = nxt_buf;
+    pend_valid = 0;
+  }
+
+  if (tid == 0) {
+    CtwLaneOut o;
+    o.status = status;
+    o.err_frame = err_frame;
+    o.n_slots_max = n_slots_max;
+    o.arcs_expanded = arcs_total;
+    o.src_total = src_total;
+    o.rec_need = rec_need;
+    if (status == CTW_OK) {
+      lane.n_src = n_src;
+      lane.src_buf = (F > 0) ? cur_buf : committed;
+      lane.frame_count += F;
+      lane.pool_used = sm.pool_used;
+      lane.n_rec = n_rec;
+      lane.pend_valid = pend_valid;
+    }
+    o.n_src = lane.n_src;
+    o.src_buf = lane.src_buf;
+    o.frame_count = lane.frame_count;
+    o.pool_used = lane.pool_used;
+    o.n_rec = lane.n_rec;
+    o.pend_valid = lane.pend_valid;
+    out[b] = o;
+  }
+}
+
+// ------------------------------------------------------------ seeding ----
+
+// Fresh channel: token at the start state plus its epsilon closure
+// (decoder.py:173-229). All closure states become sources with bp = -1 and
+// their pending olabel chains (no pruning at seed time, as in the reference).
+__global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, const int* lane_ids,
+                                                 int start, CtwDecodeCfg cfg, CtwLaneOut* out) {
+  __shared__ Smem sm;
+  const int tid = threadIdx.x;
+  CtwLane& lane = lanes[lane_ids[blockIdx.x]];
+  LaneCtx L;
+  L.T = lane.table;
+  L.tcap = 1u << lane.tlog2;
+  L.mask = L.tcap - 1;
+  L.shift = 32 - lane.tlog2;
+  L.slots = lane.slots;
+  L.pool = lane.pool;
+  L.pool_cap = lane.pcap;
+  if (tid == 0) {
+    sm.status = CTW_OK;
+    sm.pool_used = 0;
+    sm.n_slots = 0;
+    sm.hop_fail = 0;
+    bool is_new = false;
+    const uint32_t h = tok_insert(L.T, L.mask, L.shift, (uint32_t)start, is_new);
+    slot_append(sm, L, h);
+    unsigned long long oldk;
+    tok_min(&L.T[h], d2key(0.0), CTW_SEED_TB, 0, &oldk);
+  }
+  __syncthreads();
+  int status = eps_fixpoint(sm, L, g, lane.front, lane.boost, cfg.relax_eps, cfg.max_ne_iters);
+  __syncthreads();
+  const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
+  if (status == CTW_OK && sm.status >= CTW_GROW_TABLE) status = sm.status;
+  if (status == CTW_OK) {
+    CtwSrc* dst = lane.src[0];
+    for (int i = tid; i < n_slots; i += CTW_BS) {
+      const uint32_t h = L.slots[i];
+      const WalkEnd w = walk(L, g, h, nullptr, nullptr, n_slots + 2);
+      if (!w.ok) sm.hop_fail = 1;
+      CtwSrc s;
+      s.state = (int32_t)__ldcg(&L.T[h].state);
+      s.bp = -1;
+      s.cost = key2d(__ldcg(&L.T[h].key));
+      dst[i] = s;
+      lane.pend[i] = record_code(sm, L, g, h, w);
+    }
+    __syncthreads();
+    if (sm.status >= CTW_GROW_TABLE) status = sm.status;
+    else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
+  }
+  for (int i = tid; i < n_slots; i += CTW_BS) tok_clear(&L.T[L.slots[i]]);
+  __syncthreads();
+  if (tid == 0) {
+    CtwLaneOut o = {};
+    o.status = status;
+    o.err_frame = -1;
+    if (status == CTW_OK) {
+      lane.n_src = n_slots;
+      lane.src_buf = 0;
+      lane.frame_count = 0;
+      lane.pool_used = sm.pool_used;
+      lane.n_rec = 0;
+      lane.pend_valid = 1;
+    }
+    o.n_src = lane.n_src;
+    o.src_buf = lane.src_buf;
+    o.frame_count = lane.frame_count;
+    o.pool_used = lane.pool_used;
+    o.n_rec = lane.n_rec;
+    o.pend_valid = lane.pend_valid;
+    out[blockIdx.x] = o;
+  }
+}
+
+// ------------------------------------------------------- best path -------
+
+// One warp per lane: best token (final states preferred, ties -> lowest
+// state; decoder.py:384-400), then the backpointer walk over the lane's
+// records. Words are written oldest-first into words[woff[b] .. + cap[b]);
+// nwords[b] always receives the true length (host retries when too small).
+__global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_ids, int n,
+                            int32_t* words, const long long* woff, const int* wcap, int* nwords,
+                            double* total_cost, int* status) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int ln = threadIdx.x & 31;
+  if (warp >= n) return;
+  const CtwLane& lane = lanes[lane_ids[warp]];
+  const CtwSrc* src = lane.src[lane.src_buf];
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  // pass 1: final tokens; pass 2 (only if none final): all tokens
+  double best = INF;
+  int best_state = 0x7FFFFFFF, best_i = -1;
+  for (int pass = 0; pass < 2 && best_i < 0; ++pass) {
+    for (int i = ln; i < lane.n_src; i += 32) {
+      const CtwSrc t = src[i];
+      double tot;
+      if (pass == 0) {
+        const double fw = g.final_w[t.state];
+        if (fw == INF) continue;
+        tot = t.cost + fw;
+      } else {
+        tot = t.cost;
+        if (!(tot < INF)) continue;
+      }
+      if (tot < best || (tot == best && t.state < best_state)) {
+        best = tot;
+        best_state = t.state;
+        best_i = i;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+      const int os = __shfl_xor_sync(0xFFFFFFFFu, best_state, o);
+      const int oi = __shfl_xor_sync(0xFFFFFFFFu, best_i, o);
+      if (oi >= 0 && (best_i < 0 || ob < best || (ob == best && os < best_state))) {
+        best = ob;
+        best_state = os;
+        best_i = oi;
+      }
+    }
+  }
+  if (ln != 0) return;
+  if (best_i < 0) {
+    status[warp] = 1;
+    nwords[warp] = 0;
+    total_cost[warp] = INF;
+    return;
+  }
+  status[warp] = 0;
+  total_cost[warp] = best;
+  int count = 0;
+  for (int r = src[best_i].bp; r >= 0;) {
+    const int2 lk = lane.rec_link[r];
+    count += code_len(lane.pool, lk.y);
+    r = lk.x;
+  }
+  nwords[warp] = count;
+  if (count > wcap[warp]) return;
+  int32_t* w = words + woff[warp];
+  int pos = count;
+  for (int r = src[best_i].bp; r >= 0;) {
+    const int2 lk = lane.rec_link[r];
+    const int c = lk.y;
+    if (c > 0) w[--pos] = c;
+    else if (c < 0) {
+      const int32_t* seg = lane.pool + (-c - 1);
+      const int m = seg[0];
+      pos -= m;
+      for (int j = 0; j < m; ++j) w[pos + j] = seg[1 + j];
+    }
+    r = lk.x;
+  }
+}
+
+__global__ void k_clear_table(CtwTok* T, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tok_clear(&T[i]);
+}
+
+}  // namespace
+
+// ------------------------------------------------------ launch wrappers ---
+
+extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                                 const int32_t* olabel, const double* final_w, const void* loglik,
+                                 int is_f64, int width, const long long* ll_off, const int* nframes,
+                                 const int* lane_ids, int n, const CtwDecodeCfg* cfg, CtwLaneOut* out,
+                                 cudaStream_t stream) {
+  GraphDev g{ranges, arcs, olabel, final_w};
+  ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, *cfg};
+  const size_t dyn = (width <= CTW_MAX_SMEM_WIDTH ? (size_t)width : 0) * sizeof(double);
+  if (dyn > 48 * 1024)
+    cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  k_decode_chunk<<<n, CTW_BS, dyn, stream>>>(d_lanes, g, a, out);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int ctw_launch_seed(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                               const int32_t* olabel, const double* final_w, const int* lane_ids, int n,
+                               int start, const CtwDecodeCfg* cfg, CtwLaneOut* out, cudaStream_t stream) {
+  GraphDev g{ranges, arcs, olabel, final_w};
+  k_seed<<<n, CTW_BS, 0, stream>>>(d_lanes, g, lane_ids, start, *cfg, out);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int ctw_launch_best(const CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                               const int32_t* olabel, const double* final_w, const int* lane_ids, int n,
+                               int32_t* words, const long long* woff, const int* wcap, int* nwords,
+                               double* total_cost, int* status, cudaStream_t stream) {
+  GraphDev g{ranges, arcs, olabel, final_w};
+  const int warps_per_block = 4;
+  const int blocks = (n + warps_per_block - 1) / warps_per_block;
+  k_best_path<<<blocks, 32 * warps_per_block, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap,
+                                                          nwords, total_cost, status);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int ctw_launch_clear(CtwTok* T, uint32_t n, cudaStream_t stream) {
+  k_clear_table<<<(n + 255) / 256, 256, 0, stream>>>(T, n);
+  return (int)cudaGetLastError();
+}

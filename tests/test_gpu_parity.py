@@ -1,0 +1,271 @@
+"""GPU parity: the sm_100a decoder against the reference's golden vectors and
+the CPU oracle (oracle/ctw_oracle.c, itself pinned in test_oracle.py).
+
+Bar (BASELINE.json north_star): best-path words bit-exact, best-path cost
+within 1e-4 relative. The GPU computes in IEEE f64 with the reference's
+operation order, so these tests demand MORE: identical per-frame history
+records (prev, olabels, state, cost) and bit-identical costs.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GoldenGraph, expected_history, golden_chunks, golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL = 1e-4  # north_star tolerance on best-path cost (we also check exact equality)
+
+
+def _cfg(d):
+    from paper_2311_04996_b200 import DecoderConfig
+
+    return DecoderConfig(beam=d["beam"], max_active=d["max_active"], acoustic_scale=d["acoustic_scale"],
+                         nonemitting_relax_epsilon=d["relax_eps"],
+                         max_nonemitting_iters=None if d["max_ne_iters"] < 0 else d["max_ne_iters"])
+
+
+def _run_golden(d, kernel=None):
+    from paper_2311_04996_b200 import DecodeError, DecodeState, flatten
+
+    fg = flatten(GoldenGraph(d))
+    ch = DecodeState(fg, _cfg(d), kernel=kernel)
+    boost = d["boost"] if d["has_boost"] else None
+    if boost is not None:
+        if d["boost_poke"]:
+            ch.boost = boost
+        else:
+            ch.set_boost(boost)
+    seed = sorted((t.state, t.cost) for t in ch.active_tokens())
+    err = ""
+    for c in golden_chunks(d):
+        try:
+            ch.advance_frames(c)
+        except DecodeError as e:
+            err = str(e)
+            break
+    return ch, seed, err
+
+
+def _check_channel(d, ch, seed, err):
+    from paper_2311_04996_b200 import best_path
+
+    assert seed == sorted(zip(d["seed_state"].tolist(), d["seed_cost"].tolist()))
+    assert err == d["error"]
+    assert ch.history_records() == expected_history(d)
+    assert [t.state for t in ch.active_tokens()] == d["tok_state"].tolist()
+    assert [t.cost for t in ch.active_tokens()] == d["tok_cost"].tolist()
+    assert [t.backpointer for t in ch.active_tokens()] == d["tok_bp"].tolist()
+    if d["frame_count"]:
+        h = best_path(ch)
+        assert list(h.words) == d["best_words"].tolist()
+        assert h.total_cost == d["best_cost"]
+        assert h.frame_count == d["frame_count"]
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_native_lane(name):
+    d = load_golden(name)
+    ch, seed, err = _run_golden(d)
+    _check_channel(d, ch, seed, err)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_through_reference_kernel_seam(name):
+    """DecodeState(kernel=kernels.advance_chunk): the reference's plug-in
+    contract served by the GPU."""
+    from paper_2311_04996_b200 import kernels
+
+    d = load_golden(name)
+    ch, seed, err = _run_golden(d, kernel=kernels.advance_chunk)
+    _check_channel(d, ch, seed, err)
+
+
+def test_golden_decode_batch_one_launch():
+    from paper_2311_04996_b200 import Hypothesis, decode_batch, flatten
+
+    names = [n for n in golden_names() if n.startswith("c1_")]
+    ds = [load_golden(n) for n in names]
+    fg = flatten(GoldenGraph(ds[0]))
+    got = decode_batch(fg, _cfg(ds[0]), [d["frames"] for d in ds])
+    for d, h in zip(ds, got):
+        assert isinstance(h, Hypothesis)
+        assert list(h.words) == d["best_words"].tolist()
+        assert h.total_cost == d["best_cost"]
+
+
+def test_dead_beam_is_atomic_and_recoverable():
+    from paper_2311_04996_b200 import DecodeError, DecodeState, flatten
+
+    d = load_golden("kat_dead_beam")
+    ch = DecodeState(flatten(GoldenGraph(d)), _cfg(d))
+    frames = d["frames"]
+    with pytest.raises(DecodeError, match="frame 1"):
+        ch.advance_frames(frames)
+    assert ch.frame_count == 0
+    assert ch.active_states() == {0, 3}
+    ch.advance_frames(frames[:1])
+    assert ch.frame_count == 1
+
+
+# ------------------------------------------------------------ vs oracle ----
+
+
+def _system(**kw):
+    from paper_2311_04996_b200 import synth
+
+    return synth.build_system(synth.SystemSpec(**kw))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_systems_history_identical_to_oracle(oracle_mod, seed):
+    from paper_2311_04996_b200 import DecoderConfig, DecodeState, best_path, synth
+
+    spec = dict(num_units=4 + 3 * seed, num_words=10 + 7 * seed, order=1 + seed % 3, seed=seed,
+                min_pron=1, max_pron=5)
+    s = _system(**spec)
+    rng = np.random.default_rng(seed)
+    if seed % 2:
+        frames = rng.normal(-3.0, 2.5, size=(60, spec["num_units"]))
+    else:
+        frames = synth.planted_utterances(s, 1, 60, seed=seed)[0]
+    cfg = DecoderConfig(beam=[4.0, 9.0, 17.0, 1e9][seed % 4], max_active=[7, 60, 10_000, 300][seed % 4])
+    ch = DecodeState(s.graph, cfg)
+    oc = oracle_mod.OracleChannel.from_config(s.graph, cfg)
+    step = [60, 1, 7, 13][seed % 4]
+    for i in range(0, 60, step):
+        ch.advance_frames(frames[i:i + step])
+        oc.advance_frames(frames[i:i + step])
+    assert ch.history_records() == oc.history_records()
+    h = best_path(ch)
+    assert (h.words, h.total_cost, h.frame_count) == oc.best_path()
+
+
+def test_trigram_batch_matches_oracle(oracle_mod):
+    """Mid-size 3-gram TLG, 24 utterances in one launch, max_active binding."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_batch, synth
+
+    s = _system(num_units=129, blank_id=128, num_words=400, order=3, seed=5, min_pron=1, max_pron=4,
+                followers=20)
+    utts = list(synth.conformer_logprobs(s, 24, 120, seed=3, delta=5.0, sigma=1.5, dtype=np.float32))
+    cfg = DecoderConfig(beam=14.0, max_active=700)
+    got = decode_batch(s.graph, cfg, utts)
+    for u, h in zip(utts, got):
+        ow, oc, ofc = oracle_mod.decode_utterance(s.graph, cfg, u.astype(np.float64))
+        assert h.words == ow
+        assert h.total_cost == oc
+        assert math.isclose(h.total_cost, oc, rel_tol=COST_RTOL)
+
+
+def test_per_utterance_boost_matches_oracle(oracle_mod):
+    from paper_2311_04996_b200 import BoostTable, DecoderConfig, boost_costs, decode_batch, synth
+
+    s = _system(num_units=30, num_words=60, order=2, seed=9)
+    utts = synth.planted_utterances(s, 6, 80, seed=4, gap=6.0, noise=1.5)
+    rng = np.random.default_rng(0)
+    boosts = []
+    for i in range(6):
+        ids = rng.choice(np.arange(1, 61), size=10, replace=False)
+        tab = BoostTable(entries={int(w): -float(rng.uniform(0.5, 8.5)) for w in ids})
+        boosts.append(boost_costs(tab, s.graph.max_olabel) if i % 3 else None)
+    cfg = DecoderConfig(beam=12.0, max_active=500)
+    got = decode_batch(s.graph, cfg, utts, boost=boosts)
+    for u, b, h in zip(utts, boosts, got):
+        ow, oc, _ = oracle_mod.decode_utterance(s.graph, cfg, u, boost=b)
+        assert h.words == ow and h.total_cost == oc
+
+
+def test_streaming_equals_offline_bit_exact():
+    from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, StreamPool, decode_utterance, synth
+
+    s = _system(num_units=30, num_words=50, order=2, seed=2)
+    utts = synth.planted_utterances(s, 5, 70, seed=8)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    offline = [decode_utterance(s.graph, cfg, u) for u in utts]
+    for chunk in (1, 7, 60):
+        pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=3))
+        sids = [pool.create_stream() for _ in utts]
+        for sid, u in zip(sids, utts):
+            cuts = list(range(0, len(u), chunk))
+            for i in cuts:
+                pool.push_chunk(Chunk(sid, u[i:i + chunk], is_last=i + chunk >= len(u)))
+        finals = pool.drain()
+        for sid, want in zip(sids, offline):
+            assert finals[sid] == want
+
+
+def test_stream_partials_and_state_machine():
+    from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, StreamError, StreamPool, synth
+
+    s = _system(num_units=10, num_words=12, order=1, seed=4)
+    pool = StreamPool(s.graph, DecoderConfig(beam=10.0, max_active=200), BatcherConfig(max_batch=1))
+    sid = pool.create_stream()
+    for _ in range(3):
+        pool.push_chunk(Chunk(sid, np.zeros((2, 10))))
+    pool.push_chunk(Chunk(sid, np.zeros((0, 10)), is_last=True))
+    with pytest.raises(StreamError, match="draining"):
+        pool.push_chunk(Chunk(sid, np.zeros((2, 10))))
+    seen = 0
+    while True:
+        out = pool.step()
+        if not out:
+            break
+        seen += 1
+        assert out[0][0] == sid
+        assert out[0][1].frame_count == min(seen * 2, 6)
+    assert seen == 4
+    assert pool.finish_stream(sid).frame_count == 6
+    with pytest.raises(StreamError, match="finished"):
+        pool.finish_stream(sid)
+
+
+def test_api_errors_match_reference_messages():
+    from paper_2311_04996_b200 import DecodeError, DecoderConfig, advance, best_path, create_channel, synth
+
+    s = _system(num_units=6, num_words=8, order=1, seed=1)
+    ch = create_channel(s.graph, DecoderConfig(beam=1e9, max_active=10**9))
+    with pytest.raises(DecodeError, match="frames"):
+        best_path(ch)
+    ch.advance_frames(np.zeros((0, 6)))
+    assert ch.frame_count == 0
+    with pytest.raises(DecodeError, match="tokens"):
+        ch.advance_frames(np.zeros((1, 3)))
+    advance(ch, np.full(6, -1.0))
+    with pytest.raises(DecodeError, match="tokens"):
+        advance(ch, np.full(7, -1.0))
+    with pytest.raises(DecodeError, match="before"):
+        ch.set_boost(np.zeros(s.graph.max_olabel + 1))
+
+
+def test_torch_cuda_tensors_zero_copy_path(oracle_mod):
+    import torch
+
+    from paper_2311_04996_b200 import DecoderConfig, decode_batch, synth
+
+    s = _system(num_units=30, num_words=40, order=2, seed=6)
+    utts = synth.planted_utterances(s, 4, 50, seed=1, dtype=np.float32)
+    cfg = DecoderConfig(beam=12.0, max_active=400)
+    host = decode_batch(s.graph, cfg, utts)
+    dev = decode_batch(s.graph, cfg, [torch.from_numpy(u).cuda() for u in utts])
+    assert host == dev
+    for u, h in zip(utts, host):
+        assert (h.words, h.total_cost) == oracle_mod.decode_utterance(s.graph, cfg, u.astype(np.float64))[:2]
+
+
+def test_lane_reuse_and_decode_failure_per_index():
+    from paper_2311_04996_b200 import DecodeFailure, DecoderConfig, Hypothesis, decode_batch, synth
+
+    s = _system(num_units=12, num_words=20, order=2, seed=3)
+    utts = synth.planted_utterances(s, 5, 30, seed=2)
+    bad = utts[2].copy()
+    bad[4] = -np.inf
+    utts[2] = bad
+    utts[3] = np.zeros((0, 12))
+    cfg = DecoderConfig(beam=10.0, max_active=100)
+    for _ in range(3):  # lanes are recycled between calls
+        got = decode_batch(s.graph, cfg, utts)
+        assert isinstance(got[0], Hypothesis) and isinstance(got[4], Hypothesis)
+        assert isinstance(got[2], DecodeFailure) and "frame 4" in str(got[2].error)
+        assert isinstance(got[3], DecodeFailure)
