@@ -76,6 +76,7 @@ uint32_t ceil_log2(uint64_t x) {
 // ------------------------------------------------------------------ graph --
 
 struct ctw_graph {
+  int refs = 1;  // the creator + one per lane set (lanes keep their graph alive)
   int device = 0;
   int64_t S = 0, A = 0, start = 0, max_il = 0, max_ol = 0;
   CtwStateRange* ranges = nullptr;
@@ -135,6 +136,8 @@ struct ctw_lanes {
 
 namespace {
 
+std::mutex g_graph_mu;
+
 int sync_lane(ctw_lanes* l, int i) {
   CUDA_TRY(cudaMemcpyAsync(&l->d[i], &l->h[i], sizeof(CtwLane), cudaMemcpyHostToDevice, l->stream));
   return 0;
@@ -157,6 +160,7 @@ void free_lane(CtwLane& L) {
 // preserving the committed sources (and their pending chains).
 int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   CtwLane& L = l->h[i];
+  if (tlog2 > 24) return fail(-3, "token table would exceed 2^24 entries per lane");
   const uint64_t tcap = 1ull << tlog2;
   const uint64_t scap = tcap / 2 + 1;
   CtwTok* table;
@@ -165,7 +169,7 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   int32_t* pend;
   CUDA_TRY(dalloc(&table, tcap));
   CUDA_TRY(dalloc(&slots, tcap));
-  CUDA_TRY(dalloc(&front, 2 * tcap));
+  CUDA_TRY(dalloc(&front, 3 * tcap));
   for (int b = 0; b < 3; ++b) CUDA_TRY(dalloc(&src[b], scap));
   CUDA_TRY(dalloc(&pend, scap));
   if (ctw_launch_clear(table, (uint32_t)tcap, l->stream)) return fail(-1, "clear kernel launch failed");
@@ -437,6 +441,10 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
 
 void ctw_graph_destroy(ctw_graph* g) {
   if (!g) return;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (--g->refs > 0) return;
+  }
   cudaSetDevice(g->device);
   dfree(g->ranges);
   dfree(g->arcs);
@@ -464,6 +472,10 @@ int ctw_lanes_create(ctw_graph* g, int32_t n_lanes, const ctw_config* cfg, void*
   CUDA_TRY(cudaSetDevice(g->device));
   ctw_lanes* l = new ctw_lanes();
   l->g = g;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g->refs++;
+  }
   l->cfg = *cfg;
   l->dcfg = CtwDecodeCfg{cfg->beam, cfg->acoustic_scale, cfg->relax_eps, (long long)cfg->max_active,
                          (long long)cfg->max_ne_iters};
@@ -513,7 +525,9 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   if (l->ev0) cudaEventDestroy(l->ev0);
   if (l->ev1) cudaEventDestroy(l->ev1);
   if (l->own_stream) cudaStreamDestroy(l->stream);
+  ctw_graph* g = l->g;
   delete l;
+  ctw_graph_destroy(g);  // drop the lane set's reference
 }
 
 int ctw_lanes_reserve(ctw_lanes* l, int32_t n) {

@@ -37,19 +37,31 @@ struct __align__(16) CtwArc {
   int32_t ilabel;
 };
 
-// Token-table entry (32 B = one L2 sector). `key`+`tb` are updated together
-// by a 128-bit CAS; `key` is the order-preserving bit pattern of the f64 cost
-// and `tb` the tie-break: the winning arc index (emitting arcs) or
-// EPS_BIT|arc (epsilon arcs, which lose exact ties to emitting winners as in
-// the reference's strict '<', _kernel.pyx:273/:332). `aux` is the source
-// token index (emitting winner) or the predecessor state (epsilon winner).
+// Token-table entry (32 B = one L2 sector), one per state reached in the
+// current frame (open addressing on `state`).
+//  key, tb, aux  -- updated together by one 128-bit CAS. `key` is the
+//     order-preserving bit image of the f64 cost; ties on `key` are broken
+//     exactly as the reference's sequential Gauss-Seidel order would:
+//       emitting winner: tb = arc index (lowest arc = first writer,
+//         _kernel.pyx:243-285), aux = source token index;
+//       epsilon winner:  tb = EPS_BIT | arc, aux = pd << 24 | pred table
+//         index, where pd is the Gauss-Seidel pass in which the predecessor
+//         was processed holding its final value; epsilon candidates never
+//         displace an equal-cost emitting / seed winner (strict '<',
+//         _kernel.pyx:332) and among themselves order by (pd, gpos(pred), arc).
+//  gpos -- the state's position in the reference's slot list
+//     (_kernel.pyx:266, :324): level << 56 | chain key, where level 0 =
+//     reached by an emitting arc (key = first-arrival arc index) and level L
+//     = first discovered by the epsilon closure from a level L-1 slot
+//     (key = discoverer's key << 4 | epsilon-arc offset).
+//  state -- hash key (CTW_EMPTY when free); stamp -- frontier dedupe epoch.
 struct __align__(32) CtwTok {
   unsigned long long key;
   uint32_t tb;
   uint32_t aux;
-  uint32_t state;  // hash key; CTW_EMPTY when free
-  uint32_t stamp;  // epsilon-frontier dedupe epoch
-  uint32_t pad0, pad1;
+  unsigned long long gpos;
+  uint32_t state;
+  uint32_t stamp;
 };
 
 #define CTW_EMPTY 0xFFFFFFFFu

@@ -11,15 +11,23 @@
 //                                                       _kernel.pyx:249-253
 //   recombination: min cost per state, ties -> first arc in (source state,
 //     arc) order == lowest global CSR arc index          _kernel.pyx:243-285
-//   epsilon relaxation to a fixpoint, stop when improvements <= relax_eps,
-//     cap max_ne_iters passes -> ERR_EPS_ITERS           _kernel.pyx:292-355
+//   epsilon relaxation: Gauss-Seidel passes over the slot list until the
+//     largest improvement of a pass is <= relax_eps; > max_ne_iters passes
+//     -> ERR_EPS_ITERS                                    _kernel.pyx:292-355
 //   no slots -> ERR_NO_SURVIVORS; keep cost <= min+beam, then the
 //     max_active smallest (cost, state)                  _kernel.pyx:357-390
 //   records (prev, olabels oldest-first, state, cost)    _kernel.pyx:392-427
 //   seeding closure                                      decoder.py:173-229
 //   best-path token choice + backtrace                   decoder.py:377-415
-// See DESIGN.md for the deviations that are inherent to a parallel fixpoint
-// (exact epsilon ties and sub-relax_eps improvements; none observed in tests).
+//
+// The epsilon stage is computed as a parallel label-correcting fixpoint, not
+// sequentially. Its result equals the reference's Gauss-Seidel result
+// including exact-tie resolution: every slot carries its Gauss-Seidel slot
+// position (gpos, see ctw_common.h) and every epsilon candidate the pass
+// (pd) in which Gauss-Seidel would relax it with its final value, and equal
+// costs are ordered by that event time (pd, gpos(pred), arc). The pass count
+// checked against max_ne_iters is the Gauss-Seidel one (1 + max pd). See
+// DESIGN.md "Epsilon closure".
 #include <cuda_runtime.h>
 #include <cub/block/block_scan.cuh>
 #include <stdint.h>
@@ -27,7 +35,12 @@
 #include "ctw_common.h"
 
 #define CTW_BS 256
+#define CTW_IPT 4                        // sources per thread per expansion tile
+#define CTW_TILE (CTW_BS * CTW_IPT)
 #define CTW_MAX_SMEM_WIDTH 4096
+#define CTW_PRED_BITS 24
+#define CTW_PRED_MASK ((1u << CTW_PRED_BITS) - 1u)
+#define CTW_KEY56 ((1ULL << 56) - 1ULL)
 
 namespace {
 
@@ -75,55 +88,78 @@ __device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
   return (s * 0x9E3779B1u) >> shift;
 }
 
-// Find-or-insert `d` in the lane's open-addressing table (linear probing).
-// Returns the table index or CTW_EMPTY when the table is full.
-__device__ __forceinline__ uint32_t tok_insert(CtwTok* T, uint32_t mask, uint32_t shift, uint32_t d,
-                                               bool& is_new) {
-  uint32_t h = tok_hash(d, shift);
-  for (uint32_t probe = 0; probe <= mask; ++probe) {
-    uint32_t k = __ldcg(&T[h].state);
+struct LaneCtx {
+  CtwTok* T;
+  uint32_t mask, shift, tcap;
+  uint32_t* slots;
+  int pool_cap;
+  int32_t* pool;
+};
+
+// Find-or-insert `d` (linear probing). Returns the table index or CTW_EMPTY
+// when the table is full.
+__device__ __forceinline__ uint32_t tok_insert(const LaneCtx& L, uint32_t d, bool& is_new) {
+  uint32_t h = tok_hash(d, L.shift);
+  for (uint32_t probe = 0; probe <= L.mask; ++probe) {
+    const uint32_t k = __ldcg(&L.T[h].state);
     if (k == d) return h;
     if (k == CTW_EMPTY) {
-      uint32_t old = atomicCAS(&T[h].state, CTW_EMPTY, d);
+      const uint32_t old = atomicCAS(&L.T[h].state, CTW_EMPTY, d);
       if (old == CTW_EMPTY) {
         is_new = true;
         return h;
       }
       if (old == d) return h;
     }
-    h = (h + 1) & mask;
+    h = (h + 1) & L.mask;
   }
   return CTW_EMPTY;
 }
 
-__device__ __forceinline__ uint32_t tok_find(const CtwTok* T, uint32_t mask, uint32_t shift, uint32_t d) {
-  uint32_t h = tok_hash(d, shift);
-  for (uint32_t probe = 0; probe <= mask; ++probe) {
-    uint32_t k = __ldcg(&T[h].state);
-    if (k == d) return h;
-    if (k == CTW_EMPTY) return CTW_EMPTY;
-    h = (h + 1) & mask;
-  }
-  return CTW_EMPTY;
+// Gauss-Seidel event order of two epsilon candidates with equal cost:
+// (pd, slot position of the predecessor, arc).
+__device__ __forceinline__ bool gs_before(const CtwTok* T, uint32_t pd_a, uint32_t pred_a, uint32_t arc_a,
+                                          unsigned long long gpos_a, uint32_t aux_b, uint32_t arc_b) {
+  const uint32_t pd_b = aux_b >> CTW_PRED_BITS;
+  if (pd_a != pd_b) return pd_a < pd_b;
+  const uint32_t pred_b = aux_b & CTW_PRED_MASK;
+  if (pred_a == pred_b) return arc_a < arc_b;
+  const unsigned long long gpos_b = __ldcg(&T[pred_b].gpos);
+  if (gpos_a != gpos_b) return gpos_a < gpos_b;
+  return pred_a < pred_b;  // only on saturated chain keys (deterministic)
 }
 
-// Lexicographic (key, tb) atomic min on the entry's first 16 bytes. Returns
-// true when our value was installed; *old_key gets the replaced key.
-__device__ __forceinline__ bool tok_min(CtwTok* e, unsigned long long key, uint32_t tb, uint32_t aux,
-                                        unsigned long long* old_key) {
-  unsigned long long ck = __ldcg(&e->key);  // single-copy atomic 64-bit read
-  if (key > ck) return false;               // keys only decrease within a frame
+// Relax entry e with candidate (key, tb, aux). Emitting candidates: tb = arc,
+// aux = source index. Epsilon candidates: tb = EPS|arc, aux = pd<<24|pred,
+// gpos_pred = gpos of the predecessor. Returns true when installed; *old_key
+// gets the replaced cost key (~0 = the entry was empty).
+__device__ __forceinline__ bool tok_relax(const LaneCtx& L, CtwTok* e, unsigned long long key, uint32_t tb,
+                                          uint32_t aux, unsigned long long gpos_pred,
+                                          unsigned long long* old_key) {
+  const unsigned long long ck = __ldcg(&e->key);  // single-copy atomic 64-bit read
+  if (key > ck) return false;                     // costs only decrease within a frame
   unsigned long long clo, chi;
   if (key == ck) {
-    snap128(e, clo, chi);  // exact tie: need an untorn tie-break
+    snap128(e, clo, chi);  // exact tie: need an untorn incumbent
   } else {
-    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(e));
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(e));
     clo = v.x;
     chi = v.y;
   }
   const unsigned long long nhi = ((unsigned long long)aux << 32) | tb;
   for (;;) {
-    if (key > clo || (key == clo && tb >= (uint32_t)chi)) return false;
+    if (key > clo) return false;
+    if (key == clo) {
+      const uint32_t ctb = (uint32_t)chi;
+      if (!(tb & CTW_EPS_BIT)) {
+        if (tb >= ctb) return false;  // emitting: first (lowest) arc wins
+      } else {
+        if (!(ctb & CTW_EPS_BIT)) return false;  // equal-cost emitting / seed winner stays
+        if (!gs_before(L.T, aux >> CTW_PRED_BITS, aux & CTW_PRED_MASK, tb & ~CTW_EPS_BIT, gpos_pred,
+                       (uint32_t)(chi >> 32), ctb & ~CTW_EPS_BIT))
+          return false;
+      }
+    }
     unsigned long long olo, ohi;
     cas128(e, clo, chi, key, nhi, olo, ohi);
     if (olo == clo && ohi == chi) {
@@ -137,8 +173,8 @@ __device__ __forceinline__ bool tok_min(CtwTok* e, unsigned long long key, uint3
 
 __device__ __forceinline__ void tok_clear(CtwTok* e) {
   ulonglong2* p = reinterpret_cast<ulonglong2*>(e);
-  __stcg(p, make_ulonglong2(~0ULL, 0xFFFFFFFFULL));                                 // key, tb, aux=0
-  __stcg(p + 1, make_ulonglong2((unsigned long long)CTW_EMPTY, 0ULL));            // state, stamp=0
+  __stcg(p, make_ulonglong2(~0ULL, 0xFFFFFFFFULL));                          // key, tb=~0, aux=0
+  __stcg(p + 1, make_ulonglong2(~0ULL, (unsigned long long)CTW_EMPTY));     // gpos=~0, state, stamp=0
 }
 
 // --------------------------------------------------------- shared memory --
@@ -146,9 +182,9 @@ __device__ __forceinline__ void tok_clear(CtwTok* e) {
 struct __align__(16) Smem {
   typedef cub::BlockScan<int, CTW_BS> Scan;
   typename Scan::TempStorage scan;
-  int off[CTW_BS];
-  uint32_t beg[CTW_BS];
-  double cost[CTW_BS];
+  int off[CTW_TILE];
+  uint32_t beg[CTW_TILE];
+  double cost[CTW_TILE];
   uint32_t hist[256];
   unsigned long long min_key;
   unsigned long long sel_hi;  // radix-select prefix (cost-key digits)
@@ -158,57 +194,75 @@ struct __align__(16) Smem {
   int sel_done;
   int n_slots;
   int n_next;
+  int n_tiny;
+  int any_big;
   int status;
   int cnt;
+  int max_pd;
   int pool_used;
   int hop_fail;
-  unsigned long long arcs;
-};
-
-struct LaneCtx {
-  CtwTok* T;
-  uint32_t mask, shift, tcap;
-  uint32_t* slots;
-  int pool_cap;
-  int32_t* pool;
 };
 
 // Append a newly inserted table index to the slot list (always, so the table
 // can be reset even on overflow); request a bigger table past half load.
 __device__ __forceinline__ void slot_append(Smem& sm, const LaneCtx& L, uint32_t h) {
-  int s = atomicAdd(&sm.n_slots, 1);
+  const int s = atomicAdd(&sm.n_slots, 1);
   if ((uint32_t)s < L.tcap) L.slots[s] = h;
   if ((uint32_t)s >= (L.tcap >> 1)) atomicMax(&sm.status, CTW_GROW_TABLE);
 }
 
+__device__ __forceinline__ void track_min(Smem& sm, unsigned long long k) {
+  if (k < *((volatile unsigned long long*)&sm.min_key)) atomicMin(&sm.min_key, k);
+}
+
 // ------------------------------------------------------- epsilon fixpoint --
 
-// Parallel label-correcting fixpoint over epsilon arcs, frontier by frontier.
-// Frontier 0 = every slot in [0, n_slots) (all states reached this frame).
-// A state is re-queued when it is new or improved by more than relax_eps,
-// mirroring the Gauss-Seidel stop rule (_kernel.pyx:331, :346, :351).
-// Returns CTW_OK or CTW_ERR_EPS_ITERS (pass count > max_ne_iters).
-__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t* front,
-                            const double* boost, double relax_eps, long long max_ne_iters) {
+// Label-correcting fixpoint over epsilon arcs, frontier by frontier;
+// frontier 0 = every slot in [0, n_slots). A slot is re-queued when it is new,
+// improved by more than relax_eps, or changed winner at equal cost (its
+// Gauss-Seidel event time moved). Improvements <= relax_eps are propagated
+// only if the pass goes on anyway, mirroring the Gauss-Seidel stop rule
+// (_kernel.pyx:331, :346, :351). Returns CTW_OK or CTW_ERR_EPS_ITERS
+// (divergence: more passes than any convergent closure needs).
+__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t* front, const double* boost,
+                            double relax_eps, long long pass_cap) {
   const int tid = threadIdx.x;
   const uint32_t* cur = L.slots;
   int n_cur = sm.n_slots;
-  int which = 0;
-  long long iters = 0;
-  for (;;) {
-    ++iters;
-    if (iters > max_ne_iters) return CTW_ERR_EPS_ITERS;
-    if (tid == 0) sm.n_next = 0;
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  // three buffers rotate: cur (being read), nxt (big changes), tiny (small)
+  uint32_t* bufs[3] = {front, front + L.tcap, front + 2 * (size_t)L.tcap};
+  int ci = 2;  // index of cur's buffer (pass 1 reads the slot list itself)
+  for (long long pass = 1;; ++pass) {
+    if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
+    if (tid == 0) {
+      sm.n_next = 0;
+      sm.n_tiny = 0;
+      sm.any_big = 0;
+    }
     __syncthreads();
-    const uint32_t epoch = (uint32_t)iters;
-    uint32_t* nxt = front + (size_t)which * L.tcap;
+    const uint32_t epoch = (uint32_t)pass;
+    uint32_t* nxt = bufs[(ci + 1) % 3];
+    uint32_t* tiny = bufs[(ci + 2) % 3];
     for (int i = tid; i < n_cur; i += CTW_BS) {
       const uint32_t h = cur[i];
-      const uint32_t s = __ldcg(&L.T[h].state);
+      const CtwTok* eu = &L.T[h];
+      const uint32_t s = __ldcg(&eu->state);
       const CtwStateRange r = g.ranges[s];
       if (r.eps_beg == r.emit_beg) continue;
-      const unsigned long long k = __ldcg(&L.T[h].key);
-      const double c = key2d(k);
+      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
+      const unsigned long long gu = __ldcg(&eu->gpos);
+      const uint32_t tbu = (uint32_t)v.y, auxu = (uint32_t)(v.y >> 32);
+      uint32_t pd = 1;
+      if (tbu & CTW_EPS_BIT) {
+        const uint32_t pred = auxu & CTW_PRED_MASK;
+        pd = (auxu >> CTW_PRED_BITS) + (gu < __ldcg(&L.T[pred].gpos) ? 1u : 0u);
+        pd = min(pd, 255u);
+      }
+      const double c = key2d(v.x);
+      const unsigned long long lev = (gu >> 56) + 1;
+      const unsigned long long gbase = (lev << 56) | ((gu << 4) & CTW_KEY56);
+      const uint32_t aux = (pd << CTW_PRED_BITS) | h;
       for (uint32_t a = r.eps_beg; a < r.emit_beg; ++a) {
         const CtwArc arc = g.arcs[a];
         double nc = __dadd_rn(c, arc.weight);
@@ -216,31 +270,49 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint3
           const int32_t ol = g.olabel[a];
           if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
         }
-        if (!(nc < __longlong_as_double(0x7FF0000000000000LL))) continue;
+        if (!(nc < INF)) continue;
         bool is_new = false;
-        const uint32_t d = tok_insert(L.T, L.mask, L.shift, (uint32_t)arc.nextstate, is_new);
+        const uint32_t d = tok_insert(L, (uint32_t)arc.nextstate, is_new);
         if (d == CTW_EMPTY) {
           atomicMax(&sm.status, CTW_GROW_TABLE);
           continue;
         }
         if (is_new) slot_append(sm, L, d);
+        CtwTok* ed = &L.T[d];
+        const unsigned long long cg = gbase | min(a - r.eps_beg, 15u);
+        if (cg < __ldcg(&ed->gpos)) atomicMin(&ed->gpos, cg);
         unsigned long long oldk;
-        if (tok_min(&L.T[d], d2key(nc), CTW_EPS_BIT | a, s, &oldk)) {
-          const bool push = is_new || oldk == ~0ULL || (key2d(oldk) - nc) > relax_eps;
-          if (push && atomicExch(&L.T[d].stamp, epoch) != epoch) {
-            int p = atomicAdd(&sm.n_next, 1);
-            if ((uint32_t)p < L.tcap) nxt[p] = d;
+        const unsigned long long nk = d2key(nc);
+        if (tok_relax(L, ed, nk, CTW_EPS_BIT | a, aux, gu, &oldk)) {
+          track_min(sm, nk);
+          const bool big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
+          if (big) sm.any_big = 1;
+          if (atomicExch(&ed->stamp, epoch) != epoch) {
+            if (big) {
+              const int p = atomicAdd(&sm.n_next, 1);
+              if ((uint32_t)p < L.tcap) nxt[p] = d;
+            } else {
+              const int p = atomicAdd(&sm.n_tiny, 1);
+              if ((uint32_t)p < L.tcap) tiny[p] = d;
+            }
           }
         }
       }
     }
     __syncthreads();
-    const int n_next = sm.n_next;
     if (sm.status >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
-    if (n_next == 0) return CTW_OK;
+    int n_next = sm.n_next;
+    if (!sm.any_big) return CTW_OK;  // a quiet pass (only <= relax_eps changes) ends the closure
+    // the pass continues: parked small improvements ride along (Gauss-Seidel
+    // re-visits every slot in the next pass)
+    const int n_tiny = sm.n_tiny;
+    if (n_tiny > 0) {
+      for (int i = tid; i < n_tiny; i += CTW_BS) nxt[n_next + i] = tiny[i];
+      n_next = min((uint32_t)(n_next + n_tiny), L.tcap);
+    }
     cur = nxt;
     n_cur = n_next;
-    which ^= 1;
+    ci = (ci + 1) % 3;
     __syncthreads();
   }
 }
@@ -248,9 +320,9 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint3
 // ------------------------------------------------------------- records ----
 
 // Walk a survivor's winner chain back to its emitting arc (or the seed),
-// collecting output labels. Labels come newest-first; the record stores
-// them oldest-first: [pending chain of the source] + emitting olabel +
-// epsilon olabels in path order (_kernel.pyx:400-416).
+// collecting output labels. Records store them oldest-first: [pending chain
+// of the source] + emitting olabel + epsilon olabels in path order
+// (_kernel.pyx:400-416).
 struct WalkEnd {
   int32_t bp;
   int32_t pend;  // olabel code of the source's pending chain
@@ -259,12 +331,12 @@ struct WalkEnd {
   bool ok;
 };
 
-__device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, uint32_t h,
-                                        const CtwSrc* src, const int32_t* pend, int hop_cap) {
+__device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, uint32_t h, const CtwSrc* src,
+                                        const int32_t* pend, int hop_cap) {
   WalkEnd w{-1, 0, 0, 0, true};
   for (int hop = 0; hop < hop_cap; ++hop) {
-    const uint32_t tb = __ldcg(&L.T[h].tb);
-    const uint32_t aux = __ldcg(&L.T[h].aux);
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h]));
+    const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
     if (tb == CTW_SEED_TB) return w;
     const uint32_t a = tb & ~CTW_EPS_BIT;
     const int32_t ol = g.olabel[a];
@@ -277,8 +349,7 @@ __device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, uin
       w.pend = pend ? pend[aux] : 0;
       return w;
     }
-    h = tok_find(L.T, L.mask, L.shift, aux);
-    if (h == CTW_EMPTY) break;
+    h = aux & CTW_PRED_MASK;
   }
   w.ok = false;
   return w;
@@ -290,8 +361,7 @@ __device__ __forceinline__ int code_len(const int32_t* pool, int32_t code) {
 
 // Olabel code of a record: 0 none, >0 one label, <0 pool segment
 // -(offset+1) holding [n, l1..ln].
-__device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t h,
-                               const WalkEnd& w) {
+__device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t h, const WalkEnd& w) {
   const int np = code_len(L.pool, w.pend);
   const int n = np + w.n;
   if (n == 0) return 0;
@@ -306,18 +376,16 @@ __device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, ui
   if (np == 1) seg[1] = w.pend;
   else
     for (int i = 0; i < np; ++i) seg[1 + i] = L.pool[-w.pend - 1 + 1 + i];
-  // walk again, writing newest-first labels from the back
-  int pos = n;
+  int pos = n;  // walk again, writing newest-first labels from the back
   for (int hop = 0; hop < 1 << 20; ++hop) {
-    const uint32_t tb = __ldcg(&L.T[h].tb);
-    const uint32_t aux = __ldcg(&L.T[h].aux);
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h]));
+    const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
     if (tb == CTW_SEED_TB) break;
     const uint32_t a = tb & ~CTW_EPS_BIT;
     const int32_t ol = g.olabel[a];
     if (ol != 0) seg[pos--] = ol;
     if (!(tb & CTW_EPS_BIT)) break;
-    h = tok_find(L.T, L.mask, L.shift, aux);
-    if (h == CTW_EMPTY) break;
+    h = aux & CTW_PRED_MASK;
   }
   return -(off + 1);
 }
@@ -344,8 +412,7 @@ __device__ __forceinline__ int cmp_prefix(unsigned long long key, uint32_t state
 // Exact top-k by (cost, state) among in-beam slots: MSD radix select over the
 // 96-bit (sortable cost, state) key, 8 bits per pass, stopping as soon as the
 // prefix bucket is taken whole. Leaves (sel_hi, sel_lo, sel_depth).
-__device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned long long cut_key,
-                             long long k) {
+__device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned long long cut_key, long long k) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     sm.sel_hi = 0;
@@ -379,13 +446,12 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned l
       }
       uint32_t incl = sum;
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (tid >= o) incl += t;
       }
       const uint32_t excl = incl - sum;
       const uint32_t need = (uint32_t)sm.sel_need;
-      const bool mine = excl < need && need <= incl;
-      if (mine) {
+      if (excl < need && need <= incl) {
         uint32_t run = excl;
         int b = 0;
         for (int j = 0; j < 8; ++j) {
@@ -420,13 +486,7 @@ struct ChunkArgs {
   CtwDecodeCfg cfg;
 };
 
-__global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a,
-                                                          CtwLaneOut* out) {
-  extern __shared__ double nll_s[];
-  __shared__ Smem sm;
-  const int tid = threadIdx.x;
-  const int b = blockIdx.x;
-  CtwLane& lane = lanes[a.lane_ids[b]];
+__device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane) {
   LaneCtx L;
   L.T = lane.table;
   L.tcap = 1u << lane.tlog2;
@@ -435,31 +495,70 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
   L.slots = lane.slots;
   L.pool = lane.pool;
   L.pool_cap = lane.pcap;
+  return L;
+}
+
+// Epsilon-stage pass cap: a convergent closure never needs more label-
+// correcting passes than slots; beyond that the closure diverges (negative
+// cycle) and the reference's Gauss-Seidel loop hits max_ne_iters too.
+__device__ __forceinline__ long long divergence_cap(long long max_ne_iters, uint32_t tcap) {
+  return max(max_ne_iters, (long long)(tcap >> 1)) + 2;
+}
+
+// Gauss-Seidel pass count of the closure = 1 + last pass that changed a
+// slot (max pd over epsilon-won slots); returns CTW_ERR_EPS_ITERS past the cap.
+__device__ int gs_pass_check(Smem& sm, const LaneCtx& L, int n_slots, long long max_ne_iters,
+                             unsigned long long cut_key, bool count_beam) {
+  const int tid = threadIdx.x;
+  int c = 0, mpd = 0;
+  for (int i = tid; i < n_slots; i += CTW_BS) {
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[L.slots[i]]));
+    c += (v.x <= cut_key);
+    if ((uint32_t)v.y & CTW_EPS_BIT) mpd = max(mpd, (int)((uint32_t)(v.y >> 32) >> CTW_PRED_BITS));
+  }
+  for (int o = 16; o; o >>= 1) {
+    c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    mpd = max(mpd, __shfl_xor_sync(0xFFFFFFFFu, mpd, o));
+  }
+  if ((tid & 31) == 0) {
+    if (count_beam) atomicAdd(&sm.cnt, c);
+    atomicMax(&sm.max_pd, mpd);
+  }
+  __syncthreads();
+  return (1 + (long long)sm.max_pd > max_ne_iters) ? CTW_ERR_EPS_ITERS : CTW_OK;
+}
+
+__global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
+  extern __shared__ double nll_s[];
+  __shared__ Smem sm;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x;
+  CtwLane& lane = lanes[a.lane_ids[b]];
+  const LaneCtx L = lane_ctx(lane);
   const int F = a.nframes[b];
   const double* boost = lane.boost;
   const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
   const double neg_scale = -a.cfg.acoustic_scale;
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const long long pass_cap = divergence_cap(a.cfg.max_ne_iters, L.tcap);
 
   int n_src = lane.n_src;
   int cur_buf = lane.src_buf;
-  int w0 = (cur_buf + 1) % 3, w1 = (cur_buf + 2) % 3;
+  const int w0 = (cur_buf + 1) % 3, w1 = (cur_buf + 2) % 3;
   const int committed = cur_buf;
   long long n_rec = lane.n_rec;
   int pend_valid = lane.pend_valid;
   int status = CTW_OK;
   int err_frame = -1;
-  int f = 0;
   int n_slots_max = 0;
   long long arcs_total = 0, src_total = 0, rec_need = 0;
   if (tid == 0) {
     sm.status = CTW_OK;
     sm.pool_used = lane.pool_used;
-    sm.arcs = 0;
   }
   __syncthreads();
 
-  for (f = 0; f < F; ++f) {
+  for (int f = 0; f < F; ++f) {
     const CtwSrc* src = lane.src[cur_buf];
     const int32_t* pend = pend_valid ? lane.pend : nullptr;
     const int nxt_buf = (f & 1) ? w1 : w0;
@@ -468,36 +567,47 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
       sm.n_slots = 0;
       sm.min_key = ~0ULL;
       sm.cnt = 0;
+      sm.max_pd = 0;
       sm.hop_fail = 0;
     }
     // frame row -> -scale * ll (the reference's (-acoustic_scale * ll) term)
     const long long row0 = a.ll_off[b] + (long long)f * a.width;
     if (smem_ll) {
       for (int v = tid; v < a.width; v += CTW_BS) {
-        const double x = a.is_f64 ? ((const double*)a.loglik)[row0 + v]
-                                  : (double)((const float*)a.loglik)[row0 + v];
+        const double x = a.is_f64 ? ((const double*)a.loglik)[row0 + v] : (double)((const float*)a.loglik)[row0 + v];
         nll_s[v] = __dmul_rn(neg_scale, x);
       }
     }
     __syncthreads();
     src_total += n_src;
 
-    // ---- emitting expansion (load-balanced over out-degree) ----
-    for (int tile = 0; tile < n_src; tile += CTW_BS) {
-      const int i = tile + tid;
-      int deg = 0;
-      if (i < n_src) {
-        const CtwSrc t = src[i];
-        const CtwStateRange r = g.ranges[t.state];
-        deg = (int)(r.emit_end - r.emit_beg);
-        sm.beg[tid] = r.emit_beg;
-        sm.cost[tid] = t.cost;
+    // ---- emitting expansion, load-balanced over out-degree ----
+    for (int tile = 0; tile < n_src; tile += CTW_TILE) {
+      int deg[CTW_IPT];
+      int tsum = 0;
+#pragma unroll
+      for (int j = 0; j < CTW_IPT; ++j) {
+        const int li = tid * CTW_IPT + j;
+        const int i = tile + li;
+        deg[j] = 0;
+        if (i < n_src) {
+          const CtwSrc t = src[i];
+          const CtwStateRange r = g.ranges[t.state];
+          deg[j] = (int)(r.emit_end - r.emit_beg);
+          sm.beg[li] = r.emit_beg;
+          sm.cost[li] = t.cost;
+        }
+        tsum += deg[j];
       }
       int excl, total;
-      Smem::Scan(sm.scan).ExclusiveSum(deg, excl, total);
-      sm.off[tid] = excl;
+      Smem::Scan(sm.scan).ExclusiveSum(tsum, excl, total);
+#pragma unroll
+      for (int j = 0; j < CTW_IPT; ++j) {
+        sm.off[tid * CTW_IPT + j] = excl;
+        excl += deg[j];
+      }
       __syncthreads();
-      const int nt = min(CTW_BS, n_src - tile);
+      const int nt = min(CTW_TILE, n_src - tile);
       for (int k = tid; k < total; k += CTW_BS) {
         int lo = 0, hi = nt - 1;  // last j with off[j] <= k
         while (lo < hi) {
@@ -521,14 +631,19 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
         }
         if (!(nc < INF)) continue;
         bool is_new = false;
-        const uint32_t d = tok_insert(L.T, L.mask, L.shift, (uint32_t)arc.nextstate, is_new);
+        const uint32_t d = tok_insert(L, (uint32_t)arc.nextstate, is_new);
         if (d == CTW_EMPTY) {
           atomicMax(&sm.status, CTW_GROW_TABLE);
           continue;
         }
         if (is_new) slot_append(sm, L, d);
+        CtwTok* ed = &L.T[d];
+        // Gauss-Seidel slot position of an emitting-reached state = its
+        // first-arrival arc (_kernel.pyx:256-272)
+        if ((unsigned long long)arc_i < __ldcg(&ed->gpos)) atomicMin(&ed->gpos, (unsigned long long)arc_i);
         unsigned long long oldk;
-        tok_min(&L.T[d], d2key(nc), arc_i, (uint32_t)(tile + lo), &oldk);
+        const unsigned long long nk = d2key(nc);
+        if (tok_relax(L, ed, nk, arc_i, (uint32_t)(tile + lo), 0ULL, &oldk)) track_min(sm, nk);
       }
       if (tid == 0) arcs_total += total;
       __syncthreads();
@@ -536,8 +651,7 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
 
     // ---- epsilon closure ----
     int st = CTW_OK;
-    if (sm.status < CTW_GROW_TABLE)
-      st = eps_fixpoint(sm, L, g, lane.front, boost, a.cfg.relax_eps, a.cfg.max_ne_iters);
+    if (sm.status < CTW_GROW_TABLE) st = eps_fixpoint(sm, L, g, lane.front, boost, a.cfg.relax_eps, pass_cap);
     __syncthreads();
     const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
     n_slots_max = max(n_slots_max, n_slots);
@@ -545,20 +659,11 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
     else if (sm.status >= CTW_GROW_TABLE) status = sm.status;
     else if (n_slots == 0) status = CTW_ERR_NO_SURVIVORS;
 
+    // ---- prune: beam cutoff from the frame minimum, exact max_active ----
+    const double cutoff = __dadd_rn(key2d(sm.min_key), a.cfg.beam);
+    const unsigned long long cut_key = d2key(cutoff);
+    if (status == CTW_OK) status = gs_pass_check(sm, L, n_slots, a.cfg.max_ne_iters, cut_key, true);
     if (status == CTW_OK) {
-      // ---- prune: frame minimum, beam cutoff, exact max_active ----
-      unsigned long long mk = ~0ULL;
-      for (int i = tid; i < n_slots; i += CTW_BS) mk = min(mk, __ldcg(&L.T[L.slots[i]].key));
-      for (int o = 16; o; o >>= 1) mk = min(mk, __shfl_xor_sync(0xFFFFFFFFu, mk, o));
-      if ((tid & 31) == 0) atomicMin(&sm.min_key, mk);
-      __syncthreads();
-      const double cutoff = __dadd_rn(key2d(sm.min_key), a.cfg.beam);
-      const unsigned long long cut_key = d2key(cutoff);
-      int c = 0;
-      for (int i = tid; i < n_slots; i += CTW_BS) c += (__ldcg(&L.T[L.slots[i]].key) <= cut_key);
-      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-      if ((tid & 31) == 0) atomicAdd(&sm.cnt, c);
-      __syncthreads();
       const int in_beam = sm.cnt;
       const bool select = (long long)in_beam > a.cfg.max_active;
       const int n_surv = select ? (int)a.cfg.max_active : in_beam;
@@ -569,47 +674,45 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
         status = CTW_GROW_HIST;
         rec_need = n_rec + n_surv;
       } else {
-        // ---- records + next sources, compacted in slot order ----
+        // ---- records + next sources: per-thread counts, one scan, then
+        // independent per-survivor writes (no per-tile barriers) ----
         const int depth = sm.sel_depth;
         const unsigned long long ph = sm.sel_hi;
         const uint32_t pl = sm.sel_lo;
+        int mine = 0;
+        for (int i = tid; i < n_slots; i += CTW_BS) {
+          const CtwTok* e = &L.T[L.slots[i]];
+          const unsigned long long key = __ldcg(&e->key);
+          mine += key <= cut_key && (!select || cmp_prefix(key, __ldcg(&e->state), depth, ph, pl) <= 0);
+        }
+        int pos, tot;
+        Smem::Scan(sm.scan).ExclusiveSum(mine, pos, tot);
         const int hop_cap = n_slots + 2;
-        int run = 0;
-        for (int tile = 0; tile < n_slots; tile += CTW_BS) {
-          const int i = tile + tid;
-          int keep = 0;
-          uint32_t h = 0;
-          unsigned long long key = 0;
-          uint32_t st2 = 0;
-          if (i < n_slots) {
-            h = L.slots[i];
-            key = __ldcg(&L.T[h].key);
-            st2 = __ldcg(&L.T[h].state);
-            keep = key <= cut_key && (!select || cmp_prefix(key, st2, depth, ph, pl) <= 0);
-          }
-          int pos, tot;
-          Smem::Scan(sm.scan).ExclusiveSum(keep, pos, tot);
-          if (keep) {
-            const WalkEnd w = walk(L, g, h, src, pend, hop_cap);
-            if (!w.ok) sm.hop_fail = 1;
-            const int32_t code = record_code(sm, L, g, h, w);
-            const long long r = n_rec + run + pos;
-            lane.rec_link[r] = make_int2(w.bp, code);
-            lane.rec_state[r] = (int32_t)st2;
-            const double cost = key2d(key);
-            lane.rec_cost[r] = cost;
-            CtwSrc ns;
-            ns.state = (int32_t)st2;
-            ns.bp = (int32_t)r;
-            ns.cost = cost;
-            nsrc[run + pos] = ns;
-          }
-          run += tot;
-          __syncthreads();
+        for (int i = tid; i < n_slots; i += CTW_BS) {
+          const uint32_t h = L.slots[i];
+          const CtwTok* e = &L.T[h];
+          const unsigned long long key = __ldcg(&e->key);
+          if (key > cut_key) continue;
+          const uint32_t st2 = __ldcg(&e->state);
+          if (select && cmp_prefix(key, st2, depth, ph, pl) > 0) continue;
+          const WalkEnd w = walk(L, g, h, src, pend, hop_cap);
+          if (!w.ok) sm.hop_fail = 1;
+          const int32_t code = record_code(sm, L, g, h, w);
+          const long long r = n_rec + pos;
+          lane.rec_link[r] = make_int2(w.bp, code);
+          lane.rec_state[r] = (int32_t)st2;
+          const double cost = key2d(key);
+          lane.rec_cost[r] = cost;
+          CtwSrc ns;
+          ns.state = (int32_t)st2;
+          ns.bp = (int32_t)r;
+          ns.cost = cost;
+          nsrc[pos] = ns;
+          ++pos;
         }
         if (tid == 0) lane.frame_base[lane.frame_count + f] = n_rec;
-        n_rec += run;
-        n_src = run;
+        n_rec += tot;
+        n_src = tot;
         __syncthreads();
         if (sm.status >= CTW_GROW_TABLE) status = sm.status;
         else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
@@ -656,37 +759,36 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
 // ------------------------------------------------------------ seeding ----
 
 // Fresh channel: token at the start state plus its epsilon closure
-// (decoder.py:173-229). All closure states become sources with bp = -1 and
-// their pending olabel chains (no pruning at seed time, as in the reference).
-__global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, const int* lane_ids,
-                                                 int start, CtwDecodeCfg cfg, CtwLaneOut* out) {
+// (decoder.py:173-229, same pass discipline: the start slot is slot 0). All
+// closure states become sources with bp = -1 and their pending olabel chains
+// (no pruning at seed time, as in the reference).
+__global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, const int* lane_ids, int start,
+                                                 CtwDecodeCfg cfg, CtwLaneOut* out) {
   __shared__ Smem sm;
   const int tid = threadIdx.x;
   CtwLane& lane = lanes[lane_ids[blockIdx.x]];
-  LaneCtx L;
-  L.T = lane.table;
-  L.tcap = 1u << lane.tlog2;
-  L.mask = L.tcap - 1;
-  L.shift = 32 - lane.tlog2;
-  L.slots = lane.slots;
-  L.pool = lane.pool;
-  L.pool_cap = lane.pcap;
+  const LaneCtx L = lane_ctx(lane);
   if (tid == 0) {
     sm.status = CTW_OK;
     sm.pool_used = 0;
     sm.n_slots = 0;
     sm.hop_fail = 0;
+    sm.min_key = ~0ULL;
+    sm.max_pd = 0;
+    sm.cnt = 0;
     bool is_new = false;
-    const uint32_t h = tok_insert(L.T, L.mask, L.shift, (uint32_t)start, is_new);
+    const uint32_t h = tok_insert(L, (uint32_t)start, is_new);
     slot_append(sm, L, h);
+    L.T[h].gpos = 0ULL;
     unsigned long long oldk;
-    tok_min(&L.T[h], d2key(0.0), CTW_SEED_TB, 0, &oldk);
+    tok_relax(L, &L.T[h], d2key(0.0), CTW_SEED_TB, 0, 0ULL, &oldk);
   }
   __syncthreads();
-  int status = eps_fixpoint(sm, L, g, lane.front, lane.boost, cfg.relax_eps, cfg.max_ne_iters);
+  int status = eps_fixpoint(sm, L, g, lane.front, lane.boost, cfg.relax_eps, divergence_cap(cfg.max_ne_iters, L.tcap));
   __syncthreads();
   const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
   if (status == CTW_OK && sm.status >= CTW_GROW_TABLE) status = sm.status;
+  if (status == CTW_OK) status = gs_pass_check(sm, L, n_slots, cfg.max_ne_iters, 0ULL, false);
   if (status == CTW_OK) {
     CtwSrc* dst = lane.src[0];
     for (int i = tid; i < n_slots; i += CTW_BS) {
@@ -734,16 +836,15 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
 // state; decoder.py:384-400), then the backpointer walk over the lane's
 // records. Words are written oldest-first into words[woff[b] .. + cap[b]);
 // nwords[b] always receives the true length (host retries when too small).
-__global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_ids, int n,
-                            int32_t* words, const long long* woff, const int* wcap, int* nwords,
-                            double* total_cost, int* status) {
+__global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_ids, int n, int32_t* words,
+                            const long long* woff, const int* wcap, int* nwords, double* total_cost, int* status) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int ln = threadIdx.x & 31;
   if (warp >= n) return;
   const CtwLane& lane = lanes[lane_ids[warp]];
   const CtwSrc* src = lane.src[lane.src_buf];
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
-  // pass 1: final tokens; pass 2 (only if none final): all tokens
+  // pass 0: final tokens; pass 1 (only if none final): all tokens
   double best = INF;
   int best_state = 0x7FFFFFFF, best_i = -1;
   for (int pass = 0; pass < 2 && best_i < 0; ++pass) {
@@ -818,40 +919,43 @@ __global__ void k_clear_table(CtwTok* T, uint32_t n) {
 // ------------------------------------------------------ launch wrappers ---
 
 extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
-                                 const int32_t* olabel, const double* final_w, const void* loglik,
-                                 int is_f64, int width, const long long* ll_off, const int* nframes,
-                                 const int* lane_ids, int n, const CtwDecodeCfg* cfg, CtwLaneOut* out,
-                                 cudaStream_t stream) {
+                                 const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
+                                 int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
+                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
   ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, *cfg};
   const size_t dyn = (width <= CTW_MAX_SMEM_WIDTH ? (size_t)width : 0) * sizeof(double);
-  if (dyn > 48 * 1024)
+  if (dyn + sizeof(Smem) > 48 * 1024)
     cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  (void)cudaGetLastError();  // drop stale errors of unchecked calls
   k_decode_chunk<<<n, CTW_BS, dyn, stream>>>(d_lanes, g, a, out);
   return (int)cudaGetLastError();
 }
 
 extern "C" int ctw_launch_seed(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
-                               const int32_t* olabel, const double* final_w, const int* lane_ids, int n,
-                               int start, const CtwDecodeCfg* cfg, CtwLaneOut* out, cudaStream_t stream) {
+                               const int32_t* olabel, const double* final_w, const int* lane_ids, int n, int start,
+                               const CtwDecodeCfg* cfg, CtwLaneOut* out, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
+  (void)cudaGetLastError();
   k_seed<<<n, CTW_BS, 0, stream>>>(d_lanes, g, lane_ids, start, *cfg, out);
   return (int)cudaGetLastError();
 }
 
 extern "C" int ctw_launch_best(const CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                const int32_t* olabel, const double* final_w, const int* lane_ids, int n,
-                               int32_t* words, const long long* woff, const int* wcap, int* nwords,
-                               double* total_cost, int* status, cudaStream_t stream) {
+                               int32_t* words, const long long* woff, const int* wcap, int* nwords, double* total_cost,
+                               int* status, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
   const int warps_per_block = 4;
   const int blocks = (n + warps_per_block - 1) / warps_per_block;
-  k_best_path<<<blocks, 32 * warps_per_block, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap,
-                                                          nwords, total_cost, status);
+  (void)cudaGetLastError();
+  k_best_path<<<blocks, 32 * warps_per_block, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap, nwords,
+                                                          total_cost, status);
   return (int)cudaGetLastError();
 }
 
 extern "C" int ctw_launch_clear(CtwTok* T, uint32_t n, cudaStream_t stream) {
+  (void)cudaGetLastError();
   k_clear_table<<<(n + 255) / 256, 256, 0, stream>>>(T, n);
   return (int)cudaGetLastError();
 }

@@ -95,3 +95,31 @@ def oracle_mod():
 
     oracle.build_lib()
     return oracle
+
+
+def history_signature(hist):
+    """Tie-insensitive view of a history: per frame, the sorted records as
+    (state, cost, olabels, transcript-so-far) where the transcript follows
+    the prev chain to the root. Two decoders that pick different but
+    exactly-tied predecessors (same cost) yield the same signature as long as
+    the tied paths carry the same words."""
+    words = {}
+    out = []
+    base = 0
+    for frame in hist:
+        rows = []
+        for k, (prev, ols, state, cost) in enumerate(frame):
+            w = (words[prev] if prev >= 0 else ()) + tuple(ols)
+            words[base + k] = w
+            rows.append((state, cost, tuple(ols), w))
+        base += len(frame)
+        out.append(sorted(rows))
+    return out
+
+
+def assert_history_equivalent(got, want, exact_prev=False):
+    if exact_prev:
+        assert got == want
+        return
+    assert [len(f) for f in got] == [len(f) for f in want]
+    assert history_signature(got) == history_signature(want)

@@ -3,8 +3,14 @@ the CPU oracle (oracle/ctw_oracle.c, itself pinned in test_oracle.py).
 
 Bar (BASELINE.json north_star): best-path words bit-exact, best-path cost
 within 1e-4 relative. The GPU computes in IEEE f64 with the reference's
-operation order, so these tests demand MORE: identical per-frame history
-records (prev, olabels, state, cost) and bit-identical costs.
+operation order, so these tests demand MORE: bit-identical costs and, per
+frame, the identical record set (state, cost, olabels) with an identical
+transcript behind every record. Predecessor indices are compared exactly on
+the tie-free known-answer graphs; elsewhere two predecessors can tie EXACTLY
+in f64 (e.g. "backoff then emit" vs "emit then backoff" over the same
+weights) and the reference's Gauss-Seidel order vs the parallel fixpoint may
+pick different ones -- the signature check proves those ties carry the same
+words (DESIGN.md, "epsilon ties").
 """
 
 import math
@@ -12,7 +18,8 @@ import math
 import numpy as np
 import pytest
 
-from conftest import GoldenGraph, expected_history, golden_chunks, golden_names, load_golden
+from conftest import (GoldenGraph, assert_history_equivalent, expected_history, golden_chunks, golden_names,
+                      load_golden)
 
 pytestmark = pytest.mark.gpu
 
@@ -49,15 +56,17 @@ def _run_golden(d, kernel=None):
     return ch, seed, err
 
 
-def _check_channel(d, ch, seed, err):
+def _check_channel(d, ch, seed, err, name=""):
     from paper_2311_04996_b200 import best_path
 
+    exact = name.startswith("kat_")  # tie-free known-answer graphs: identical prev pointers too
     assert seed == sorted(zip(d["seed_state"].tolist(), d["seed_cost"].tolist()))
     assert err == d["error"]
-    assert ch.history_records() == expected_history(d)
+    assert_history_equivalent(ch.history_records(), expected_history(d), exact_prev=exact)
     assert [t.state for t in ch.active_tokens()] == d["tok_state"].tolist()
     assert [t.cost for t in ch.active_tokens()] == d["tok_cost"].tolist()
-    assert [t.backpointer for t in ch.active_tokens()] == d["tok_bp"].tolist()
+    if exact:
+        assert [t.backpointer for t in ch.active_tokens()] == d["tok_bp"].tolist()
     if d["frame_count"]:
         h = best_path(ch)
         assert list(h.words) == d["best_words"].tolist()
@@ -69,7 +78,7 @@ def _check_channel(d, ch, seed, err):
 def test_golden_native_lane(name):
     d = load_golden(name)
     ch, seed, err = _run_golden(d)
-    _check_channel(d, ch, seed, err)
+    _check_channel(d, ch, seed, err, name)
 
 
 @pytest.mark.parametrize("name", golden_names())
@@ -80,7 +89,7 @@ def test_golden_through_reference_kernel_seam(name):
 
     d = load_golden(name)
     ch, seed, err = _run_golden(d, kernel=kernels.advance_chunk)
-    _check_channel(d, ch, seed, err)
+    _check_channel(d, ch, seed, err, name)
 
 
 def test_golden_decode_batch_one_launch():
@@ -138,7 +147,7 @@ def test_random_systems_history_identical_to_oracle(oracle_mod, seed):
     for i in range(0, 60, step):
         ch.advance_frames(frames[i:i + step])
         oc.advance_frames(frames[i:i + step])
-    assert ch.history_records() == oc.history_records()
+    assert_history_equivalent(ch.history_records(), oc.history_records())
     h = best_path(ch)
     assert (h.words, h.total_cost, h.frame_count) == oc.best_path()
 
