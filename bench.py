@@ -174,6 +174,18 @@ def cpu_model():
 # ------------------------------------------------------------- main -------
 
 
+def _stage_profile(prof, st):
+    """Share of frame-kernel SM cycles per stage (thread-0 clock64 deltas)."""
+    stages = ("emit", "eps", "beam_count", "select", "records", "reset")
+    tot = sum(prof[k] for k in stages) or 1
+    lf = max(1, st["frames"])
+    out = {k: round(prof[k] / tot, 4) for k in stages}
+    out["cycles_per_lane_frame"] = tot / lf
+    out["eps_passes_per_frame"] = prof["eps_passes"] / lf
+    out["select_frame_frac"] = prof["select_frames"] / lf
+    return out
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -267,6 +279,7 @@ def main():
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     st = pool.stats()
+    prof = pool.profile()
     ms = sum(step_ms) / len(step_ms)
     ms_max = ms
     if world > 1:
@@ -337,6 +350,7 @@ def main():
                            "tokens_per_lane_frame": st["src_tokens"] / max(1, st["frames"]),
                            "max_slots": st["max_slots"], "wall_s_timed": t_wall},
         "clocks": clk.summary(),
+        "stage_profile": _stage_profile(prof, st),
     }
     if world == 1 and not args.no_cpu:
         k = min(args.cpu_sample, n)

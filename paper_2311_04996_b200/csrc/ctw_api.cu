@@ -78,6 +78,8 @@ uint32_t ceil_log2(uint64_t x) {
 struct ctw_graph {
   int refs = 1;  // the creator + one per lane set (lanes keep their graph alive)
   int device = 0;
+  bool eps_nonneg = true;  // every epsilon arc weight >= 0
+  bool eps_olabel = false; // some epsilon arc carries an output label (boost applies)
   int64_t S = 0, A = 0, start = 0, max_il = 0, max_ol = 0;
   CtwStateRange* ranges = nullptr;
   CtwArc* arcs = nullptr;
@@ -131,6 +133,7 @@ struct ctw_lanes {
   // stats
   int64_t launches = 0, decode_launches = 0, arcs = 0, srcs = 0, frames = 0, max_slots = 0;
   double decode_ms = 0.0;
+  int64_t prof[CTW_NPROF] = {0, 0, 0, 0, 0, 0, 0, 0};
   std::mutex mu;
 };
 
@@ -164,7 +167,7 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   const uint64_t tcap = 1ull << tlog2;
   const uint64_t scap = tcap / 2 + 1;
   CtwTok* table;
-  uint32_t *slots, *front;
+  uint2 *slots, *front;
   CtwSrc* src[3];
   int32_t* pend;
   CUDA_TRY(dalloc(&table, tcap));
@@ -311,6 +314,18 @@ int reserve_lanes(ctw_lanes* l, int n) {
   return 0;
 }
 
+// Early beam pruning is exact when epsilon increments cannot be negative
+// (see CtwLane::prune_ok); tight user caps on max_ne_iters keep the full
+// Gauss-Seidel pass accounting.
+int32_t prune_flag(const ctw_lanes* l, const double* boost, int64_t len) {
+  const ctw_graph* g = l->g;
+  if (!g->eps_nonneg || l->cfg.max_ne_iters < (1 << 16)) return 0;
+  if (boost && g->eps_olabel)
+    for (int64_t i = 0; i < len; ++i)
+      if (!(boost[i] >= 0.0)) return 0;
+  return 1;
+}
+
 void update_from_out(CtwLane& L, const CtwLaneOut& o) {
   L.n_src = o.n_src;
   L.src_buf = o.src_buf;
@@ -403,6 +418,7 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
     r[s] = CtwStateRange{(uint32_t)off[s], (uint32_t)eps_end[s], (uint32_t)off[s + 1], 0u};
   }
   std::vector<CtwArc> arcs((size_t)std::max<int64_t>(num_arcs, 1));
+  bool eps_nonneg = true, eps_olabel = false;
   for (int64_t s = 0; s < num_states; ++s) {
     for (int64_t a = off[s]; a < off[s + 1]; ++a) {
       const bool eps = a < eps_end[s];
@@ -410,6 +426,10 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
       if (nextstate[a] < 0 || nextstate[a] >= num_states) return fail(-1, "nextstate out of range");
       if (olabel[a] < 0 || ilabel[a] < 0) return fail(-1, "negative label");
       arcs[a] = CtwArc{weight[a], nextstate[a], ilabel[a]};
+      if (eps) {
+        if (!(weight[a] >= 0.0)) eps_nonneg = false;
+        if (olabel[a] != 0) eps_olabel = true;
+      }
       max_il = std::max<int64_t>(max_il, ilabel[a]);
       max_ol = std::max<int64_t>(max_ol, olabel[a]);
     }
@@ -422,6 +442,8 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
   g->max_il = max_il;
   g->max_ol = max_ol;
   g->h_final.assign(final_w, final_w + num_states);
+  g->eps_nonneg = eps_nonneg;
+  g->eps_olabel = eps_olabel;
   auto bail = [&](int code) {
     ctw_graph_destroy(g);
     return code;
@@ -563,6 +585,7 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
       L.boost = nullptr;
       L.boost_len = 0;
     }
+    L.prune_ok = prune_flag(l, b, b ? boost_lens[i] : 0);
     L.n_src = 0;
     L.src_buf = 0;
     L.frame_count = 0;
@@ -601,6 +624,7 @@ int ctw_lane_set_boost(ctw_lanes* l, int32_t lane, const double* boost, int64_t 
     L.boost = nullptr;
     L.boost_len = 0;
   }
+  L.prune_ok = prune_flag(l, boost, boost_len);
   if (int r = sync_lane(l, lane)) return r;
   CUDA_TRY(cudaStreamSynchronize(l->stream));
   return 0;
@@ -704,6 +728,7 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
         status[i] = o.status;
         err_frame[i] = o.err_frame;
         if (o.status == CTW_OK) {
+          for (int k = 0; k < CTW_NPROF; ++k) l->prof[k] += o.prof[k];
           l->arcs += o.arcs_expanded;
           l->srcs += o.src_total;
           l->frames += frames[i];
@@ -968,11 +993,18 @@ int ctw_lanes_stats(ctw_lanes* l, int64_t* launches, int64_t* decode_launches, d
 int ctw_lanes_reset_stats(ctw_lanes* l) {
   std::lock_guard<std::mutex> lk(l->mu);
   l->launches = l->decode_launches = l->arcs = l->srcs = l->frames = l->max_slots = 0;
+  for (int k = 0; k < CTW_NPROF; ++k) l->prof[k] = 0;
   l->decode_ms = 0.0;
   return 0;
 }
 
 void* ctw_lanes_stream(ctw_lanes* l) { return (void*)l->stream; }
+
+int ctw_lanes_profile(ctw_lanes* l, int64_t* out8) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  for (int k = 0; k < CTW_NPROF; ++k) out8[k] = l->prof[k];
+  return 0;
+}
 
 // ------------------------------------------------------------- compat ----
 }  // extern "C"
@@ -1085,6 +1117,7 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
     L.pend_valid = any_pend ? 1 : 0;
     L.boost = dboost;
     L.boost_len = (int32_t)boost_len;
+    L.prune_ok = prune_flag(l, boost, boost_len);
     l->seeded[0] = 1;
     return sync_lane(l, 0);
   };

@@ -80,8 +80,8 @@ struct __align__(16) CtwSrc {
 struct CtwLane {
   // token hash table: capacity 1 << tlog2
   CtwTok* table;
-  uint32_t* slots;   // [tcap]  table index of each slot, discovery order
-  uint32_t* front;   // [2 * tcap] epsilon frontier ping-pong
+  uint2* slots;      // [tcap]  (table index, state) of each slot, discovery order
+  uint2* front;      // [3 * tcap] epsilon frontier buffers (same pairs)
   CtwSrc* src[3];    // [tcap/2 + 1] each: committed + two working buffers
   int32_t* pend;     // [tcap/2 + 1] pending olabel segment of seeded sources
   int2* rec_link;    // [rcap] {prev record, olabel code}
@@ -98,7 +98,10 @@ struct CtwLane {
   int32_t n_src, src_buf, frame_count, pool_used;
   int64_t n_rec;
   int32_t pend_valid;  // committed sources carry pending olabel chains
-  int32_t pad;
+  // 1 = candidates provably outside the final beam may skip value work:
+  // epsilon increments are >= 0 (graph weights and, when epsilon arcs carry
+  // olabels, the boost) and max_ne_iters is not a tight cap. Set by the host.
+  int32_t prune_ok;
 };
 
 // Per-launch result of one lane.
@@ -112,7 +115,13 @@ struct CtwLaneOut {
   int64_t arcs_expanded;  // diagnostics: emitting arcs relaxed (E_emit)
   int64_t src_total;      // diagnostics: sum of sources over frames (N_src)
   int64_t rec_need;       // CTW_GROW_HIST: records needed through the failing frame
+  // stage profile (SM cycles summed over the chunk's frames, thread 0):
+  // [0] emitting expansion, [1] epsilon closure, [2] beam count + pass check,
+  // [3] max-active select, [4] records, [5] table reset, [6] epsilon passes,
+  // [7] frames that needed the select
+  int64_t prof[8];
 };
+#define CTW_NPROF 8
 
 struct CtwDecodeCfg {
   double beam;

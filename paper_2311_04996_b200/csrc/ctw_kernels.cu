@@ -41,6 +41,11 @@
 #define CTW_PRED_BITS 24
 #define CTW_PRED_MASK ((1u << CTW_PRED_BITS) - 1u)
 #define CTW_KEY56 ((1ULL << 56) - 1ULL)
+#define CTW_EIPT 2                       // frontier items per thread per epsilon tile
+#define CTW_ETILE (CTW_BS * CTW_EIPT)
+#define CTW_DISC 0xFFFFFFFFu             // epsilon tile item: discovery only (no value)
+#define CTW_NB 1024      // cost-histogram bins over [min, min + beam] for the max-active select
+#define CTW_BBUF 1024    // boundary-bin capacity of the exact (cost, state) sort
 
 namespace {
 
@@ -91,9 +96,10 @@ __device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
 struct LaneCtx {
   CtwTok* T;
   uint32_t mask, shift, tcap;
-  uint32_t* slots;
+  uint2* slots;  // (table index, state)
   int pool_cap;
   int32_t* pool;
+  bool prune;    // CtwLane::prune_ok
 };
 
 // Find-or-insert `d` (linear probing). Returns the table index or CTW_EMPTY
@@ -101,19 +107,22 @@ struct LaneCtx {
 __device__ __forceinline__ uint32_t tok_insert(const LaneCtx& L, uint32_t d, bool& is_new) {
   uint32_t h = tok_hash(d, L.shift);
   for (uint32_t probe = 0; probe <= L.mask; ++probe) {
-    const uint32_t k = __ldcg(&L.T[h].state);
-    if (k == d) return h;
-    if (k == CTW_EMPTY) {
-      const uint32_t old = atomicCAS(&L.T[h].state, CTW_EMPTY, d);
-      if (old == CTW_EMPTY) {
-        is_new = true;
-        return h;
-      }
-      if (old == d) return h;
+    // one L2 round trip per probe: the CAS both claims a free entry and
+    // reports an occupied one
+    const uint32_t old = atomicCAS(&L.T[h].state, CTW_EMPTY, d);
+    if (old == CTW_EMPTY) {
+      is_new = true;
+      return h;
     }
+    if (old == d) return h;
     h = (h + 1) & L.mask;
   }
   return CTW_EMPTY;
+}
+
+// Fire-and-forget slot-position update (compiles to RED.MIN: no round trip).
+__device__ __forceinline__ void gpos_min(CtwTok* e, unsigned long long v) {
+  atomicMin(&e->gpos, v);
 }
 
 // Gauss-Seidel event order of two epsilon candidates with equal cost:
@@ -182,10 +191,29 @@ __device__ __forceinline__ void tok_clear(CtwTok* e) {
 struct __align__(16) Smem {
   typedef cub::BlockScan<int, CTW_BS> Scan;
   typename Scan::TempStorage scan;
-  int off[CTW_TILE];
-  uint32_t beg[CTW_TILE];
-  double cost[CTW_TILE];
+  union {
+    struct {  // emitting-expansion tile
+      double cost[CTW_TILE];
+      int off[CTW_TILE];
+      uint32_t beg[CTW_TILE];
+    };
+    ulonglong2 bbuf[CTW_BBUF];  // max-active boundary bin: (cost key, state)
+    struct {  // epsilon-closure tile: one entry per frontier item
+      double ecost[CTW_ETILE];
+      unsigned long long egb[CTW_ETILE];  // slot-position prefix handed to discovered successors
+      unsigned long long egu[CTW_ETILE];  // the item's own slot position (tie-break)
+      int eoff[CTW_ETILE];
+      uint32_t ebeg[CTW_ETILE];
+      uint32_t eaux[CTW_ETILE];           // pd << 24 | table index, or CTW_DISC
+    };
+  };
+  uint32_t bhist[CTW_NB];
   uint32_t hist[256];
+  int sel_bin;     // boundary bin (CTW_NB = no select)
+  int sel_bcount;  // members of the boundary bin
+  unsigned long long thr_key;  // survivor iff bin < sel_bin or (bin == sel_bin and (key, state) <= thr)
+  uint32_t thr_state;
+  int sel_radix;   // boundary bin overflowed CTW_BBUF: digit-wise radix select over all slots
   unsigned long long min_key;
   unsigned long long sel_hi;  // radix-select prefix (cost-key digits)
   uint32_t sel_lo;            // radix-select prefix (state digits)
@@ -196,6 +224,7 @@ struct __align__(16) Smem {
   int n_next;
   int n_tiny;
   int any_big;
+  int passes;
   int status;
   int cnt;
   int max_pd;
@@ -205,14 +234,20 @@ struct __align__(16) Smem {
 
 // Append a newly inserted table index to the slot list (always, so the table
 // can be reset even on overflow); request a bigger table past half load.
-__device__ __forceinline__ void slot_append(Smem& sm, const LaneCtx& L, uint32_t h) {
+__device__ __forceinline__ void slot_append(Smem& sm, const LaneCtx& L, uint32_t h, uint32_t state) {
   const int s = atomicAdd(&sm.n_slots, 1);
-  if ((uint32_t)s < L.tcap) L.slots[s] = h;
+  if ((uint32_t)s < L.tcap) L.slots[s] = make_uint2(h, state);
   if ((uint32_t)s >= (L.tcap >> 1)) atomicMax(&sm.status, CTW_GROW_TABLE);
 }
 
 __device__ __forceinline__ void track_min(Smem& sm, unsigned long long k) {
   if (k < *((volatile unsigned long long*)&sm.min_key)) atomicMin(&sm.min_key, k);
+}
+
+// Running beam cutoff: the frame minimum only decreases, so a cost above
+// (running min + beam) is above the final cutoff too.
+__device__ __forceinline__ double running_cut(const Smem& sm, double beam) {
+  return __dadd_rn(key2d(*((volatile const unsigned long long*)&sm.min_key)), beam);
 }
 
 // ------------------------------------------------------- epsilon fixpoint --
@@ -222,53 +257,101 @@ __device__ __forceinline__ void track_min(Smem& sm, unsigned long long k) {
 // improved by more than relax_eps, or changed winner at equal cost (its
 // Gauss-Seidel event time moved). Improvements <= relax_eps are propagated
 // only if the pass goes on anyway, mirroring the Gauss-Seidel stop rule
-// (_kernel.pyx:331, :346, :351). Returns CTW_OK or CTW_ERR_EPS_ITERS
-// (divergence: more passes than any convergent closure needs).
-__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t* front, const double* boost,
-                            double relax_eps, long long pass_cap) {
+// (_kernel.pyx:331, :346, :351). With L.prune, a predecessor whose cost is
+// above the running cutoff (or that has no value yet) only *discovers* its
+// successors -- slot positions stay exact -- without relaxing their costs:
+// with non-negative epsilon increments nothing it reaches can enter the
+// beam. Returns CTW_OK or CTW_ERR_EPS_ITERS (divergence: more passes than a
+// convergent closure needs).
+__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2* front, const double* boost,
+                            double relax_eps, double beam, long long pass_cap) {
   const int tid = threadIdx.x;
-  const uint32_t* cur = L.slots;
+  const uint2* cur = L.slots;
   int n_cur = sm.n_slots;
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
   // three buffers rotate: cur (being read), nxt (big changes), tiny (small)
-  uint32_t* bufs[3] = {front, front + L.tcap, front + 2 * (size_t)L.tcap};
+  uint2* bufs[3] = {front, front + L.tcap, front + 2 * (size_t)L.tcap};
   int ci = 2;  // index of cur's buffer (pass 1 reads the slot list itself)
   for (long long pass = 1;; ++pass) {
     if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
     if (tid == 0) {
+      sm.passes = (int)pass;
       sm.n_next = 0;
       sm.n_tiny = 0;
       sm.any_big = 0;
     }
     __syncthreads();
     const uint32_t epoch = (uint32_t)pass;
-    uint32_t* nxt = bufs[(ci + 1) % 3];
-    uint32_t* tiny = bufs[(ci + 2) % 3];
-    for (int i = tid; i < n_cur; i += CTW_BS) {
-      const uint32_t h = cur[i];
-      const CtwTok* eu = &L.T[h];
-      const uint32_t s = __ldcg(&eu->state);
-      const CtwStateRange r = g.ranges[s];
-      if (r.eps_beg == r.emit_beg) continue;
-      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
-      const unsigned long long gu = __ldcg(&eu->gpos);
-      const uint32_t tbu = (uint32_t)v.y, auxu = (uint32_t)(v.y >> 32);
-      uint32_t pd = 1;
-      if (tbu & CTW_EPS_BIT) {
-        const uint32_t pred = auxu & CTW_PRED_MASK;
-        pd = (auxu >> CTW_PRED_BITS) + (gu < __ldcg(&L.T[pred].gpos) ? 1u : 0u);
-        pd = min(pd, 255u);
+    uint2* nxt = bufs[(ci + 1) % 3];
+    uint2* tiny = bufs[(ci + 2) % 3];
+    for (int tile = 0; tile < n_cur; tile += CTW_ETILE) {
+      // -- setup: per frontier item its epsilon range, cost, tie-break data
+      int deg[CTW_EIPT];
+      int tsum = 0;
+#pragma unroll
+      for (int j = 0; j < CTW_EIPT; ++j) {
+        const int li = tid * CTW_EIPT + j;
+        const int i = tile + li;
+        deg[j] = 0;
+        if (i < n_cur) {
+          const uint2 it = cur[i];
+          const CtwStateRange r = g.ranges[it.y];
+          deg[j] = (int)(r.emit_beg - r.eps_beg);
+          if (deg[j] > 0) {
+            const CtwTok* eu = &L.T[it.x];
+            const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
+            const unsigned long long gu = __ldcg(&eu->gpos);
+            const double c = key2d(v.x);
+            const bool valued = v.x != ~0ULL && !(L.prune && c > running_cut(sm, beam));
+            uint32_t aux = CTW_DISC;
+            if (valued) {
+              const uint32_t tbu = (uint32_t)v.y, auxu = (uint32_t)(v.y >> 32);
+              uint32_t pd = 1;
+              if (tbu & CTW_EPS_BIT) {
+                const uint32_t pred = auxu & CTW_PRED_MASK;
+                pd = (auxu >> CTW_PRED_BITS) + (gu < __ldcg(&L.T[pred].gpos) ? 1u : 0u);
+                pd = min(pd, 255u);
+              }
+              aux = (pd << CTW_PRED_BITS) | it.x;
+            }
+            sm.ecost[li] = c;
+            sm.egu[li] = gu;
+            sm.egb[li] = (((gu >> 56) + 1) << 56) | ((gu << 4) & CTW_KEY56);
+            sm.ebeg[li] = r.eps_beg;
+            sm.eaux[li] = aux;
+          }
+        }
+        tsum += deg[j];
       }
-      const double c = key2d(v.x);
-      const unsigned long long lev = (gu >> 56) + 1;
-      const unsigned long long gbase = (lev << 56) | ((gu << 4) & CTW_KEY56);
-      const uint32_t aux = (pd << CTW_PRED_BITS) | h;
-      for (uint32_t a = r.eps_beg; a < r.emit_beg; ++a) {
+      int excl, total;
+      Smem::Scan(sm.scan).ExclusiveSum(tsum, excl, total);
+#pragma unroll
+      for (int j = 0; j < CTW_EIPT; ++j) {
+        sm.eoff[tid * CTW_EIPT + j] = excl;
+        excl += deg[j];
+      }
+      __syncthreads();
+      // -- flat, load-balanced loop over the tile's epsilon arcs
+      const int nt = min(CTW_ETILE, n_cur - tile);
+      for (int k = tid; k < total; k += CTW_BS) {
+        int lo = 0, hi = nt - 1;  // last item with eoff <= k
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.eoff[mid] <= k) lo = mid;
+          else hi = mid - 1;
+        }
+        const uint32_t o = (uint32_t)(k - sm.eoff[lo]);
+        const uint32_t a = sm.ebeg[lo] + o;
+        const uint32_t aux = sm.eaux[lo];
+        const bool valued = aux != CTW_DISC;
         const CtwArc arc = g.arcs[a];
-        double nc = __dadd_rn(c, arc.weight);
-        if (boost) {
-          const int32_t ol = g.olabel[a];
-          if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+        double nc = arc.weight;
+        if (valued) {
+          nc = __dadd_rn(sm.ecost[lo], arc.weight);
+          if (boost) {
+            const int32_t ol = g.olabel[a];
+            if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+          }
         }
         if (!(nc < INF)) continue;
         bool is_new = false;
@@ -277,37 +360,46 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint3
           atomicMax(&sm.status, CTW_GROW_TABLE);
           continue;
         }
-        if (is_new) slot_append(sm, L, d);
+        if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
         CtwTok* ed = &L.T[d];
-        const unsigned long long cg = gbase | min(a - r.eps_beg, 15u);
-        if (cg < __ldcg(&ed->gpos)) atomicMin(&ed->gpos, cg);
-        unsigned long long oldk;
-        const unsigned long long nk = d2key(nc);
-        if (tok_relax(L, ed, nk, CTW_EPS_BIT | a, aux, gu, &oldk)) {
-          track_min(sm, nk);
-          const bool big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
-          if (big) sm.any_big = 1;
-          if (atomicExch(&ed->stamp, epoch) != epoch) {
-            if (big) {
-              const int p = atomicAdd(&sm.n_next, 1);
-              if ((uint32_t)p < L.tcap) nxt[p] = d;
-            } else {
-              const int p = atomicAdd(&sm.n_tiny, 1);
-              if ((uint32_t)p < L.tcap) tiny[p] = d;
-            }
+        gpos_min(ed, sm.egb[lo] | min(o, 15u));
+        const uint2 item = make_uint2(d, (uint32_t)arc.nextstate);
+        bool push = false, big = false;
+        if (valued) {
+          unsigned long long oldk;
+          const unsigned long long nk = d2key(nc);
+          if (tok_relax(L, ed, nk, CTW_EPS_BIT | a, aux, sm.egu[lo], &oldk)) {
+            track_min(sm, nk);
+            push = true;
+            big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
+          } else {
+            push = big = is_new;
+          }
+        } else {
+          push = big = is_new;  // discovery only: successors are discovered next pass
+        }
+        if (!push) continue;
+        if (big) sm.any_big = 1;
+        if (atomicExch(&ed->stamp, epoch) != epoch) {
+          if (big) {
+            const int p = atomicAdd(&sm.n_next, 1);
+            if ((uint32_t)p < L.tcap) nxt[p] = item;
+          } else {
+            const int p = atomicAdd(&sm.n_tiny, 1);
+            if ((uint32_t)p < L.tcap) tiny[p] = item;
           }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (sm.status >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
-    int n_next = sm.n_next;
+    int n_next = min((uint32_t)sm.n_next, L.tcap);
     if (!sm.any_big) return CTW_OK;  // a quiet pass (only <= relax_eps changes) ends the closure
     // the pass continues: parked small improvements ride along (Gauss-Seidel
     // re-visits every slot in the next pass)
-    const int n_tiny = sm.n_tiny;
+    const int n_tiny = min((uint32_t)sm.n_tiny, L.tcap);
     if (n_tiny > 0) {
-      for (int i = tid; i < n_tiny; i += CTW_BS) nxt[n_next + i] = tiny[i];
+      for (int i = tid; i < n_tiny && n_next + i < (int)L.tcap; i += CTW_BS) nxt[n_next + i] = tiny[i];
       n_next = min((uint32_t)(n_next + n_tiny), L.tcap);
     }
     cur = nxt;
@@ -331,11 +423,16 @@ struct WalkEnd {
   bool ok;
 };
 
-__device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, uint32_t h, const CtwSrc* src,
+// v0 = the survivor's own (key, tb|aux), already gathered.
+__device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, ulonglong2 v0, const CtwSrc* src,
                                         const int32_t* pend, int hop_cap) {
   WalkEnd w{-1, 0, 0, 0, true};
+  ulonglong2 v = v0;
   for (int hop = 0; hop < hop_cap; ++hop) {
-    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h]));
+    if (hop) {
+      // epsilon winner: continue at the predecessor
+      v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[(uint32_t)(v.y >> 32) & CTW_PRED_MASK]));
+    }
     const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
     if (tb == CTW_SEED_TB) return w;
     const uint32_t a = tb & ~CTW_EPS_BIT;
@@ -349,7 +446,6 @@ __device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, uin
       w.pend = pend ? pend[aux] : 0;
       return w;
     }
-    h = aux & CTW_PRED_MASK;
   }
   w.ok = false;
   return w;
@@ -428,10 +524,10 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned l
     const unsigned long long ph = sm.sel_hi;
     const uint32_t pl = sm.sel_lo;
     for (int i = tid; i < n_slots; i += CTW_BS) {
-      const CtwTok* e = &L.T[L.slots[i]];
-      const unsigned long long key = __ldcg(&e->key);
+      const uint2 it = L.slots[i];
+      const unsigned long long key = __ldcg(&L.T[it.x].key);
       if (key > cut_key) continue;
-      const uint32_t st = __ldcg(&e->state);
+      const uint32_t st = it.y;
       if (cmp_prefix(key, st, d, ph, pl) != 0) continue;
       atomicAdd(&sm.hist[digit_of(key, st, d)], 1u);
     }
@@ -495,6 +591,7 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane) {
   L.slots = lane.slots;
   L.pool = lane.pool;
   L.pool_cap = lane.pcap;
+  L.prune = lane.prune_ok != 0;
   return L;
 }
 
@@ -505,30 +602,163 @@ __device__ __forceinline__ long long divergence_cap(long long max_ne_iters, uint
   return max(max_ne_iters, (long long)(tcap >> 1)) + 2;
 }
 
-// Gauss-Seidel pass count of the closure = 1 + last pass that changed a
-// slot (max pd over epsilon-won slots); returns CTW_ERR_EPS_ITERS past the cap.
-__device__ int gs_pass_check(Smem& sm, const LaneCtx& L, int n_slots, long long max_ne_iters,
-                             unsigned long long cut_key, bool count_beam) {
+__device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost, double bin_scale) {
+  const int b = (int)__dmul_rn(__dsub_rn(key2d(key), min_cost), bin_scale);
+  return min(max(b, 0), CTW_NB - 1);
+}
+
+#define CTW_UNR 4  // independent table loads in flight per thread in slot sweeps
+
+// One sweep over the frame's slots: gathers every slot's final (key, tb|aux)
+// into the compact array sv (coalesced for the later sweeps; CTW_UNR table
+// loads in flight per thread), and computes the Gauss-Seidel pass count of
+// the closure (= 1 + last pass that changed a slot, i.e. max pd over
+// epsilon-won slots; > max_ne_iters -> CTW_ERR_EPS_ITERS), the in-beam count
+// and (hist) the cost histogram over [min, min + beam] for the max-active select.
+__device__ int count_pass(Smem& sm, const LaneCtx& L, ulonglong2* sv, int n_slots, long long max_ne_iters,
+                          unsigned long long cut_key, double min_cost, double bin_scale, bool hist) {
   const int tid = threadIdx.x;
+  if (hist)
+    for (int i = tid; i < CTW_NB; i += CTW_BS) sm.bhist[i] = 0;
+  __syncthreads();
   int c = 0, mpd = 0;
-  for (int i = tid; i < n_slots; i += CTW_BS) {
-    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[L.slots[i]]));
-    c += (v.x <= cut_key);
-    if ((uint32_t)v.y & CTW_EPS_BIT) mpd = max(mpd, (int)((uint32_t)(v.y >> 32) >> CTW_PRED_BITS));
+  for (int i0 = tid; i0 < n_slots; i0 += CTW_UNR * CTW_BS) {
+    uint32_t h[CTW_UNR];
+    ulonglong2 v[CTW_UNR];
+#pragma unroll
+    for (int u = 0; u < CTW_UNR; ++u) {
+      const int i = i0 + u * CTW_BS;
+      h[u] = i < n_slots ? L.slots[i].x : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < CTW_UNR; ++u) {
+      const int i = i0 + u * CTW_BS;
+      if (i < n_slots) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u]]));
+    }
+#pragma unroll
+    for (int u = 0; u < CTW_UNR; ++u) {
+      const int i = i0 + u * CTW_BS;
+      if (i >= n_slots) break;
+      sv[i] = v[u];
+      if (v[u].x <= cut_key) {
+        ++c;
+        if (hist) atomicAdd(&sm.bhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
+      }
+      if ((uint32_t)v[u].y & CTW_EPS_BIT) mpd = max(mpd, (int)((uint32_t)(v[u].y >> 32) >> CTW_PRED_BITS));
+    }
   }
   for (int o = 16; o; o >>= 1) {
     c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
     mpd = max(mpd, __shfl_xor_sync(0xFFFFFFFFu, mpd, o));
   }
   if ((tid & 31) == 0) {
-    if (count_beam) atomicAdd(&sm.cnt, c);
+    atomicAdd(&sm.cnt, c);
     atomicMax(&sm.max_pd, mpd);
   }
   __syncthreads();
   return (1 + (long long)sm.max_pd > max_ne_iters) ? CTW_ERR_EPS_ITERS : CTW_OK;
 }
 
-__global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
+// Reset every touched table entry; slot loads batched ahead of the stores.
+__device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_slots) {
+  for (int i0 = threadIdx.x; i0 < n_slots; i0 += CTW_UNR * CTW_BS) {
+    uint32_t h[CTW_UNR];
+#pragma unroll
+    for (int u = 0; u < CTW_UNR; ++u) {
+      const int i = i0 + u * CTW_BS;
+      h[u] = i < n_slots ? L.slots[i].x : CTW_EMPTY;
+    }
+#pragma unroll
+    for (int u = 0; u < CTW_UNR; ++u)
+      if (h[u] != CTW_EMPTY) tok_clear(&L.T[h[u]]);
+  }
+}
+
+// Exact max-active threshold by (cost, state) (decoder.py:361-374,
+// _kernel.pyx:385-390): the histogram locates the boundary bin; its members
+// are sorted exactly in shared memory (bitonic). Falls back to the
+// digit-wise radix select when the boundary bin overflows CTW_BBUF.
+__device__ void select_threshold(Smem& sm, const LaneCtx& L, const ulonglong2* sv, int n_slots,
+                                 unsigned long long cut_key, double min_cost, double bin_scale, long long k) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    uint32_t cnt[CTW_NB / 32];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < CTW_NB / 32; ++j) {
+      cnt[j] = sm.bhist[tid * (CTW_NB / 32) + j];
+      sum += cnt[j];
+    }
+    uint32_t incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (tid >= o) incl += t;
+    }
+    const uint32_t excl = incl - sum;
+    const uint32_t need = (uint32_t)k;
+    if (excl < need && need <= incl) {
+      uint32_t run = excl;
+      for (int j = 0; j < CTW_NB / 32; ++j) {
+        if (run + cnt[j] >= need) {
+          sm.sel_bin = tid * (CTW_NB / 32) + j;
+          sm.sel_need = (int)(need - run);
+          sm.sel_bcount = (int)cnt[j];
+          break;
+        }
+        run += cnt[j];
+      }
+    }
+    if (tid == 0) {
+      sm.sel_radix = 0;
+      sm.thr_key = ~0ULL;
+      sm.thr_state = 0xFFFFFFFFu;
+      sm.n_next = 0;
+    }
+  }
+  __syncthreads();
+  const int bsel = sm.sel_bin, need = sm.sel_need, bcount = sm.sel_bcount;
+  if (bcount == need) return;  // the whole boundary bin survives
+  if (bcount > CTW_BBUF) {
+    if (tid == 0) sm.sel_radix = 1;
+    radix_select(sm, L, n_slots, cut_key, k);
+    return;
+  }
+  for (int i = tid; i < n_slots; i += CTW_BS) {
+    const unsigned long long key = sv[i].x;
+    if (key <= cut_key && cost_bin(key, min_cost, bin_scale) == bsel) {
+      const int p = atomicAdd(&sm.n_next, 1);
+      sm.bbuf[p] = make_ulonglong2(key, L.slots[i].y);
+    }
+  }
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < bcount) n2 <<= 1;
+  for (int i = bcount + tid; i < n2; i += CTW_BS) sm.bbuf[i] = make_ulonglong2(~0ULL, ~0ULL);
+  __syncthreads();
+  for (int kk = 2; kk <= n2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n2; i += CTW_BS) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const ulonglong2 x = sm.bbuf[i], y = sm.bbuf[ixj];
+          const bool gt = x.x > y.x || (x.x == y.x && x.y > y.y);
+          if (gt == ((i & kk) == 0)) {
+            sm.bbuf[i] = y;
+            sm.bbuf[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    sm.thr_key = sm.bbuf[need - 1].x;
+    sm.thr_state = (uint32_t)sm.bbuf[need - 1].y;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
   extern __shared__ double nll_s[];
   __shared__ Smem sm;
   const int tid = threadIdx.x;
@@ -552,6 +782,7 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
   int err_frame = -1;
   int n_slots_max = 0;
   long long arcs_total = 0, src_total = 0, rec_need = 0;
+  long long prof[CTW_NPROF] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (tid == 0) {
     sm.status = CTW_OK;
     sm.pool_used = lane.pool_used;
@@ -559,6 +790,7 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
   __syncthreads();
 
   for (int f = 0; f < F; ++f) {
+    long long tclk = clock64();
     const CtwSrc* src = lane.src[cur_buf];
     const int32_t* pend = pend_valid ? lane.pend : nullptr;
     const int nxt_buf = (f & 1) ? w1 : w0;
@@ -636,11 +868,12 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
           atomicMax(&sm.status, CTW_GROW_TABLE);
           continue;
         }
-        if (is_new) slot_append(sm, L, d);
+        if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
         CtwTok* ed = &L.T[d];
         // Gauss-Seidel slot position of an emitting-reached state = its
         // first-arrival arc (_kernel.pyx:256-272)
-        if ((unsigned long long)arc_i < __ldcg(&ed->gpos)) atomicMin(&ed->gpos, (unsigned long long)arc_i);
+        gpos_min(ed, (unsigned long long)arc_i);
+        if (L.prune && nc > running_cut(sm, a.cfg.beam)) continue;  // cannot make the final beam
         unsigned long long oldk;
         const unsigned long long nk = d2key(nc);
         if (tok_relax(L, ed, nk, arc_i, (uint32_t)(tile + lo), 0ULL, &oldk)) track_min(sm, nk);
@@ -649,10 +882,22 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
       __syncthreads();
     }
 
+    {
+      const long long t = clock64();
+      prof[0] += t - tclk;
+      tclk = t;
+    }
     // ---- epsilon closure ----
     int st = CTW_OK;
-    if (sm.status < CTW_GROW_TABLE) st = eps_fixpoint(sm, L, g, lane.front, boost, a.cfg.relax_eps, pass_cap);
+    if (sm.status < CTW_GROW_TABLE)
+      st = eps_fixpoint(sm, L, g, lane.front, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
     __syncthreads();
+    {
+      const long long t = clock64();
+      prof[1] += t - tclk;
+      prof[6] += sm.passes;
+      tclk = t;
+    }
     const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
     n_slots_max = max(n_slots_max, n_slots);
     if (st != CTW_OK) status = st;
@@ -660,42 +905,62 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
     else if (n_slots == 0) status = CTW_ERR_NO_SURVIVORS;
 
     // ---- prune: beam cutoff from the frame minimum, exact max_active ----
-    const double cutoff = __dadd_rn(key2d(sm.min_key), a.cfg.beam);
+    const double min_cost = key2d(sm.min_key);
+    const double cutoff = __dadd_rn(min_cost, a.cfg.beam);
     const unsigned long long cut_key = d2key(cutoff);
-    if (status == CTW_OK) status = gs_pass_check(sm, L, n_slots, a.cfg.max_ne_iters, cut_key, true);
+    const double bin_scale = (double)CTW_NB / a.cfg.beam;
+    ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);  // frontier buffers are free now
+    if (status == CTW_OK)
+      status = count_pass(sm, L, sv, n_slots, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
+    {
+      const long long t = clock64();
+      prof[2] += t - tclk;
+      tclk = t;
+    }
     if (status == CTW_OK) {
       const int in_beam = sm.cnt;
       const bool select = (long long)in_beam > a.cfg.max_active;
       const int n_surv = select ? (int)a.cfg.max_active : in_beam;
-      if (select) radix_select(sm, L, n_slots, cut_key, a.cfg.max_active);
-      else if (tid == 0) sm.sel_depth = 0;
+      if (select) select_threshold(sm, L, sv, n_slots, cut_key, min_cost, bin_scale, a.cfg.max_active);
       __syncthreads();
+      {
+        const long long t = clock64();
+        prof[3] += t - tclk;
+        prof[7] += select;
+        tclk = t;
+      }
       if (n_rec + n_surv > lane.rcap) {
         status = CTW_GROW_HIST;
         rec_need = n_rec + n_surv;
       } else {
         // ---- records + next sources: per-thread counts, one scan, then
         // independent per-survivor writes (no per-tile barriers) ----
+        const bool radix = select && sm.sel_radix;
+        const int bsel = select ? sm.sel_bin : CTW_NB;
+        const unsigned long long tk = sm.thr_key;
+        const uint32_t ts = sm.thr_state;
         const int depth = sm.sel_depth;
         const unsigned long long ph = sm.sel_hi;
         const uint32_t pl = sm.sel_lo;
+        auto keep = [&](unsigned long long key, uint32_t state) -> bool {
+          if (key > cut_key) return false;
+          if (!select) return true;
+          if (radix) return cmp_prefix(key, state, depth, ph, pl) <= 0;
+          const int bb = cost_bin(key, min_cost, bin_scale);
+          return bb < bsel || (bb == bsel && (key < tk || (key == tk && state <= ts)));
+        };
         int mine = 0;
-        for (int i = tid; i < n_slots; i += CTW_BS) {
-          const CtwTok* e = &L.T[L.slots[i]];
-          const unsigned long long key = __ldcg(&e->key);
-          mine += key <= cut_key && (!select || cmp_prefix(key, __ldcg(&e->state), depth, ph, pl) <= 0);
-        }
+        for (int i = tid; i < n_slots; i += CTW_BS) mine += keep(sv[i].x, L.slots[i].y);
         int pos, tot;
         Smem::Scan(sm.scan).ExclusiveSum(mine, pos, tot);
         const int hop_cap = n_slots + 2;
         for (int i = tid; i < n_slots; i += CTW_BS) {
-          const uint32_t h = L.slots[i];
-          const CtwTok* e = &L.T[h];
-          const unsigned long long key = __ldcg(&e->key);
-          if (key > cut_key) continue;
-          const uint32_t st2 = __ldcg(&e->state);
-          if (select && cmp_prefix(key, st2, depth, ph, pl) > 0) continue;
-          const WalkEnd w = walk(L, g, h, src, pend, hop_cap);
+          const ulonglong2 v0 = sv[i];
+          const unsigned long long key = v0.x;
+          const uint2 it = L.slots[i];
+          const uint32_t h = it.x, st2 = it.y;
+          if (!keep(key, st2)) continue;
+          const WalkEnd w = walk(L, g, v0, src, pend, hop_cap);
           if (!w.ok) sm.hop_fail = 1;
           const int32_t code = record_code(sm, L, g, h, w);
           const long long r = n_rec + pos;
@@ -718,10 +983,16 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
         else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
       }
     }
+    {
+      const long long t = clock64();
+      prof[4] += t - tclk;
+      tclk = t;
+    }
 
     // ---- reset every touched table entry (also on failure) ----
-    for (int i = tid; i < n_slots; i += CTW_BS) tok_clear(&L.T[L.slots[i]]);
+    reset_slots(L, n_slots);
     __syncthreads();
+    prof[5] += clock64() - tclk;
     if (status != CTW_OK) {
       err_frame = f;
       break;
@@ -738,6 +1009,7 @@ __global__ void __launch_bounds__(CTW_BS) k_decode_chunk(CtwLane* lanes, GraphDe
     o.arcs_expanded = arcs_total;
     o.src_total = src_total;
     o.rec_need = rec_need;
+    for (int k = 0; k < CTW_NPROF; ++k) o.prof[k] = prof[k];
     if (status == CTW_OK) {
       lane.n_src = n_src;
       lane.src_buf = (F > 0) ? cur_buf : committed;
@@ -767,7 +1039,8 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
   __shared__ Smem sm;
   const int tid = threadIdx.x;
   CtwLane& lane = lanes[lane_ids[blockIdx.x]];
-  const LaneCtx L = lane_ctx(lane);
+  LaneCtx L = lane_ctx(lane);
+  L.prune = false;  // no beam at seed time: the whole closure is kept
   if (tid == 0) {
     sm.status = CTW_OK;
     sm.pool_used = 0;
@@ -778,27 +1051,30 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
     sm.cnt = 0;
     bool is_new = false;
     const uint32_t h = tok_insert(L, (uint32_t)start, is_new);
-    slot_append(sm, L, h);
+    slot_append(sm, L, h, (uint32_t)start);
     L.T[h].gpos = 0ULL;
     unsigned long long oldk;
     tok_relax(L, &L.T[h], d2key(0.0), CTW_SEED_TB, 0, 0ULL, &oldk);
   }
   __syncthreads();
-  int status = eps_fixpoint(sm, L, g, lane.front, lane.boost, cfg.relax_eps, divergence_cap(cfg.max_ne_iters, L.tcap));
+  int status = eps_fixpoint(sm, L, g, lane.front, lane.boost, cfg.relax_eps, cfg.beam,
+                            divergence_cap(cfg.max_ne_iters, L.tcap));
   __syncthreads();
   const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
   if (status == CTW_OK && sm.status >= CTW_GROW_TABLE) status = sm.status;
-  if (status == CTW_OK) status = gs_pass_check(sm, L, n_slots, cfg.max_ne_iters, 0ULL, false);
+  ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);
+  if (status == CTW_OK) status = count_pass(sm, L, sv, n_slots, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
   if (status == CTW_OK) {
     CtwSrc* dst = lane.src[0];
     for (int i = tid; i < n_slots; i += CTW_BS) {
-      const uint32_t h = L.slots[i];
-      const WalkEnd w = walk(L, g, h, nullptr, nullptr, n_slots + 2);
+      const uint32_t h = L.slots[i].x;
+      const ulonglong2 v0 = sv[i];
+      const WalkEnd w = walk(L, g, v0, nullptr, nullptr, n_slots + 2);
       if (!w.ok) sm.hop_fail = 1;
       CtwSrc s;
-      s.state = (int32_t)__ldcg(&L.T[h].state);
+      s.state = (int32_t)L.slots[i].y;
       s.bp = -1;
-      s.cost = key2d(__ldcg(&L.T[h].key));
+      s.cost = key2d(v0.x);
       dst[i] = s;
       lane.pend[i] = record_code(sm, L, g, h, w);
     }
@@ -806,7 +1082,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
     if (sm.status >= CTW_GROW_TABLE) status = sm.status;
     else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
   }
-  for (int i = tid; i < n_slots; i += CTW_BS) tok_clear(&L.T[L.slots[i]]);
+  reset_slots(L, n_slots);
   __syncthreads();
   if (tid == 0) {
     CtwLaneOut o = {};

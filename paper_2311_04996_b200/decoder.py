@@ -292,6 +292,13 @@ class LanePool:
         return {"launches": v[0].value, "decode_launches": v[1].value, "decode_ms": v[2].value,
                 "arcs": v[3].value, "src_tokens": v[4].value, "frames": v[5].value, "max_slots": v[6].value}
 
+    def profile(self) -> dict:
+        """Per-stage SM cycles of the frame kernel (ctw_lanes_profile)."""
+        v = np.zeros(8, np.int64)
+        _lib.load().ctw_lanes_profile(self.handle, _lib.ptr(v))
+        names = ("emit", "eps", "beam_count", "select", "records", "reset", "eps_passes", "select_frames")
+        return dict(zip(names, (int(x) for x in v)))
+
     def reset_stats(self) -> None:
         _lib.load().ctw_lanes_reset_stats(self.handle)
 

@@ -117,7 +117,7 @@ def history_signature(hist):
     return out
 
 
-def assert_history_equivalent(got, want, exact_prev=False):
+def assert_history_equivalent(got, want, exact_prev=True):
     if exact_prev:
         assert got == want
         return
