@@ -183,6 +183,8 @@ def _stage_profile(prof, st):
     out["cycles_per_lane_frame"] = tot / lf
     out["eps_passes_per_frame"] = prof["eps_passes"] / lf
     out["select_frame_frac"] = prof["select_frames"] / lf
+    for k in ("slots", "eps_items", "eps_arcs", "in_beam"):
+        out[k + "_per_lane_frame"] = prof[k] / lf
     return out
 
 

@@ -148,11 +148,12 @@ void ctw_export_free(ctw_export* e);
 int ctw_lanes_stats(ctw_lanes* l, int64_t* launches, int64_t* decode_launches, double* decode_ms,
                     int64_t* arcs, int64_t* src_tokens, int64_t* frames, int64_t* max_slots);
 int ctw_lanes_reset_stats(ctw_lanes* l);
-/* Per-stage SM-cycle profile of the frame kernel summed over lanes and frames
- * since the last reset: [0] emitting expansion, [1] epsilon closure, [2] beam
- * count, [3] max-active select, [4] records, [5] table reset, [6] epsilon
- * passes, [7] frames needing the select. */
-int ctw_lanes_profile(ctw_lanes* l, int64_t* out8);
+/* Per-stage profile of the frame kernel summed over lanes and frames since
+ * the last reset (12 counters): SM cycles of [0] emitting expansion, [1]
+ * epsilon closure, [2] beam count, [3] max-active select, [4] records, [5]
+ * table reset; [6] epsilon passes, [7] frames needing the select, [8] slots,
+ * [9] epsilon frontier items, [10] epsilon arcs relaxed, [11] in-beam slots. */
+int ctw_lanes_profile(ctw_lanes* l, int64_t* out12);
 void* ctw_lanes_stream(ctw_lanes* l);
 
 /* The reference kernel contract (_pykernel.py:28-248) on the GPU: same inputs

@@ -133,7 +133,7 @@ struct ctw_lanes {
   // stats
   int64_t launches = 0, decode_launches = 0, arcs = 0, srcs = 0, frames = 0, max_slots = 0;
   double decode_ms = 0.0;
-  int64_t prof[CTW_NPROF] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t prof[CTW_NPROF] = {0};
   std::mutex mu;
 };
 
@@ -1000,9 +1000,9 @@ int ctw_lanes_reset_stats(ctw_lanes* l) {
 
 void* ctw_lanes_stream(ctw_lanes* l) { return (void*)l->stream; }
 
-int ctw_lanes_profile(ctw_lanes* l, int64_t* out8) {
+int ctw_lanes_profile(ctw_lanes* l, int64_t* out) {
   std::lock_guard<std::mutex> lk(l->mu);
-  for (int k = 0; k < CTW_NPROF; ++k) out8[k] = l->prof[k];
+  for (int k = 0; k < CTW_NPROF; ++k) out[k] = l->prof[k];
   return 0;
 }
 

@@ -118,10 +118,11 @@ struct CtwLaneOut {
   // stage profile (SM cycles summed over the chunk's frames, thread 0):
   // [0] emitting expansion, [1] epsilon closure, [2] beam count + pass check,
   // [3] max-active select, [4] records, [5] table reset, [6] epsilon passes,
-  // [7] frames that needed the select
-  int64_t prof[8];
+  // [7] frames that needed the select, [8] slots, [9] epsilon frontier items,
+  // [10] epsilon arcs relaxed, [11] in-beam slots
+  int64_t prof[12];
 };
-#define CTW_NPROF 8
+#define CTW_NPROF 12
 
 struct CtwDecodeCfg {
   double beam;

@@ -125,6 +125,39 @@ __device__ __forceinline__ void gpos_min(CtwTok* e, unsigned long long v) {
   atomicMin(&e->gpos, v);
 }
 
+// Find-or-insert `d` and return a snapshot of its (key, tb|aux) in *v: the
+// probe reads the entry's value and hash key together (plain loads; a
+// claimed hash key never changes within a frame), so a hit costs one round
+// trip and feeds the relax CAS directly; a fresh insert returns the empty
+// value. The snapshot may be stale or torn -- it is only ever used as the
+// expected value of a CAS, which then fails and reports the exact value.
+__device__ __forceinline__ uint32_t tok_locate(const LaneCtx& L, uint32_t d, ulonglong2* v, bool& is_new) {
+  uint32_t h = tok_hash(d, L.shift);
+  for (uint32_t probe = 0; probe <= L.mask; ++probe) {
+    const CtwTok* e = &L.T[h];
+    const ulonglong2 val = __ldcg(reinterpret_cast<const ulonglong2*>(e));
+    const uint32_t k = __ldcg(&e->state);
+    if (k == d) {
+      *v = val;
+      return h;
+    }
+    if (k == CTW_EMPTY) {
+      const uint32_t old = atomicCAS(&L.T[h].state, CTW_EMPTY, d);
+      if (old == CTW_EMPTY) {
+        is_new = true;
+        *v = make_ulonglong2(~0ULL, 0xFFFFFFFFULL);
+        return h;
+      }
+      if (old == d) {
+        *v = val;
+        return h;
+      }
+    }
+    h = (h + 1) & L.mask;
+  }
+  return CTW_EMPTY;
+}
+
 // Gauss-Seidel event order of two epsilon candidates with equal cost:
 // (pd, slot position of the predecessor, arc).
 __device__ __forceinline__ bool gs_before(const CtwTok* T, uint32_t pd_a, uint32_t pred_a, uint32_t arc_a,
@@ -142,19 +175,14 @@ __device__ __forceinline__ bool gs_before(const CtwTok* T, uint32_t pd_a, uint32
 // aux = source index. Epsilon candidates: tb = EPS|arc, aux = pd<<24|pred,
 // gpos_pred = gpos of the predecessor. Returns true when installed; *old_key
 // gets the replaced cost key (~0 = the entry was empty).
-__device__ __forceinline__ bool tok_relax(const LaneCtx& L, CtwTok* e, unsigned long long key, uint32_t tb,
-                                          uint32_t aux, unsigned long long gpos_pred,
-                                          unsigned long long* old_key) {
-  const unsigned long long ck = __ldcg(&e->key);  // single-copy atomic 64-bit read
-  if (key > ck) return false;                     // costs only decrease within a frame
-  unsigned long long clo, chi;
-  if (key == ck) {
-    snap128(e, clo, chi);  // exact tie: need an untorn incumbent
-  } else {
-    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(e));
-    clo = v.x;
-    chi = v.y;
-  }
+__device__ __forceinline__ bool tok_relax_from(const LaneCtx& L, CtwTok* e, unsigned long long key, uint32_t tb,
+                                               uint32_t aux, unsigned long long gpos_pred, ulonglong2 seen,
+                                               unsigned long long* old_key) {
+  // seen.x is a historical key (64-bit halves are single-copy atomic), and
+  // keys only decrease within a frame: key > seen.x rejects safely
+  if (key > seen.x) return false;
+  unsigned long long clo = seen.x, chi = seen.y;
+  if (key == clo) snap128(e, clo, chi);  // exact tie: need an untorn incumbent
   const unsigned long long nhi = ((unsigned long long)aux << 32) | tb;
   for (;;) {
     if (key > clo) return false;
@@ -178,6 +206,11 @@ __device__ __forceinline__ bool tok_relax(const LaneCtx& L, CtwTok* e, unsigned 
     clo = olo;
     chi = ohi;
   }
+}
+
+__device__ __forceinline__ bool tok_relax(const LaneCtx& L, CtwTok* e, unsigned long long key, uint32_t tb,
+                                          uint32_t aux, unsigned long long gpos_pred, unsigned long long* old_key) {
+  return tok_relax_from(L, e, key, tb, aux, gpos_pred, __ldcg(reinterpret_cast<const ulonglong2*>(e)), old_key);
 }
 
 __device__ __forceinline__ void tok_clear(CtwTok* e) {
@@ -225,6 +258,8 @@ struct __align__(16) Smem {
   int n_tiny;
   int any_big;
   int passes;
+  int eps_items;
+  int eps_arcs;
   int status;
   int cnt;
   int max_pd;
@@ -275,6 +310,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
   for (long long pass = 1;; ++pass) {
     if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
     if (tid == 0) {
+      sm.eps_items += n_cur;
       sm.passes = (int)pass;
       sm.n_next = 0;
       sm.n_tiny = 0;
@@ -325,6 +361,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
       }
       int excl, total;
       Smem::Scan(sm.scan).ExclusiveSum(tsum, excl, total);
+      if (tid == 0) sm.eps_arcs += total;
 #pragma unroll
       for (int j = 0; j < CTW_EIPT; ++j) {
         sm.eoff[tid * CTW_EIPT + j] = excl;
@@ -355,7 +392,8 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
         }
         if (!(nc < INF)) continue;
         bool is_new = false;
-        const uint32_t d = tok_insert(L, (uint32_t)arc.nextstate, is_new);
+        ulonglong2 seen;
+        const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
         if (d == CTW_EMPTY) {
           atomicMax(&sm.status, CTW_GROW_TABLE);
           continue;
@@ -368,7 +406,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
         if (valued) {
           unsigned long long oldk;
           const unsigned long long nk = d2key(nc);
-          if (tok_relax(L, ed, nk, CTW_EPS_BIT | a, aux, sm.egu[lo], &oldk)) {
+          if (tok_relax_from(L, ed, nk, CTW_EPS_BIT | a, aux, sm.egu[lo], seen, &oldk)) {
             track_min(sm, nk);
             push = true;
             big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
@@ -380,7 +418,14 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
         }
         if (!push) continue;
         if (big) sm.any_big = 1;
-        if (atomicExch(&ed->stamp, epoch) != epoch) {
+        bool first;
+        if (is_new) {  // this thread created the slot: first to touch its stamp
+          ed->stamp = epoch;
+          first = true;
+        } else {
+          first = atomicExch(&ed->stamp, epoch) != epoch;
+        }
+        if (first) {
           if (big) {
             const int p = atomicAdd(&sm.n_next, 1);
             if ((uint32_t)p < L.tcap) nxt[p] = item;
@@ -782,7 +827,7 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
   int err_frame = -1;
   int n_slots_max = 0;
   long long arcs_total = 0, src_total = 0, rec_need = 0;
-  long long prof[CTW_NPROF] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof[CTW_NPROF] = {0};
   if (tid == 0) {
     sm.status = CTW_OK;
     sm.pool_used = lane.pool_used;
@@ -796,6 +841,8 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
     const int nxt_buf = (f & 1) ? w1 : w0;
     CtwSrc* nsrc = lane.src[nxt_buf];
     if (tid == 0) {
+      sm.eps_items = 0;
+      sm.eps_arcs = 0;
       sm.n_slots = 0;
       sm.min_key = ~0ULL;
       sm.cnt = 0;
@@ -863,7 +910,8 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
         }
         if (!(nc < INF)) continue;
         bool is_new = false;
-        const uint32_t d = tok_insert(L, (uint32_t)arc.nextstate, is_new);
+        ulonglong2 seen;
+        const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
         if (d == CTW_EMPTY) {
           atomicMax(&sm.status, CTW_GROW_TABLE);
           continue;
@@ -876,7 +924,7 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
         if (L.prune && nc > running_cut(sm, a.cfg.beam)) continue;  // cannot make the final beam
         unsigned long long oldk;
         const unsigned long long nk = d2key(nc);
-        if (tok_relax(L, ed, nk, arc_i, (uint32_t)(tile + lo), 0ULL, &oldk)) track_min(sm, nk);
+        if (tok_relax_from(L, ed, nk, arc_i, (uint32_t)(tile + lo), 0ULL, seen, &oldk)) track_min(sm, nk);
       }
       if (tid == 0) arcs_total += total;
       __syncthreads();
@@ -896,6 +944,9 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
       const long long t = clock64();
       prof[1] += t - tclk;
       prof[6] += sm.passes;
+      prof[8] += sm.n_slots;
+      prof[9] += sm.eps_items;
+      prof[10] += sm.eps_arcs;
       tclk = t;
     }
     const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
@@ -917,6 +968,7 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
       prof[2] += t - tclk;
       tclk = t;
     }
+    prof[11] += sm.cnt;
     if (status == CTW_OK) {
       const int in_beam = sm.cnt;
       const bool select = (long long)in_beam > a.cfg.max_active;
