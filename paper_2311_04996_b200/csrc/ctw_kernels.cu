@@ -35,6 +35,7 @@
 #include "ctw_common.h"
 
 #define CTW_BS 256
+#define CTW_WARPS (CTW_BS / 32)
 #define CTW_IPT 4                        // sources per thread per expansion tile
 #define CTW_TILE (CTW_BS * CTW_IPT)
 #define CTW_MAX_SMEM_WIDTH 4096
@@ -225,21 +226,23 @@ struct __align__(16) Smem {
   typedef cub::BlockScan<int, CTW_BS> Scan;
   typename Scan::TempStorage scan;
   union {
-    struct {  // emitting-expansion tile
-      double cost[CTW_TILE];
-      int off[CTW_TILE];
-      uint32_t beg[CTW_TILE];
-    };
+    struct {  // emitting expansion: each warp's current chunk of 32 sources
+      double cost[CTW_WARPS][32];
+      int off[CTW_WARPS][32];
+      uint32_t beg[CTW_WARPS][32];
+    } em;
+    struct {  // epsilon closure: each warp's current chunk of 32 frontier items
+      double cost[CTW_WARPS][32];
+      unsigned long long gb[CTW_WARPS][32];  // slot-position prefix handed to discovered successors
+      unsigned long long gu[CTW_WARPS][32];  // the item's own slot position (tie-break)
+      int off[CTW_WARPS][32];
+      uint32_t beg[CTW_WARPS][32];
+      uint32_t aux[CTW_WARPS][32];           // pd << 24 | table index, or CTW_DISC
+    } ep;
     ulonglong2 bbuf[CTW_BBUF];  // max-active boundary bin: (cost key, state)
-    struct {  // epsilon-closure tile: one entry per frontier item
-      double ecost[CTW_ETILE];
-      unsigned long long egb[CTW_ETILE];  // slot-position prefix handed to discovered successors
-      unsigned long long egu[CTW_ETILE];  // the item's own slot position (tie-break)
-      int eoff[CTW_ETILE];
-      uint32_t ebeg[CTW_ETILE];
-      uint32_t eaux[CTW_ETILE];           // pd << 24 | table index, or CTW_DISC
-    };
   };
+  int work;  // dynamic chunk counter of the current stage / pass
+  unsigned long long arcs_acc;  // emitting arcs expanded over the chunk (diagnostics)
   uint32_t bhist[CTW_NB];
   uint32_t hist[256];
   int sel_bin;     // boundary bin (CTW_NB = no select)
@@ -310,6 +313,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
   for (long long pass = 1;; ++pass) {
     if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
     if (tid == 0) {
+      sm.work = 0;
       sm.eps_items += n_cur;
       sm.passes = (int)pass;
       sm.n_next = 0;
@@ -320,71 +324,69 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
     const uint32_t epoch = (uint32_t)pass;
     uint2* nxt = bufs[(ci + 1) % 3];
     uint2* tiny = bufs[(ci + 2) % 3];
-    for (int tile = 0; tile < n_cur; tile += CTW_ETILE) {
-      // -- setup: per frontier item its epsilon range, cost, tie-break data
-      int deg[CTW_EIPT];
-      int tsum = 0;
-#pragma unroll
-      for (int j = 0; j < CTW_EIPT; ++j) {
-        const int li = tid * CTW_EIPT + j;
-        const int i = tile + li;
-        deg[j] = 0;
-        if (i < n_cur) {
-          const uint2 it = cur[i];
-          const CtwStateRange r = g.ranges[it.y];
-          deg[j] = (int)(r.emit_beg - r.eps_beg);
-          if (deg[j] > 0) {
-            const CtwTok* eu = &L.T[it.x];
-            const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
-            const unsigned long long gu = __ldcg(&eu->gpos);
-            const double c = key2d(v.x);
-            const bool valued = v.x != ~0ULL && !(L.prune && c > running_cut(sm, beam));
-            uint32_t aux = CTW_DISC;
-            if (valued) {
-              const uint32_t tbu = (uint32_t)v.y, auxu = (uint32_t)(v.y >> 32);
-              uint32_t pd = 1;
-              if (tbu & CTW_EPS_BIT) {
-                const uint32_t pred = auxu & CTW_PRED_MASK;
-                pd = (auxu >> CTW_PRED_BITS) + (gu < __ldcg(&L.T[pred].gpos) ? 1u : 0u);
-                pd = min(pd, 255u);
-              }
-              aux = (pd << CTW_PRED_BITS) | it.x;
+    // warps grab 32 frontier items at a time (no block barriers inside a
+    // pass) and spread the items' epsilon arcs over their lanes
+    const int lane = tid & 31, w = tid >> 5;
+    for (;;) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&sm.work, 32);
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (base >= n_cur) break;
+      const int nv = min(32, n_cur - base);
+      int deg = 0;
+      if (lane < nv) {
+        const uint2 it = cur[base + lane];
+        const CtwStateRange r = g.ranges[it.y];
+        deg = (int)(r.emit_beg - r.eps_beg);
+        if (deg > 0) {
+          const CtwTok* eu = &L.T[it.x];
+          const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
+          const unsigned long long gu = __ldcg(&eu->gpos);
+          const double c = key2d(v.x);
+          const bool valued = v.x != ~0ULL && !(L.prune && c > running_cut(sm, beam));
+          uint32_t aux = CTW_DISC;
+          if (valued) {
+            const uint32_t tbu = (uint32_t)v.y, auxu = (uint32_t)(v.y >> 32);
+            uint32_t pd = 1;
+            if (tbu & CTW_EPS_BIT) {
+              const uint32_t pred = auxu & CTW_PRED_MASK;
+              pd = (auxu >> CTW_PRED_BITS) + (gu < __ldcg(&L.T[pred].gpos) ? 1u : 0u);
+              pd = min(pd, 255u);
             }
-            sm.ecost[li] = c;
-            sm.egu[li] = gu;
-            sm.egb[li] = (((gu >> 56) + 1) << 56) | ((gu << 4) & CTW_KEY56);
-            sm.ebeg[li] = r.eps_beg;
-            sm.eaux[li] = aux;
+            aux = (pd << CTW_PRED_BITS) | it.x;
           }
+          sm.ep.cost[w][lane] = c;
+          sm.ep.gu[w][lane] = gu;
+          sm.ep.gb[w][lane] = (((gu >> 56) + 1) << 56) | ((gu << 4) & CTW_KEY56);
+          sm.ep.beg[w][lane] = r.eps_beg;
+          sm.ep.aux[w][lane] = aux;
         }
-        tsum += deg[j];
       }
-      int excl, total;
-      Smem::Scan(sm.scan).ExclusiveSum(tsum, excl, total);
-      if (tid == 0) sm.eps_arcs += total;
+      int incl = deg;
 #pragma unroll
-      for (int j = 0; j < CTW_EIPT; ++j) {
-        sm.eoff[tid * CTW_EIPT + j] = excl;
-        excl += deg[j];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
       }
-      __syncthreads();
-      // -- flat, load-balanced loop over the tile's epsilon arcs
-      const int nt = min(CTW_ETILE, n_cur - tile);
-      for (int k = tid; k < total; k += CTW_BS) {
-        int lo = 0, hi = nt - 1;  // last item with eoff <= k
+      sm.ep.off[w][lane] = incl - deg;
+      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (lane == 0) atomicAdd(&sm.eps_arcs, total);
+      __syncwarp();
+      for (int k = lane; k < total; k += 32) {
+        int lo = 0, hi = nv - 1;  // last item with off <= k
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (sm.eoff[mid] <= k) lo = mid;
+          if (sm.ep.off[w][mid] <= k) lo = mid;
           else hi = mid - 1;
         }
-        const uint32_t o = (uint32_t)(k - sm.eoff[lo]);
-        const uint32_t a = sm.ebeg[lo] + o;
-        const uint32_t aux = sm.eaux[lo];
+        const uint32_t o = (uint32_t)(k - sm.ep.off[w][lo]);
+        const uint32_t a = sm.ep.beg[w][lo] + o;
+        const uint32_t aux = sm.ep.aux[w][lo];
         const bool valued = aux != CTW_DISC;
         const CtwArc arc = g.arcs[a];
         double nc = arc.weight;
         if (valued) {
-          nc = __dadd_rn(sm.ecost[lo], arc.weight);
+          nc = __dadd_rn(sm.ep.cost[w][lo], arc.weight);
           if (boost) {
             const int32_t ol = g.olabel[a];
             if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
@@ -400,13 +402,13 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
         }
         if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
         CtwTok* ed = &L.T[d];
-        gpos_min(ed, sm.egb[lo] | min(o, 15u));
+        gpos_min(ed, sm.ep.gb[w][lo] | min(o, 15u));
         const uint2 item = make_uint2(d, (uint32_t)arc.nextstate);
         bool push = false, big = false;
         if (valued) {
           unsigned long long oldk;
           const unsigned long long nk = d2key(nc);
-          if (tok_relax_from(L, ed, nk, CTW_EPS_BIT | a, aux, sm.egu[lo], seen, &oldk)) {
+          if (tok_relax_from(L, ed, nk, CTW_EPS_BIT | a, aux, sm.ep.gu[w][lo], seen, &oldk)) {
             track_min(sm, nk);
             push = true;
             big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
@@ -435,8 +437,9 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
           }
         }
       }
-      __syncthreads();
+      __syncwarp();
     }
+    __syncthreads();
     if (sm.status >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
     int n_next = min((uint32_t)sm.n_next, L.tcap);
     if (!sm.any_big) return CTW_OK;  // a quiet pass (only <= relax_eps changes) ends the closure
@@ -826,11 +829,12 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
   int status = CTW_OK;
   int err_frame = -1;
   int n_slots_max = 0;
-  long long arcs_total = 0, src_total = 0, rec_need = 0;
+  long long src_total = 0, rec_need = 0;
   long long prof[CTW_NPROF] = {0};
   if (tid == 0) {
     sm.status = CTW_OK;
     sm.pool_used = lane.pool_used;
+    sm.arcs_acc = 0;
   }
   __syncthreads();
 
@@ -841,6 +845,7 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
     const int nxt_buf = (f & 1) ? w1 : w0;
     CtwSrc* nsrc = lane.src[nxt_buf];
     if (tid == 0) {
+      sm.work = 0;
       sm.eps_items = 0;
       sm.eps_arcs = 0;
       sm.n_slots = 0;
@@ -861,72 +866,75 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
     src_total += n_src;
 
     // ---- emitting expansion, load-balanced over out-degree ----
-    for (int tile = 0; tile < n_src; tile += CTW_TILE) {
-      int deg[CTW_IPT];
-      int tsum = 0;
-#pragma unroll
-      for (int j = 0; j < CTW_IPT; ++j) {
-        const int li = tid * CTW_IPT + j;
-        const int i = tile + li;
-        deg[j] = 0;
-        if (i < n_src) {
-          const CtwSrc t = src[i];
+    {
+      // warps grab 32 sources at a time and spread their emitting arcs over
+      // the lanes (warp scan of out-degrees; no block barriers)
+      const int lane = tid & 31, w = tid >> 5;
+      for (;;) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&sm.work, 32);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base >= n_src) break;
+        const int nv = min(32, n_src - base);
+        int deg = 0;
+        if (lane < nv) {
+          const CtwSrc t = src[base + lane];
           const CtwStateRange r = g.ranges[t.state];
-          deg[j] = (int)(r.emit_end - r.emit_beg);
-          sm.beg[li] = r.emit_beg;
-          sm.cost[li] = t.cost;
+          deg = (int)(r.emit_end - r.emit_beg);
+          sm.em.beg[w][lane] = r.emit_beg;
+          sm.em.cost[w][lane] = t.cost;
         }
-        tsum += deg[j];
-      }
-      int excl, total;
-      Smem::Scan(sm.scan).ExclusiveSum(tsum, excl, total);
+        int incl = deg;
 #pragma unroll
-      for (int j = 0; j < CTW_IPT; ++j) {
-        sm.off[tid * CTW_IPT + j] = excl;
-        excl += deg[j];
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        sm.em.off[w][lane] = incl - deg;
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (lane == 0) atomicAdd(&sm.arcs_acc, (unsigned long long)total);
+        __syncwarp();
+        for (int k = lane; k < total; k += 32) {
+          int lo = 0, hi = nv - 1;  // last source with off <= k
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.em.off[w][mid] <= k) lo = mid;
+            else hi = mid - 1;
+          }
+          const uint32_t arc_i = sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]);
+          const CtwArc arc = g.arcs[arc_i];
+          double ac;
+          if (smem_ll) ac = nll_s[arc.ilabel - 1];
+          else {
+            const long long idx = row0 + arc.ilabel - 1;
+            const double x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+            ac = __dmul_rn(neg_scale, x);
+          }
+          double nc = __dadd_rn(__dadd_rn(sm.em.cost[w][lo], ac), arc.weight);
+          if (boost) {
+            const int32_t ol = g.olabel[arc_i];
+            if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+          }
+          if (!(nc < INF)) continue;
+          bool is_new = false;
+          ulonglong2 seen;
+          const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
+          if (d == CTW_EMPTY) {
+            atomicMax(&sm.status, CTW_GROW_TABLE);
+            continue;
+          }
+          if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
+          CtwTok* ed = &L.T[d];
+          // Gauss-Seidel slot position of an emitting-reached state = its
+          // first-arrival arc (_kernel.pyx:256-272)
+          gpos_min(ed, (unsigned long long)arc_i);
+          if (L.prune && nc > running_cut(sm, a.cfg.beam)) continue;  // cannot make the final beam
+          unsigned long long oldk;
+          const unsigned long long nk = d2key(nc);
+          if (tok_relax_from(L, ed, nk, arc_i, (uint32_t)(base + lo), 0ULL, seen, &oldk)) track_min(sm, nk);
+        }
+        __syncwarp();
       }
-      __syncthreads();
-      const int nt = min(CTW_TILE, n_src - tile);
-      for (int k = tid; k < total; k += CTW_BS) {
-        int lo = 0, hi = nt - 1;  // last j with off[j] <= k
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (sm.off[mid] <= k) lo = mid;
-          else hi = mid - 1;
-        }
-        const uint32_t arc_i = sm.beg[lo] + (uint32_t)(k - sm.off[lo]);
-        const CtwArc arc = g.arcs[arc_i];
-        double ac;
-        if (smem_ll) ac = nll_s[arc.ilabel - 1];
-        else {
-          const long long idx = row0 + arc.ilabel - 1;
-          const double x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
-          ac = __dmul_rn(neg_scale, x);
-        }
-        double nc = __dadd_rn(__dadd_rn(sm.cost[lo], ac), arc.weight);
-        if (boost) {
-          const int32_t ol = g.olabel[arc_i];
-          if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
-        }
-        if (!(nc < INF)) continue;
-        bool is_new = false;
-        ulonglong2 seen;
-        const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
-        if (d == CTW_EMPTY) {
-          atomicMax(&sm.status, CTW_GROW_TABLE);
-          continue;
-        }
-        if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
-        CtwTok* ed = &L.T[d];
-        // Gauss-Seidel slot position of an emitting-reached state = its
-        // first-arrival arc (_kernel.pyx:256-272)
-        gpos_min(ed, (unsigned long long)arc_i);
-        if (L.prune && nc > running_cut(sm, a.cfg.beam)) continue;  // cannot make the final beam
-        unsigned long long oldk;
-        const unsigned long long nk = d2key(nc);
-        if (tok_relax_from(L, ed, nk, arc_i, (uint32_t)(tile + lo), 0ULL, seen, &oldk)) track_min(sm, nk);
-      }
-      if (tid == 0) arcs_total += total;
       __syncthreads();
     }
 
@@ -1058,7 +1066,7 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
     o.status = status;
     o.err_frame = err_frame;
     o.n_slots_max = n_slots_max;
-    o.arcs_expanded = arcs_total;
+    o.arcs_expanded = (long long)sm.arcs_acc;
     o.src_total = src_total;
     o.rec_need = rec_need;
     for (int k = 0; k < CTW_NPROF; ++k) o.prof[k] = prof[k];
