@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=24, help="utterances in the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small", action="store_true", help="tiny graph smoke run (not a bench number)")
+    ap.add_argument("--streams", type=int, default=2000, help="C4 streaming channels (0 = skip)")
+    ap.add_argument("--stream-seconds", type=float, default=5.0, help="audio per stream in the C4 run")
+    ap.add_argument("--cpu-streams", type=int, default=32, help="streams in the CPU reference C4 run")
     return ap.parse_args()
 
 
@@ -183,9 +186,52 @@ def _stage_profile(prof, st):
     out["cycles_per_lane_frame"] = tot / lf
     out["eps_passes_per_frame"] = prof["eps_passes"] / lf
     out["select_frame_frac"] = prof["select_frames"] / lf
-    for k in ("slots", "eps_items", "eps_arcs", "in_beam"):
+    for k in ("slots", "eps_items", "eps_arcs", "in_beam", "tie_frames", "ties", "eps_disc_arcs"):
         out[k + "_per_lane_frame"] = prof[k] / lf
     return out
+
+
+def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cores=1):
+    """BASELINE config 4: n_streams concurrent channels, 0.5 s chunks (12/13
+    frames alternate via 12-frame chunks of 40 ms frames = 0.48 s), two chunks
+    per second per stream, arrivals staggered; measured-service simulation of
+    the reference's stream-sim scheduler (cli.py:209-297) through the public
+    StreamPool API. Returns latency stats (p50/p99 per the reference's
+    order-statistic convention) and the final hypotheses."""
+    from paper_2311_04996_b200 import streamsim
+
+    frames = int(round(seconds / FRAME_S))
+    utts = list(workload(s, n_streams, frames, 7000 + seed))
+    if reference:
+        ctcwfst = ref_module()
+        from ctcwfst.streaming import BatcherConfig, Chunk, StreamPool
+
+        pool = StreamPool(ref_flatgraph(ctcwfst, s.graph), ctcwfst.DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE),
+                          BatcherConfig(max_batch=max(1, cores)), workers=cores)
+        res = streamsim.simulate(pool, Chunk, [u.astype(np.float64) for u in utts], chunk_frames=12, rate=2.0,
+                                 max_batch=max(1, cores))
+        pool.close()
+    else:
+        import torch
+
+        from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, StreamPool
+
+        pool = StreamPool(s.graph, DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE),
+                          BatcherConfig(max_batch=n_streams), device=device)
+        lp = s.graph.device_graph(device).pool(DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE), s.graph.num_states)
+        k0 = lp.stats()
+        res = streamsim.simulate(pool, Chunk, utts, chunk_frames=12, rate=2.0, max_batch=n_streams,
+                                 sync=torch.cuda.synchronize)
+        k1 = lp.stats()
+        pool.close()
+    st = res.stats()
+    if not reference:
+        st["breakdown_s"] = {k: round(v, 4) for k, v in pool.timing.items()}
+        st["breakdown_s"]["frame_kernel_s"] = round((k1["decode_ms"] - k0["decode_ms"]) / 1e3, 4)
+        st["breakdown_s"]["frame_kernel_launches"] = k1["decode_launches"] - k0["decode_launches"]
+    st.update(streams=n_streams, audio_s_per_stream=frames * FRAME_S, chunk_s=12 * FRAME_S,
+              arrivals_per_stream_per_s=2.0)
+    return st, res.finals, utts
 
 
 def dist_setup(args):
@@ -354,6 +400,21 @@ def main():
         "clocks": clk.summary(),
         "stage_profile": _stage_profile(prof, st),
     }
+    if args.streams > 0:
+        # warm-up: the same number of channels for one second (lane tables and
+        # histories grow to their steady-state sizes; lanes are then recycled)
+        streaming_run(s, args.streams, 1.0, rank + 100, device=dev)
+        st, finals, sutts = streaming_run(s, args.streams, args.stream_seconds, rank, device=dev)
+        line["streaming"] = {"gpu": st}
+        if world == 1 and not args.no_cpu and args.cpu_streams > 0:
+            cores = cores_available()
+            cst, cfinals, _ = streaming_run(s, args.cpu_streams, args.stream_seconds, rank, reference=True,
+                                            cores=cores)
+            cst["cores"] = cores
+            line["streaming"]["cpu_reference"] = cst
+            # same utterances, same scheduler: transcripts must agree
+            line["streaming"]["parity_words_identical"] = all(
+                finals[k].words == cfinals[k].words for k in range(args.cpu_streams))
     if world == 1 and not args.no_cpu:
         k = min(args.cpu_sample, n)
         cores = cores_available()

@@ -149,11 +149,13 @@ int ctw_lanes_stats(ctw_lanes* l, int64_t* launches, int64_t* decode_launches, d
                     int64_t* arcs, int64_t* src_tokens, int64_t* frames, int64_t* max_slots);
 int ctw_lanes_reset_stats(ctw_lanes* l);
 /* Per-stage profile of the frame kernel summed over lanes and frames since
- * the last reset (12 counters): SM cycles of [0] emitting expansion, [1]
+ * the last reset (16 counters): SM cycles of [0] emitting expansion, [1]
  * epsilon closure, [2] beam count, [3] max-active select, [4] records, [5]
  * table reset; [6] epsilon passes, [7] frames needing the select, [8] slots,
- * [9] epsilon frontier items, [10] epsilon arcs relaxed, [11] in-beam slots. */
-int ctw_lanes_profile(ctw_lanes* l, int64_t* out12);
+ * [9] epsilon frontier items, [10] epsilon arcs relaxed, [11] in-beam slots,
+ * [12] frames with an epsilon/epsilon tie between distinct predecessors,
+ * [13] such ties, [14] epsilon arcs relaxed for discovery only, [15] reserved. */
+int ctw_lanes_profile(ctw_lanes* l, int64_t* out16);
 void* ctw_lanes_stream(ctw_lanes* l);
 
 /* The reference kernel contract (_pykernel.py:28-248) on the GPU: same inputs

@@ -65,6 +65,22 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+// Lane buffers come from the stream-ordered pool allocator: growing a lane
+// (table, history, pool) is an async alloc + copy + free on the lane stream,
+// with no device-wide synchronisation.
+template <class T>
+cudaError_t salloc(T** p, size_t n, cudaStream_t st) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  return cudaMallocAsync((void**)p, n * sizeof(T), st);
+}
+
+template <class T>
+void sfree(T*& p, cudaStream_t st) {
+  if (p) cudaFreeAsync((void*)p, st);
+  p = nullptr;
+}
+
 uint32_t ceil_log2(uint64_t x) {
   uint32_t r = 0;
   while ((1ull << r) < x) ++r;
@@ -134,6 +150,7 @@ struct ctw_lanes {
   int64_t launches = 0, decode_launches = 0, arcs = 0, srcs = 0, frames = 0, max_slots = 0;
   double decode_ms = 0.0;
   int64_t prof[CTW_NPROF] = {0};
+  uint32_t tlog2_hint = 0;  // largest token-table size any lane of this set grew to
   std::mutex mu;
 };
 
@@ -146,17 +163,17 @@ int sync_lane(ctw_lanes* l, int i) {
   return 0;
 }
 
-void free_lane(CtwLane& L) {
-  dfree(L.table);
-  dfree(L.slots);
-  dfree(L.front);
-  for (auto& s : L.src) dfree(s);
-  dfree(L.pend);
-  dfree(L.rec_link);
-  dfree(L.rec_state);
-  dfree(L.rec_cost);
-  dfree(L.frame_base);
-  dfree(L.pool);
+void free_lane(CtwLane& L, cudaStream_t st) {
+  sfree(L.table, st);
+  sfree(L.slots, st);
+  sfree(L.front, st);
+  for (auto& s : L.src) sfree(s, st);
+  sfree(L.pend, st);
+  sfree(L.rec_link, st);
+  sfree(L.rec_state, st);
+  sfree(L.rec_cost, st);
+  sfree(L.frame_base, st);
+  sfree(L.pool, st);
 }
 
 // (Re)allocate the table-sized buffers of lane i at capacity 1 << tlog2,
@@ -170,11 +187,12 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   uint2 *slots, *front;
   CtwSrc* src[3];
   int32_t* pend;
-  CUDA_TRY(dalloc(&table, tcap));
-  CUDA_TRY(dalloc(&slots, tcap));
-  CUDA_TRY(dalloc(&front, 3 * tcap));
-  for (int b = 0; b < 3; ++b) CUDA_TRY(dalloc(&src[b], scap));
-  CUDA_TRY(dalloc(&pend, scap));
+  cudaStream_t st = l->stream;
+  CUDA_TRY(salloc(&table, tcap, st));
+  CUDA_TRY(salloc(&slots, tcap, st));
+  CUDA_TRY(salloc(&front, 3 * tcap, st));
+  for (int b = 0; b < 3; ++b) CUDA_TRY(salloc(&src[b], scap, st));
+  CUDA_TRY(salloc(&pend, scap, st));
   if (ctw_launch_clear(table, (uint32_t)tcap, l->stream)) return fail(-1, "clear kernel launch failed");
   if (L.table) {
     if (L.n_src > 0) {
@@ -183,12 +201,11 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
       CUDA_TRY(cudaMemcpyAsync(pend, L.pend, (size_t)L.n_src * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                l->stream));
     }
-    CUDA_TRY(cudaStreamSynchronize(l->stream));
-    dfree(L.table);
-    dfree(L.slots);
-    dfree(L.front);
-    for (auto& s : L.src) dfree(s);
-    dfree(L.pend);
+    sfree(L.table, st);
+    sfree(L.slots, st);
+    sfree(L.front, st);
+    for (auto& s : L.src) sfree(s, st);
+    sfree(L.pend, st);
   }
   L.table = table;
   L.slots = slots;
@@ -196,16 +213,16 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   for (int b = 0; b < 3; ++b) L.src[b] = src[b];
   L.pend = pend;
   L.tlog2 = tlog2;
+  l->tlog2_hint = std::max(l->tlog2_hint, tlog2);
   return sync_lane(l, i);
 }
 
 template <class T>
 int grow_keep(cudaStream_t st, T*& p, int64_t keep, int64_t ncap) {
   T* np;
-  CUDA_TRY(dalloc(&np, (size_t)ncap));
+  CUDA_TRY(salloc(&np, (size_t)ncap, st));
   if (p && keep > 0) CUDA_TRY(cudaMemcpyAsync(np, p, (size_t)keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  dfree(p);
+  sfree(p, st);
   p = np;
   return 0;
 }
@@ -213,7 +230,7 @@ int grow_keep(cudaStream_t st, T*& p, int64_t keep, int64_t ncap) {
 int grow_hist(ctw_lanes* l, int i, int64_t need) {
   CtwLane& L = l->h[i];
   if (need <= L.rcap) return 0;
-  int64_t ncap = std::max<int64_t>(need, L.rcap + L.rcap / 2);
+  int64_t ncap = std::max<int64_t>(need, 2 * L.rcap);
   if (int r = grow_keep(l->stream, L.rec_link, L.n_rec, ncap)) return r;
   if (int r = grow_keep(l->stream, L.rec_state, L.n_rec, ncap)) return r;
   if (int r = grow_keep(l->stream, L.rec_cost, L.n_rec, ncap)) return r;
@@ -245,16 +262,19 @@ int init_lane(ctw_lanes* l, int i) {
   CtwLane& L = l->h[i];
   std::memset(&L, 0, sizeof(L));
   const uint64_t S = (uint64_t)std::max<int64_t>(l->g->S, 1);
-  const uint32_t tlog2 = std::min<uint32_t>(std::max<uint32_t>(6, ceil_log2(2 * S + 2)), 16);
+  // new lanes start at the largest table any lane of this set needed
+  const uint32_t tlog2 = std::max(std::min<uint32_t>(std::max<uint32_t>(6, ceil_log2(2 * S + 2)), 16),
+                                  std::min<uint32_t>(l->tlog2_hint, ceil_log2(2 * S + 2)));
   if (int r = alloc_table(l, i, tlog2)) return r;
   L.rcap = 1 << 12;
   L.fcap = 256;
   L.pcap = 1 << 10;
-  CUDA_TRY(dalloc(&L.rec_link, (size_t)L.rcap));
-  CUDA_TRY(dalloc(&L.rec_state, (size_t)L.rcap));
-  CUDA_TRY(dalloc(&L.rec_cost, (size_t)L.rcap));
-  CUDA_TRY(dalloc(&L.frame_base, (size_t)L.fcap));
-  CUDA_TRY(dalloc(&L.pool, (size_t)L.pcap));
+  cudaStream_t st = l->stream;
+  CUDA_TRY(salloc(&L.rec_link, (size_t)L.rcap, st));
+  CUDA_TRY(salloc(&L.rec_state, (size_t)L.rcap, st));
+  CUDA_TRY(salloc(&L.rec_cost, (size_t)L.rcap, st));
+  CUDA_TRY(salloc(&L.frame_base, (size_t)L.fcap, st));
+  CUDA_TRY(salloc(&L.pool, (size_t)L.pcap, st));
   return sync_lane(l, i);
 }
 
@@ -492,6 +512,14 @@ int ctw_lanes_create(ctw_graph* g, int32_t n_lanes, const ctw_config* cfg, void*
   if (!(cfg->beam > 0) || cfg->max_active < 1 || !(cfg->acoustic_scale > 0))
     return fail(-1, "invalid decoder config");
   CUDA_TRY(cudaSetDevice(g->device));
+  {
+    // keep freed lane memory in the pool (no release at synchronisation points)
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, g->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   ctw_lanes* l = new ctw_lanes();
   l->g = g;
   {
@@ -525,9 +553,10 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   cudaSetDevice(l->g->device);
   cudaStreamSynchronize(l->stream);
   for (int i = 0; i < l->n; ++i) {
-    free_lane(l->h[i]);
+    free_lane(l->h[i], l->stream);
     dfree(l->boost_buf[i]);
   }
+  cudaStreamSynchronize(l->stream);
   if (l->h) cudaFreeHost(l->h);
   dfree(l->d);
   dfree(l->d_ids);

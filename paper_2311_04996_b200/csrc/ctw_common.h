@@ -119,10 +119,12 @@ struct CtwLaneOut {
   // [0] emitting expansion, [1] epsilon closure, [2] beam count + pass check,
   // [3] max-active select, [4] records, [5] table reset, [6] epsilon passes,
   // [7] frames that needed the select, [8] slots, [9] epsilon frontier items,
-  // [10] epsilon arcs relaxed, [11] in-beam slots
-  int64_t prof[12];
+  // [10] epsilon arcs relaxed, [11] in-beam slots, [12] frames with an
+  // equal-cost epsilon/epsilon tie between distinct predecessors, [13] such ties,
+  // [14] epsilon arcs from predecessors outside the running beam (discovery only)
+  int64_t prof[16];
 };
-#define CTW_NPROF 12
+#define CTW_NPROF 16
 
 struct CtwDecodeCfg {
   double beam;

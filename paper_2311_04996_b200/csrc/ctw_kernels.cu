@@ -101,6 +101,7 @@ struct LaneCtx {
   int pool_cap;
   int32_t* pool;
   bool prune;    // CtwLane::prune_ok
+  int* tie_ctr;  // diagnostics: epsilon/epsilon ties between distinct predecessors
 };
 
 // Find-or-insert `d` (linear probing). Returns the table index or CTW_EMPTY
@@ -193,6 +194,7 @@ __device__ __forceinline__ bool tok_relax_from(const LaneCtx& L, CtwTok* e, unsi
         if (tb >= ctb) return false;  // emitting: first (lowest) arc wins
       } else {
         if (!(ctb & CTW_EPS_BIT)) return false;  // equal-cost emitting / seed winner stays
+        if (((uint32_t)(chi >> 32) & CTW_PRED_MASK) != (aux & CTW_PRED_MASK) && L.tie_ctr) atomicAdd(L.tie_ctr, 1);
         if (!gs_before(L.T, aux >> CTW_PRED_BITS, aux & CTW_PRED_MASK, tb & ~CTW_EPS_BIT, gpos_pred,
                        (uint32_t)(chi >> 32), ctb & ~CTW_EPS_BIT))
           return false;
@@ -263,6 +265,8 @@ struct __align__(16) Smem {
   int passes;
   int eps_items;
   int eps_arcs;
+  int eps_ties;
+  int eps_disc;
   int status;
   int cnt;
   int max_pd;
@@ -371,6 +375,11 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
       sm.ep.off[w][lane] = incl - deg;
       const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
       if (lane == 0) atomicAdd(&sm.eps_arcs, total);
+      {
+        int dsc = (lane < nv && deg > 0 && sm.ep.aux[w][lane] == CTW_DISC) ? deg : 0;
+        for (int o = 16; o; o >>= 1) dsc += __shfl_xor_sync(0xFFFFFFFFu, dsc, o);
+        if (lane == 0) atomicAdd(&sm.eps_disc, dsc);
+      }
       __syncwarp();
       for (int k = lane; k < total; k += 32) {
         int lo = 0, hi = nv - 1;  // last item with off <= k
@@ -640,6 +649,7 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane) {
   L.pool = lane.pool;
   L.pool_cap = lane.pcap;
   L.prune = lane.prune_ok != 0;
+  L.tie_ctr = nullptr;
   return L;
 }
 
@@ -812,7 +822,8 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
   const int tid = threadIdx.x;
   const int b = blockIdx.x;
   CtwLane& lane = lanes[a.lane_ids[b]];
-  const LaneCtx L = lane_ctx(lane);
+  LaneCtx L = lane_ctx(lane);
+  L.tie_ctr = &sm.eps_ties;
   const int F = a.nframes[b];
   const double* boost = lane.boost;
   const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
@@ -848,6 +859,8 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
       sm.work = 0;
       sm.eps_items = 0;
       sm.eps_arcs = 0;
+      sm.eps_ties = 0;
+      sm.eps_disc = 0;
       sm.n_slots = 0;
       sm.min_key = ~0ULL;
       sm.cnt = 0;
@@ -955,6 +968,9 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
       prof[8] += sm.n_slots;
       prof[9] += sm.eps_items;
       prof[10] += sm.eps_arcs;
+      prof[12] += sm.eps_ties > 0;
+      prof[13] += sm.eps_ties;
+      prof[14] += sm.eps_disc;
       tclk = t;
     }
     const int n_slots = min((uint32_t)sm.n_slots, L.tcap);

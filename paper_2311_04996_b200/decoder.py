@@ -294,10 +294,10 @@ class LanePool:
 
     def profile(self) -> dict:
         """Per-stage SM cycles of the frame kernel (ctw_lanes_profile)."""
-        v = np.zeros(12, np.int64)
+        v = np.zeros(16, np.int64)
         _lib.load().ctw_lanes_profile(self.handle, _lib.ptr(v))
         names = ("emit", "eps", "beam_count", "select", "records", "reset", "eps_passes", "select_frames",
-                 "slots", "eps_items", "eps_arcs", "in_beam")
+                 "slots", "eps_items", "eps_arcs", "in_beam", "tie_frames", "ties", "eps_disc_arcs", "r15")
         return dict(zip(names, (int(x) for x in v)))
 
     def reset_stats(self) -> None:

@@ -426,13 +426,15 @@ def planted_utterances(sys_: System, n: int, frames: int, seed: int = 0, gap: fl
 def conformer_logprobs(sys_: System, n: int, frames: int, seed: int = 0, delta: float = 6.0,
                        sigma: float = 1.5, dtype=np.float32) -> np.ndarray:
     """(n, frames, V) log-softmax of N(0, sigma) logits with +delta on a
-    planted CTC path (blank-dominant, Conformer-CTC shaped)."""
-    rng = np.random.default_rng(seed)
+    planted CTC path (blank-dominant, Conformer-CTC shaped). Utterance i
+    depends only on (seed, i), not on n."""
     V = sys_.num_units
-    logits = rng.normal(0.0, sigma, size=(n, frames, V))
+    out = np.empty((n, frames, V), dtype=dtype)
     for i in range(n):
+        rng = np.random.default_rng([seed, i])
+        logits = rng.normal(0.0, sigma, size=(frames, V))
         path = render_path(rng, sys_, frames)
-        logits[i, np.arange(frames), path] += delta
-    m = logits.max(axis=-1, keepdims=True)
-    lp = logits - m - np.log(np.exp(logits - m).sum(axis=-1, keepdims=True))
-    return lp.astype(dtype)
+        logits[np.arange(frames), path] += delta
+        m = logits.max(axis=-1, keepdims=True)
+        out[i] = logits - m - np.log(np.exp(logits - m).sum(axis=-1, keepdims=True))
+    return out
