@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return OUT
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-o", str(OUT), *map(str, SRC)]
+           "-o", str(OUT), *os.environ.get("CTW_NVCC_FLAGS", "").split(), *map(str, SRC)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -189,8 +189,8 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   int32_t* pend;
   cudaStream_t st = l->stream;
   CUDA_TRY(salloc(&table, tcap, st));
-  CUDA_TRY(salloc(&slots, tcap, st));
-  CUDA_TRY(salloc(&front, 3 * tcap, st));
+  CUDA_TRY(salloc(&slots, CTW_SLOTS_LEN(tcap), st));
+  CUDA_TRY(salloc(&front, CTW_FRONT_LEN(tcap), st));
   for (int b = 0; b < 3; ++b) CUDA_TRY(salloc(&src[b], scap, st));
   CUDA_TRY(salloc(&pend, scap, st));
   if (ctw_launch_clear(table, (uint32_t)tcap, l->stream)) return fail(-1, "clear kernel launch failed");
@@ -340,6 +340,7 @@ int reserve_lanes(ctw_lanes* l, int n) {
 int32_t prune_flag(const ctw_lanes* l, const double* boost, int64_t len) {
   const ctw_graph* g = l->g;
   if (!g->eps_nonneg || l->cfg.max_ne_iters < (1 << 16)) return 0;
+  if (getenv("CTW_NOPRUNE")) return 0;  // diagnostics: exact full closure
   if (boost && g->eps_olabel)
     for (int64_t i = 0; i < len; ++i)
       if (!(boost[i] >= 0.0)) return 0;

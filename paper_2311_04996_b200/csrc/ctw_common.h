@@ -77,11 +77,20 @@ struct __align__(16) CtwSrc {
 
 // Device-side descriptor of one lane (= one decoding channel). The host owns
 // the authoritative copy; kernels read it and write the committed fields back.
+// A lane is decoded by one thread-block cluster of up to CTW_RMAX CTAs
+// ("ranks"). Every rank appends the slots it creates to its own segment of
+// the slot list and the epsilon frontiers it produces to its own segments of
+// the frontier sets; segments hold tcap/2 entries (the table is grown before
+// it is half full, so a segment never needs more).
+#define CTW_RMAX 8
+#define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_RMAX * ((tcap) / 2))
+#define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_RMAX * ((tcap) / 2))
+
 struct CtwLane {
   // token hash table: capacity 1 << tlog2
   CtwTok* table;
-  uint2* slots;      // [tcap]  (table index, state) of each slot, discovery order
-  uint2* front;      // [3 * tcap] epsilon frontier buffers (same pairs)
+  uint2* slots;      // [CTW_SLOTS_LEN] (table index, state) per slot; rank r owns [r*tcap/2, (r+1)*tcap/2)
+  uint2* front;      // [CTW_FRONT_LEN] 4 frontier sets x CTW_RMAX rank segments (same pairs); also scratch
   CtwSrc* src[3];    // [tcap/2 + 1] each: committed + two working buffers
   int32_t* pend;     // [tcap/2 + 1] pending olabel segment of seeded sources
   int2* rec_link;    // [rcap] {prev record, olabel code}

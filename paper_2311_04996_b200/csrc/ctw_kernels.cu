@@ -1,10 +1,15 @@
 // ctw_kernels.cu -- sm_100a kernels of the batched WFST beam-search decoder.
 //
-// One CTA owns one lane (= one decoding channel) for a whole chunk of frames
-// and loops over the frames itself: emitting expansion -> epsilon fixpoint ->
-// beam / max-active prune -> records + next sources -> table reset, with only
-// __syncthreads between stages. There is no host round trip and no grid-wide
-// sync inside a chunk; the batch of lanes is the grid.
+// One thread-block CLUSTER (1..CTW_RMAX CTAs, "ranks") owns one lane (= one
+// decoding channel) for a whole chunk of frames and loops over the frames
+// itself: emitting expansion -> epsilon fixpoint -> beam / max-active prune
+// -> records + next sources -> table reset. The ranks of a lane share its
+// token table in global memory (L2), hand out work through counters in rank
+// 0's shared memory (DSMEM atomics) and meet at cluster barriers between
+// stages. There is no host round trip and no grid-wide sync inside a chunk;
+// the batch of lanes x ranks is the grid. Spreading a lane over several SMs
+// cuts the per-frame latency (dependent L2 round trips are the bound) and
+// keeps fewer lanes' token tables live in L2 at a time.
 //
 // Reference semantics (all paths under /root/reference/pkg/src/ctcwfst/):
 //   expansion arithmetic  ((c + (-scale*ll[f, il-1])) + w) (+ boost[ol])
@@ -29,12 +34,21 @@
 // checked against max_ne_iters is the Gauss-Seidel one (1 + max pd). See
 // DESIGN.md "Epsilon closure".
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 #include <stdint.h>
 
 #include "ctw_common.h"
 
-#define CTW_BS 256
+#ifndef CTW_BS
+#define CTW_BS 512
+#endif
+#ifndef CTW_MINB
+#define CTW_MINB (1024 / CTW_BS)
+#endif
+#ifndef CTW_DEFAULT_CLUSTER
+#define CTW_DEFAULT_CLUSTER 8
+#endif
 #define CTW_WARPS (CTW_BS / 32)
 #define CTW_IPT 4                        // sources per thread per expansion tile
 #define CTW_TILE (CTW_BS * CTW_IPT)
@@ -48,7 +62,11 @@
 #define CTW_NB 1024      // cost-histogram bins over [min, min + beam] for the max-active select
 #define CTW_BBUF 1024    // boundary-bin capacity of the exact (cost, state) sort
 
+namespace cg = cooperative_groups;
+
 namespace {
+
+struct Smem;
 
 struct GraphDev {
   const CtwStateRange* ranges;
@@ -97,7 +115,12 @@ __device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
 struct LaneCtx {
   CtwTok* T;
   uint32_t mask, shift, tcap;
-  uint2* slots;  // (table index, state)
+  uint32_t seg;        // entries per rank segment (tcap / 2)
+  uint2* slots;        // this rank's slot segment: (table index, state)
+  uint2* slots_base;   // rank 0's segment (rank k's starts at + k * seg)
+  uint2* front;        // frontier sets (CTW_FRONT_LEN)
+  Smem* G;             // rank 0's shared memory (cluster counters)
+  int rank, nranks;
   int pool_cap;
   int32_t* pool;
   bool prune;    // CtwLane::prune_ok
@@ -224,6 +247,36 @@ __device__ __forceinline__ void tok_clear(CtwTok* e) {
 
 // --------------------------------------------------------- shared memory --
 
+#define CTW_NBIG 1024  // high out-degree sources expanded arc-parallel per frame (list capacity)
+#ifndef CTW_BIG
+#define CTW_BIG 64  // emitting out-degree above which a source is expanded arc-parallel
+#endif
+
+// Per-frame cluster counters. They live in rank 0 and are double-buffered by
+// frame parity: rank 0 zeroes the other parity's copy after the frame-start
+// barrier, when no rank can still read it and none uses it before the next
+// frame-start barrier.
+struct FrameCtr {
+  int work_e;   // emitting: source chunks handed out
+  int work_b;   // emitting: arc chunks of the high-degree list handed out
+  int nbig;     // high-degree sources listed
+  int cnt;      // in-beam slots
+  int max_pd;   // Gauss-Seidel pass depth of the closure
+  int nbb;      // boundary-bin members collected
+  int rec_ctr;  // survivors written (records of the frame)
+  int pad;
+  uint32_t bhist[CTW_NB];      // cost histogram over [min, min + beam]
+};
+
+// One high out-degree source, listed for the arc-parallel pass (global scratch).
+struct BigSrc {
+  int32_t idx;  // source index (emitting winners' aux)
+  uint32_t beg;
+  int32_t deg;
+  int32_t pad;
+  double cost;
+};
+
 struct __align__(16) Smem {
   typedef cub::BlockScan<int, CTW_BS> Scan;
   typename Scan::TempStorage scan;
@@ -241,45 +294,65 @@ struct __align__(16) Smem {
       uint32_t beg[CTW_WARPS][32];
       uint32_t aux[CTW_WARPS][32];           // pd << 24 | table index, or CTW_DISC
     } ep;
-    ulonglong2 bbuf[CTW_BBUF];  // max-active boundary bin: (cost key, state)
+    struct {  // arc-parallel expansion of the high-degree sources
+      int pref[CTW_NBIG + 1];
+      uint32_t beg[CTW_NBIG];
+      int idx[CTW_NBIG];
+      double cost[CTW_NBIG];
+    } bg;
+    ulonglong2 bbuf[CTW_BBUF];  // rank 0: max-active boundary bin (cost key, state)
   };
-  int work;  // dynamic chunk counter of the current stage / pass
-  unsigned long long arcs_acc;  // emitting arcs expanded over the chunk (diagnostics)
-  uint32_t bhist[CTW_NB];
-  uint32_t hist[256];
-  int sel_bin;     // boundary bin (CTW_NB = no select)
-  int sel_bcount;  // members of the boundary bin
+  // ---- cluster fields: meaningful in rank 0 only, reached through DSMEM ----
+  FrameCtr fc[2];
+  int pw[2];            // epsilon pass chunk counters (pass parity)
+  int pool_used;        // olabel pool fill
+  int sel_bin, sel_need, sel_bcount, sel_radix;
   unsigned long long thr_key;  // survivor iff bin < sel_bin or (bin == sel_bin and (key, state) <= thr)
   uint32_t thr_state;
-  int sel_radix;   // boundary bin overflowed CTW_BBUF: digit-wise radix select over all slots
-  unsigned long long min_key;
   unsigned long long sel_hi;  // radix-select prefix (cost-key digits)
   uint32_t sel_lo;            // radix-select prefix (state digits)
   int sel_depth;              // digits fixed; survivor iff top digits <= prefix
-  int sel_need;
+  int rneed;
   int sel_done;
-  int n_slots;
-  int n_next;
-  int n_tiny;
-  int any_big;
+  uint32_t rhist[2][256];     // radix digit histogram (digit parity)
+  // ---- per-rank fields ----
+  int status_l;         // sticky local status (grow requests, walk failures)
+  int st_pub[2];        // status published at a barrier (barrier parity)
+  unsigned long long min_pub[2];  // running minimum published at a barrier (barrier parity)
+  unsigned long long mydiag[CTW_NPROF + 1];  // this rank's diagnostics, read by rank 0 at the end
+  int epoch;            // barriers passed (all ranks pass the same sequence)
+  int st_all;           // max status over the ranks at the last barrier
+  int n_slots;          // slots this rank created in the frame
+  int snap_slots;       // n_slots at the start of the epsilon stage
+  int pc_next[2], pc_tiny[2], pc_big[2];  // frontier pushes of this rank (pass parity)
+  int n_seg, n_cur, any_big;
+  int seg_pref[2 * CTW_RMAX + 1];  // input segments of the current epsilon pass
+  uint2* seg_ptr[2 * CTW_RMAX];
+  int work;             // this rank's chunk counter (rank-local sweeps)
+  unsigned long long min_key;  // running minimum seen by this rank (>= the cluster's)
+  uint32_t hist[256];          // local digit histogram (radix select)
+  uint32_t lbhist[CTW_NB];     // local cost histogram
+  int n_all;            // slots of all ranks (after the closure)
+  int svoff;            // this rank's offset in the gathered value array
+  int cnt_l, mpd_l, cnt_all, mpd_all;
+  int nbig;
+  int rbase;            // first survivor index of this rank in the frame
+  int tot_surv;
   int passes;
-  int eps_items;
-  int eps_arcs;
-  int eps_ties;
-  int eps_disc;
-  int status;
-  int cnt;
-  int max_pd;
-  int pool_used;
-  int hop_fail;
+  int eps_items, eps_arcs, eps_ties, eps_disc;
+  int arcs_f;           // emitting arcs expanded in the frame (diagnostics)
+  // local copies of the select result
+  int l_bin, l_need, l_bcount, l_radix, l_depth;
+  unsigned long long l_tk, l_ph;
+  uint32_t l_ts, l_pl;
 };
 
-// Append a newly inserted table index to the slot list (always, so the table
-// can be reset even on overflow); request a bigger table past half load.
+// Append a newly inserted table index to this rank's slot segment; request a
+// bigger table when the segment is full (the table is grown before half load).
 __device__ __forceinline__ void slot_append(Smem& sm, const LaneCtx& L, uint32_t h, uint32_t state) {
   const int s = atomicAdd(&sm.n_slots, 1);
-  if ((uint32_t)s < L.tcap) L.slots[s] = make_uint2(h, state);
-  if ((uint32_t)s >= (L.tcap >> 1)) atomicMax(&sm.status, CTW_GROW_TABLE);
+  if ((uint32_t)s < L.seg) L.slots[s] = make_uint2(h, state);
+  else atomicMax(&sm.status_l, CTW_GROW_TABLE);
 }
 
 __device__ __forceinline__ void track_min(Smem& sm, unsigned long long k) {
@@ -287,59 +360,125 @@ __device__ __forceinline__ void track_min(Smem& sm, unsigned long long k) {
 }
 
 // Running beam cutoff: the frame minimum only decreases, so a cost above
-// (running min + beam) is above the final cutoff too.
+// (running min + beam) is above the final cutoff too. Each rank uses its own
+// running minimum (never below the cluster's), which is looser, hence exact.
 __device__ __forceinline__ double running_cut(const Smem& sm, double beam) {
   return __dadd_rn(key2d(*((volatile const unsigned long long*)&sm.min_key)), beam);
 }
 
+// Cluster barrier with a status vote and a minimum exchange: every rank
+// publishes its sticky local status and its running minimum in its own
+// shared memory, passes the barrier and reads everyone's, so all ranks take
+// the same branch and leave with the same (cluster-wide) running minimum.
+// Published values are double-buffered by barrier parity (a rank rewrites a
+// slot only after every rank has passed the barrier that follows the reads
+// of it). Plain stores + remote loads: shared memory has no native 64-bit
+// min, and a generic 64-bit atomic min on a DSMEM address is not atomic.
+__device__ __forceinline__ int csync(Smem& sm) {
+  cg::cluster_group cl = cg::this_cluster();
+  __syncthreads();
+  const int e = sm.epoch;
+  if (threadIdx.x == 0) {
+    sm.st_pub[e & 1] = *((volatile int*)&sm.status_l);
+    sm.min_pub[e & 1] = *((volatile unsigned long long*)&sm.min_key);
+  }
+  cl.sync();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    unsigned long long m = sm.min_key;
+    for (int k = 0; k < (int)cl.num_blocks(); ++k) {
+      const Smem* o = cl.map_shared_rank(&sm, k);
+      s = max(s, o->st_pub[e & 1]);
+      const unsigned long long mk = o->min_pub[e & 1];
+      if (mk < m) m = mk;
+    }
+    sm.st_all = s;
+    sm.min_key = m;
+    sm.epoch = e + 1;
+  }
+  __syncthreads();
+  return sm.st_all;
+}
+
 // ------------------------------------------------------- epsilon fixpoint --
 
-// Label-correcting fixpoint over epsilon arcs, frontier by frontier;
-// frontier 0 = every slot in [0, n_slots). A slot is re-queued when it is new,
-// improved by more than relax_eps, or changed winner at equal cost (its
-// Gauss-Seidel event time moved). Improvements <= relax_eps are propagated
-// only if the pass goes on anyway, mirroring the Gauss-Seidel stop rule
-// (_kernel.pyx:331, :346, :351). With L.prune, a predecessor whose cost is
-// above the running cutoff (or that has no value yet) only *discovers* its
-// successors -- slot positions stay exact -- without relaxing their costs:
-// with non-negative epsilon increments nothing it reaches can enter the
-// beam. Returns CTW_OK or CTW_ERR_EPS_ITERS (divergence: more passes than a
-// convergent closure needs).
-__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2* front, const double* boost,
+// Label-correcting fixpoint over epsilon arcs, frontier by frontier; the
+// input of pass 1 is every slot created so far (all ranks' segments). A slot
+// is re-queued when it is new, improved by more than relax_eps, or changed
+// winner at equal cost (its Gauss-Seidel event time moved). Improvements <=
+// relax_eps are propagated only if the pass goes on anyway, mirroring the
+// Gauss-Seidel stop rule (_kernel.pyx:331, :346, :351). With L.prune, a
+// predecessor whose cost is above the running cutoff (or that has no value
+// yet) only *discovers* its successors -- slot positions stay exact --
+// without relaxing their costs: with non-negative epsilon increments nothing
+// it reaches can enter the beam. Work of a pass is handed out cluster-wide in
+// 32-item chunks over the virtual concatenation of the ranks' input segments;
+// every rank pushes to its own output segments. Returns CTW_OK or
+// CTW_ERR_EPS_ITERS (divergence: more passes than a convergent closure needs).
+__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, FrameCtr* fc, const double* boost,
                             double relax_eps, double beam, long long pass_cap) {
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
-  const uint2* cur = L.slots;
-  int n_cur = sm.n_slots;
+  const int R = L.nranks, rank = L.rank;
+  Smem* G = L.G;
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
-  // three buffers rotate: cur (being read), nxt (big changes), tiny (small)
-  uint2* bufs[3] = {front, front + L.tcap, front + 2 * (size_t)L.tcap};
-  int ci = 2;  // index of cur's buffer (pass 1 reads the slot list itself)
   for (long long pass = 1;; ++pass) {
-    if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
+    const int q = (int)(pass & 1);
+    const int so = 2 * (int)((pass - 1) & 1);  // output sets of this pass
+    uint2* nxt = L.front + ((size_t)so * CTW_RMAX + rank) * L.seg;
+    uint2* tiny = L.front + ((size_t)(so + 1) * CTW_RMAX + rank) * L.seg;
     if (tid == 0) {
-      sm.work = 0;
-      sm.eps_items += n_cur;
+      int tot = 0, ns = 0;
+      if (pass == 1) {
+        for (int k = 0; k < R; ++k) {
+          const Smem* o = cl.map_shared_rank(&sm, k);
+          sm.seg_pref[ns] = tot;
+          sm.seg_ptr[ns++] = L.slots_base + (size_t)k * L.seg;
+          tot += min(o->snap_slots, (int)L.seg);
+        }
+      } else {
+        const int qp = q ^ 1;
+        const int si = 2 * (int)((pass - 2) & 1);
+        for (int k = 0; k < R; ++k) {
+          const Smem* o = cl.map_shared_rank(&sm, k);
+          const int nn = min(o->pc_next[qp], (int)L.seg), nt = min(o->pc_tiny[qp], (int)L.seg);
+          sm.seg_pref[ns] = tot;
+          sm.seg_ptr[ns++] = L.front + ((size_t)si * CTW_RMAX + k) * L.seg;
+          tot += nn;
+          sm.seg_pref[ns] = tot;
+          sm.seg_ptr[ns++] = L.front + ((size_t)(si + 1) * CTW_RMAX + k) * L.seg;
+          tot += nt;
+        }
+      }
+      sm.seg_pref[ns] = tot;
+      sm.n_seg = ns;
+      sm.n_cur = tot;
+      sm.pc_next[q] = 0;
+      sm.pc_tiny[q] = 0;
+      sm.pc_big[q] = 0;
+      if (rank == 0) sm.pw[q ^ 1] = 0;  // the next pass's chunk counter
       sm.passes = (int)pass;
-      sm.n_next = 0;
-      sm.n_tiny = 0;
-      sm.any_big = 0;
     }
     __syncthreads();
+    if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
+    const int n_cur = sm.n_cur, n_seg = sm.n_seg;
     const uint32_t epoch = (uint32_t)pass;
-    uint2* nxt = bufs[(ci + 1) % 3];
-    uint2* tiny = bufs[(ci + 2) % 3];
-    // warps grab 32 frontier items at a time (no block barriers inside a
-    // pass) and spread the items' epsilon arcs over their lanes
+    // warps grab 32 frontier items at a time and spread the items' epsilon
+    // arcs over their lanes
     const int lane = tid & 31, w = tid >> 5;
     for (;;) {
       int base = 0;
-      if (lane == 0) base = atomicAdd(&sm.work, 32);
+      if (lane == 0) base = atomicAdd(&G->pw[q], 32);
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
       if (base >= n_cur) break;
       const int nv = min(32, n_cur - base);
+      if (lane == 0) atomicAdd(&sm.eps_items, nv);
       int deg = 0;
       if (lane < nv) {
-        const uint2 it = cur[base + lane];
+        const int i = base + lane;
+        int s = 0;
+        while (s + 1 < n_seg && sm.seg_pref[s + 1] <= i) ++s;
+        const uint2 it = sm.seg_ptr[s][i - sm.seg_pref[s]];
         const CtwStateRange r = g.ranges[it.y];
         deg = (int)(r.emit_beg - r.eps_beg);
         if (deg > 0) {
@@ -406,7 +545,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
         ulonglong2 seen;
         const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
         if (d == CTW_EMPTY) {
-          atomicMax(&sm.status, CTW_GROW_TABLE);
+          atomicMax(&sm.status_l, CTW_GROW_TABLE);
           continue;
         }
         if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
@@ -428,7 +567,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
           push = big = is_new;  // discovery only: successors are discovered next pass
         }
         if (!push) continue;
-        if (big) sm.any_big = 1;
+        if (big) sm.pc_big[q] = 1;
         bool first;
         if (is_new) {  // this thread created the slot: first to touch its stamp
           ed->stamp = epoch;
@@ -438,31 +577,29 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, uint2
         }
         if (first) {
           if (big) {
-            const int p = atomicAdd(&sm.n_next, 1);
-            if ((uint32_t)p < L.tcap) nxt[p] = item;
+            const int p = atomicAdd(&sm.pc_next[q], 1);
+            if ((uint32_t)p < L.seg) nxt[p] = item;
+            else atomicMax(&sm.status_l, CTW_GROW_TABLE);
           } else {
-            const int p = atomicAdd(&sm.n_tiny, 1);
-            if ((uint32_t)p < L.tcap) tiny[p] = item;
+            const int p = atomicAdd(&sm.pc_tiny[q], 1);
+            if ((uint32_t)p < L.seg) tiny[p] = item;
+            else atomicMax(&sm.status_l, CTW_GROW_TABLE);
           }
         }
       }
       __syncwarp();
     }
-    __syncthreads();
-    if (sm.status >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
-    int n_next = min((uint32_t)sm.n_next, L.tcap);
-    if (!sm.any_big) return CTW_OK;  // a quiet pass (only <= relax_eps changes) ends the closure
-    // the pass continues: parked small improvements ride along (Gauss-Seidel
-    // re-visits every slot in the next pass)
-    const int n_tiny = min((uint32_t)sm.n_tiny, L.tcap);
-    if (n_tiny > 0) {
-      for (int i = tid; i < n_tiny && n_next + i < (int)L.tcap; i += CTW_BS) nxt[n_next + i] = tiny[i];
-      n_next = min((uint32_t)(n_next + n_tiny), L.tcap);
+    // the barrier ending the pass (also merges the ranks' running minima)
+    if (csync(sm) >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
+    if (tid == 0) {
+      int any = 0;
+      for (int k = 0; k < R; ++k) any |= cl.map_shared_rank(&sm, k)->pc_big[q];
+      sm.any_big = any;
     }
-    cur = nxt;
-    n_cur = n_next;
-    ci = (ci + 1) % 3;
     __syncthreads();
+    // a quiet pass (only <= relax_eps changes) ends the closure; otherwise the
+    // parked small improvements ride along in the next pass
+    if (!sm.any_big) return CTW_OK;
   }
 }
 
@@ -519,9 +656,9 @@ __device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, ui
   const int n = np + w.n;
   if (n == 0) return 0;
   if (n == 1) return np ? w.pend : w.last;
-  const int off = atomicAdd(&sm.pool_used, n + 1);
+  const int off = atomicAdd(&L.G->pool_used, n + 1);  // cluster-wide pool fill (rank 0)
   if (off + n + 1 > L.pool_cap) {
-    atomicMax(&sm.status, CTW_GROW_POOL);
+    atomicMax(&sm.status_l, CTW_GROW_POOL);
     return 0;
   }
   int32_t* seg = L.pool + off;
@@ -564,37 +701,53 @@ __device__ __forceinline__ int cmp_prefix(unsigned long long key, uint32_t state
 
 // Exact top-k by (cost, state) among in-beam slots: MSD radix select over the
 // 96-bit (sortable cost, state) key, 8 bits per pass, stopping as soon as the
-// prefix bucket is taken whole. Leaves (sel_hi, sel_lo, sel_depth).
-__device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned long long cut_key, long long k) {
+// prefix bucket is taken whole. Every rank histograms its own slots into rank
+// 0's digit histogram; rank 0 fixes the digit. Leaves (l_ph, l_pl, l_depth)
+// in every rank.
+__device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, int n_own, unsigned long long cut_key,
+                             long long k) {
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    sm.sel_hi = 0;
-    sm.sel_lo = 0;
-    sm.sel_depth = 0;
-    sm.sel_need = (int)k;
-    sm.sel_done = 0;
+  Smem* G = L.G;
+  if (L.rank == 0) {
+    if (tid == 0) {
+      sm.sel_hi = 0;
+      sm.sel_lo = 0;
+      sm.sel_depth = 0;
+      sm.rneed = (int)k;
+      sm.sel_done = 0;
+    }
+    for (int i = tid; i < 256; i += CTW_BS) sm.rhist[0][i] = 0;
   }
-  __syncthreads();
+  cl.sync();
   for (int d = 0; d < 12; ++d) {
+    if (tid == 0) {
+      sm.l_ph = *((volatile unsigned long long*)&G->sel_hi);
+      sm.l_pl = *((volatile uint32_t*)&G->sel_lo);
+    }
     for (int i = tid; i < 256; i += CTW_BS) sm.hist[i] = 0;
     __syncthreads();
-    const unsigned long long ph = sm.sel_hi;
-    const uint32_t pl = sm.sel_lo;
-    for (int i = tid; i < n_slots; i += CTW_BS) {
-      const uint2 it = L.slots[i];
-      const unsigned long long key = __ldcg(&L.T[it.x].key);
+    const unsigned long long ph = sm.l_ph;
+    const uint32_t pl = sm.l_pl;
+    for (int i = tid; i < n_own; i += CTW_BS) {
+      const unsigned long long key = sv[i].x;
       if (key > cut_key) continue;
-      const uint32_t st = it.y;
+      const uint32_t st = L.slots[i].y;
       if (cmp_prefix(key, st, d, ph, pl) != 0) continue;
       atomicAdd(&sm.hist[digit_of(key, st, d)], 1u);
     }
     __syncthreads();
-    if (tid < 32) {
-      // warp 0: locate the bucket holding the need-th smallest
+    for (int i = tid; i < 256; i += CTW_BS)
+      if (sm.hist[i]) atomicAdd(&G->rhist[d & 1][i], sm.hist[i]);
+    if (L.rank == 0)
+      for (int i = tid; i < 256; i += CTW_BS) sm.rhist[(d + 1) & 1][i] = 0;
+    cl.sync();
+    if (L.rank == 0 && tid < 32) {
+      // warp 0 of rank 0: locate the bucket holding the need-th smallest
       uint32_t c[8];
       uint32_t sum = 0;
       for (int j = 0; j < 8; ++j) {
-        c[j] = sm.hist[tid * 8 + j];
+        c[j] = sm.rhist[d & 1][tid * 8 + j];
         sum += c[j];
       }
       uint32_t incl = sum;
@@ -603,7 +756,7 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned l
         if (tid >= o) incl += t;
       }
       const uint32_t excl = incl - sum;
-      const uint32_t need = (uint32_t)sm.sel_need;
+      const uint32_t need = (uint32_t)sm.rneed;
       if (excl < need && need <= incl) {
         uint32_t run = excl;
         int b = 0;
@@ -618,13 +771,21 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, int n_slots, unsigned l
         if (d < 8) sm.sel_hi = (sm.sel_hi << 8) | (unsigned long long)b;
         else sm.sel_lo = (sm.sel_lo << 8) | (uint32_t)b;
         sm.sel_depth = d + 1;
-        sm.sel_need = (int)rem;
-        if (sm.hist[b] == rem) sm.sel_done = 1;
+        sm.rneed = (int)rem;
+        if (sm.rhist[d & 1][b] == rem) sm.sel_done = 1;
       }
     }
+    cl.sync();
+    if (tid == 0) sm.l_depth = *((volatile int*)&G->sel_done);
     __syncthreads();
-    if (sm.sel_done) break;
+    if (sm.l_depth) break;
   }
+  if (tid == 0) {
+    sm.l_ph = *((volatile unsigned long long*)&G->sel_hi);
+    sm.l_pl = *((volatile uint32_t*)&G->sel_lo);
+    sm.l_depth = *((volatile int*)&G->sel_depth);
+  }
+  __syncthreads();
 }
 
 // --------------------------------------------------------- frame kernel ---
@@ -639,13 +800,19 @@ struct ChunkArgs {
   CtwDecodeCfg cfg;
 };
 
-__device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane) {
+__device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int nranks, Smem* G) {
   LaneCtx L;
   L.T = lane.table;
   L.tcap = 1u << lane.tlog2;
   L.mask = L.tcap - 1;
   L.shift = 32 - lane.tlog2;
-  L.slots = lane.slots;
+  L.seg = L.tcap >> 1;
+  L.slots_base = lane.slots;
+  L.slots = lane.slots + (size_t)rank * L.seg;
+  L.front = lane.front;
+  L.G = G;
+  L.rank = rank;
+  L.nranks = nranks;
   L.pool = lane.pool;
   L.pool_cap = lane.pcap;
   L.prune = lane.prune_ok != 0;
@@ -667,40 +834,46 @@ __device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost,
 
 #define CTW_UNR 4  // independent table loads in flight per thread in slot sweeps
 
-// One sweep over the frame's slots: gathers every slot's final (key, tb|aux)
-// into the compact array sv (coalesced for the later sweeps; CTW_UNR table
-// loads in flight per thread), and computes the Gauss-Seidel pass count of
-// the closure (= 1 + last pass that changed a slot, i.e. max pd over
-// epsilon-won slots; > max_ne_iters -> CTW_ERR_EPS_ITERS), the in-beam count
-// and (hist) the cost histogram over [min, min + beam] for the max-active select.
-__device__ int count_pass(Smem& sm, const LaneCtx& L, ulonglong2* sv, int n_slots, long long max_ne_iters,
+// One sweep over this rank's slots: gathers every slot's final (key, tb|aux)
+// into sv (this rank's part of the compact value array; coalesced for the
+// later sweeps, CTW_UNR table loads in flight per thread), and computes the
+// Gauss-Seidel pass count of the closure (= 1 + last pass that changed a
+// slot, i.e. max pd over epsilon-won slots; > max_ne_iters ->
+// CTW_ERR_EPS_ITERS), the in-beam count and (hist) the cost histogram over
+// [min, min + beam] for the max-active select; merges them into the frame
+// counters and meets the other ranks at a barrier.
+__device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* sv, int n_own, long long max_ne_iters,
                           unsigned long long cut_key, double min_cost, double bin_scale, bool hist) {
   const int tid = threadIdx.x;
   if (hist)
-    for (int i = tid; i < CTW_NB; i += CTW_BS) sm.bhist[i] = 0;
+    for (int i = tid; i < CTW_NB; i += CTW_BS) sm.lbhist[i] = 0;
+  if (tid == 0) {
+    sm.cnt_l = 0;
+    sm.mpd_l = 0;
+  }
   __syncthreads();
   int c = 0, mpd = 0;
-  for (int i0 = tid; i0 < n_slots; i0 += CTW_UNR * CTW_BS) {
+  for (int i0 = tid; i0 < n_own; i0 += CTW_UNR * CTW_BS) {
     uint32_t h[CTW_UNR];
     ulonglong2 v[CTW_UNR];
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * CTW_BS;
-      h[u] = i < n_slots ? L.slots[i].x : 0u;
+      h[u] = i < n_own ? L.slots[i].x : 0u;
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * CTW_BS;
-      if (i < n_slots) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u]]));
+      if (i < n_own) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u]]));
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * CTW_BS;
-      if (i >= n_slots) break;
+      if (i >= n_own) break;
       sv[i] = v[u];
       if (v[u].x <= cut_key) {
         ++c;
-        if (hist) atomicAdd(&sm.bhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
+        if (hist) atomicAdd(&sm.lbhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
       }
       if ((uint32_t)v[u].y & CTW_EPS_BIT) mpd = max(mpd, (int)((uint32_t)(v[u].y >> 32) >> CTW_PRED_BITS));
     }
@@ -710,21 +883,36 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, ulonglong2* sv, int n_slot
     mpd = max(mpd, __shfl_xor_sync(0xFFFFFFFFu, mpd, o));
   }
   if ((tid & 31) == 0) {
-    atomicAdd(&sm.cnt, c);
-    atomicMax(&sm.max_pd, mpd);
+    atomicAdd(&sm.cnt_l, c);
+    atomicMax(&sm.mpd_l, mpd);
   }
   __syncthreads();
-  return (1 + (long long)sm.max_pd > max_ne_iters) ? CTW_ERR_EPS_ITERS : CTW_OK;
+  if (hist)
+    for (int i = tid; i < CTW_NB; i += CTW_BS) {
+      const uint32_t n = sm.lbhist[i];
+      if (n) atomicAdd(&fc->bhist[i], n);
+    }
+  if (tid == 0) {
+    atomicAdd(&fc->cnt, sm.cnt_l);
+    atomicMax(&fc->max_pd, sm.mpd_l);
+  }
+  csync(sm);
+  if (tid == 0) {
+    sm.cnt_all = *((volatile int*)&fc->cnt);
+    sm.mpd_all = *((volatile int*)&fc->max_pd);
+  }
+  __syncthreads();
+  return (1 + (long long)sm.mpd_all > max_ne_iters) ? CTW_ERR_EPS_ITERS : CTW_OK;
 }
 
-// Reset every touched table entry; slot loads batched ahead of the stores.
-__device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_slots) {
-  for (int i0 = threadIdx.x; i0 < n_slots; i0 += CTW_UNR * CTW_BS) {
+// Reset every table entry this rank created; slot loads batched ahead of the stores.
+__device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_own) {
+  for (int i0 = threadIdx.x; i0 < n_own; i0 += CTW_UNR * CTW_BS) {
     uint32_t h[CTW_UNR];
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * CTW_BS;
-      h[u] = i < n_slots ? L.slots[i].x : CTW_EMPTY;
+      h[u] = i < n_own ? L.slots[i].x : CTW_EMPTY;
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u)
@@ -733,18 +921,22 @@ __device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_slots) {
 }
 
 // Exact max-active threshold by (cost, state) (decoder.py:361-374,
-// _kernel.pyx:385-390): the histogram locates the boundary bin; its members
-// are sorted exactly in shared memory (bitonic). Falls back to the
-// digit-wise radix select when the boundary bin overflows CTW_BBUF.
-__device__ void select_threshold(Smem& sm, const LaneCtx& L, const ulonglong2* sv, int n_slots,
+// _kernel.pyx:385-390): rank 0 locates the boundary bin in the merged
+// histogram; every rank hands its boundary-bin members to rank 0, which sorts
+// them exactly in shared memory (bitonic). Falls back to the cluster-wide
+// digit-wise radix select when the boundary bin overflows CTW_BBUF. Leaves
+// the threshold in every rank's l_* fields.
+__device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const ulonglong2* sv, int n_own,
                                  unsigned long long cut_key, double min_cost, double bin_scale, long long k) {
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
-  if (tid < 32) {
+  Smem* G = L.G;
+  if (L.rank == 0 && tid < 32) {
     uint32_t cnt[CTW_NB / 32];
     uint32_t sum = 0;
 #pragma unroll
     for (int j = 0; j < CTW_NB / 32; ++j) {
-      cnt[j] = sm.bhist[tid * (CTW_NB / 32) + j];
+      cnt[j] = fc->bhist[tid * (CTW_NB / 32) + j];
       sum += cnt[j];
     }
     uint32_t incl = sum;
@@ -767,69 +959,128 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, const ulonglong2* s
       }
     }
     if (tid == 0) {
-      sm.sel_radix = 0;
       sm.thr_key = ~0ULL;
       sm.thr_state = 0xFFFFFFFFu;
-      sm.n_next = 0;
     }
   }
+  cl.sync();
+  if (tid == 0) {
+    sm.l_bin = *((volatile int*)&G->sel_bin);
+    sm.l_need = *((volatile int*)&G->sel_need);
+    sm.l_bcount = *((volatile int*)&G->sel_bcount);
+    sm.l_radix = 0;
+    sm.l_tk = ~0ULL;
+    sm.l_ts = 0xFFFFFFFFu;
+  }
   __syncthreads();
-  const int bsel = sm.sel_bin, need = sm.sel_need, bcount = sm.sel_bcount;
+  const int bsel = sm.l_bin, need = sm.l_need, bcount = sm.l_bcount;
+  // (rank 0 rewrites the select fields only in a later frame, after several
+  // barriers: every rank has copied them by then)
   if (bcount == need) return;  // the whole boundary bin survives
   if (bcount > CTW_BBUF) {
-    if (tid == 0) sm.sel_radix = 1;
-    radix_select(sm, L, n_slots, cut_key, k);
+    if (tid == 0) sm.l_radix = 1;
+    radix_select(sm, L, sv, n_own, cut_key, k);
     return;
   }
-  for (int i = tid; i < n_slots; i += CTW_BS) {
+  for (int i = tid; i < n_own; i += CTW_BS) {
     const unsigned long long key = sv[i].x;
     if (key <= cut_key && cost_bin(key, min_cost, bin_scale) == bsel) {
-      const int p = atomicAdd(&sm.n_next, 1);
-      sm.bbuf[p] = make_ulonglong2(key, L.slots[i].y);
+      const int p = atomicAdd(&fc->nbb, 1);
+      G->bbuf[p] = make_ulonglong2(key, L.slots[i].y);
     }
   }
-  __syncthreads();
-  int n2 = 1;
-  while (n2 < bcount) n2 <<= 1;
-  for (int i = bcount + tid; i < n2; i += CTW_BS) sm.bbuf[i] = make_ulonglong2(~0ULL, ~0ULL);
-  __syncthreads();
-  for (int kk = 2; kk <= n2; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < n2; i += CTW_BS) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const ulonglong2 x = sm.bbuf[i], y = sm.bbuf[ixj];
-          const bool gt = x.x > y.x || (x.x == y.x && x.y > y.y);
-          if (gt == ((i & kk) == 0)) {
-            sm.bbuf[i] = y;
-            sm.bbuf[ixj] = x;
+  cl.sync();
+  if (L.rank == 0) {
+    int n2 = 1;
+    while (n2 < bcount) n2 <<= 1;
+    for (int i = bcount + tid; i < n2; i += CTW_BS) sm.bbuf[i] = make_ulonglong2(~0ULL, ~0ULL);
+    __syncthreads();
+    for (int kk = 2; kk <= n2; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < n2; i += CTW_BS) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const ulonglong2 x = sm.bbuf[i], y = sm.bbuf[ixj];
+            const bool gt = x.x > y.x || (x.x == y.x && x.y > y.y);
+            if (gt == ((i & kk) == 0)) {
+              sm.bbuf[i] = y;
+              sm.bbuf[ixj] = x;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
+    }
+    if (tid == 0) {
+      sm.thr_key = sm.bbuf[need - 1].x;
+      sm.thr_state = (uint32_t)sm.bbuf[need - 1].y;
     }
   }
+  cl.sync();
   if (tid == 0) {
-    sm.thr_key = sm.bbuf[need - 1].x;
-    sm.thr_state = (uint32_t)sm.bbuf[need - 1].y;
+    sm.l_tk = *((volatile unsigned long long*)&G->thr_key);
+    sm.l_ts = *((volatile uint32_t*)&G->thr_state);
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
+// Relax one emitting arc: ((c + (-scale * ll)) + w) (+ boost), then
+// find-or-insert the destination and install the candidate if it wins
+// (_kernel.pyx:243-287).
+__device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
+                                         const double* nll_s, bool smem_ll, long long row0, double neg_scale,
+                                         const double* boost, uint32_t arc_i, double cost, uint32_t src_idx) {
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const CtwArc arc = g.arcs[arc_i];
+  double ac;
+  if (smem_ll) ac = nll_s[arc.ilabel - 1];
+  else {
+    const long long idx = row0 + arc.ilabel - 1;
+    const double x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+    ac = __dmul_rn(neg_scale, x);
+  }
+  double nc = __dadd_rn(__dadd_rn(cost, ac), arc.weight);
+  if (boost) {
+    const int32_t ol = g.olabel[arc_i];
+    if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+  }
+  if (!(nc < INF)) return;
+  bool is_new = false;
+  ulonglong2 seen;
+  const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
+  if (d == CTW_EMPTY) {
+    atomicMax(&sm.status_l, CTW_GROW_TABLE);
+    return;
+  }
+  if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
+  CtwTok* ed = &L.T[d];
+  // Gauss-Seidel slot position of an emitting-reached state = its
+  // first-arrival arc (_kernel.pyx:256-272)
+  gpos_min(ed, (unsigned long long)arc_i);
+  if (L.prune && nc > running_cut(sm, a.cfg.beam)) return;  // cannot make the final beam
+  unsigned long long oldk;
+  const unsigned long long nk = d2key(nc);
+  if (tok_relax_from(L, ed, nk, arc_i, src_idx, 0ULL, seen, &oldk)) track_min(sm, nk);
+}
+
+__global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
   extern __shared__ double nll_s[];
   __shared__ Smem sm;
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
-  const int b = blockIdx.x;
+  const int R = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int b = blockIdx.x / R;
+  Smem* G = cl.map_shared_rank(&sm, 0);
   CtwLane& lane = lanes[a.lane_ids[b]];
-  LaneCtx L = lane_ctx(lane);
+  LaneCtx L = lane_ctx(lane, rank, R, G);
   L.tie_ctr = &sm.eps_ties;
   const int F = a.nframes[b];
   const double* boost = lane.boost;
   const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
   const double neg_scale = -a.cfg.acoustic_scale;
-  const double INF = __longlong_as_double(0x7FF0000000000000LL);
   const long long pass_cap = divergence_cap(a.cfg.max_ne_iters, L.tcap);
+  BigSrc* bigl = reinterpret_cast<BigSrc*>(L.front + (size_t)3 * CTW_RMAX * L.seg);  // set 3: free until pass 2
+  const int big_cap = (int)min((size_t)CTW_NBIG, ((size_t)CTW_RMAX * L.seg * sizeof(uint2)) / sizeof(BigSrc));
 
   int n_src = lane.n_src;
   int cur_buf = lane.src_buf;
@@ -843,29 +1094,38 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
   long long src_total = 0, rec_need = 0;
   long long prof[CTW_NPROF] = {0};
   if (tid == 0) {
-    sm.status = CTW_OK;
-    sm.pool_used = lane.pool_used;
-    sm.arcs_acc = 0;
+    sm.status_l = CTW_OK;
+    sm.epoch = 0;
+    sm.st_pub[0] = sm.st_pub[1] = 0;
+    sm.st_all = 0;
+    sm.min_pub[0] = sm.min_pub[1] = ~0ULL;
+    if (rank == 0) {
+      sm.pool_used = lane.pool_used;
+      sm.pw[0] = sm.pw[1] = 0;
+    }
   }
-  __syncthreads();
+  if (rank == 0) {
+    int* z = reinterpret_cast<int*>(&sm.fc[0]);
+    for (int i = tid; i < (int)(2 * sizeof(FrameCtr) / sizeof(int)); i += CTW_BS) z[i] = 0;
+  }
+  cl.sync();
 
   for (int f = 0; f < F; ++f) {
     long long tclk = clock64();
+    FrameCtr* fc = &G->fc[f & 1];
     const CtwSrc* src = lane.src[cur_buf];
     const int32_t* pend = pend_valid ? lane.pend : nullptr;
     const int nxt_buf = (f & 1) ? w1 : w0;
     CtwSrc* nsrc = lane.src[nxt_buf];
     if (tid == 0) {
-      sm.work = 0;
+      sm.n_slots = 0;
+      sm.min_key = ~0ULL;
       sm.eps_items = 0;
       sm.eps_arcs = 0;
       sm.eps_ties = 0;
       sm.eps_disc = 0;
-      sm.n_slots = 0;
-      sm.min_key = ~0ULL;
-      sm.cnt = 0;
-      sm.max_pd = 0;
-      sm.hop_fail = 0;
+      sm.passes = 0;
+      sm.arcs_f = 0;
     }
     // frame row -> -scale * ll (the reference's (-acoustic_scale * ll) term)
     const long long row0 = a.ll_off[b] + (long long)f * a.width;
@@ -875,131 +1135,193 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
         nll_s[v] = __dmul_rn(neg_scale, x);
       }
     }
-    __syncthreads();
+    csync(sm);  // (A) the previous frame (sources, table reset) is complete in every rank
+    if (rank == 0) {
+      // the other parity's counters: last read before this barrier, next used after the next frame's
+      FrameCtr* nf = &sm.fc[(f + 1) & 1];
+      int* z = reinterpret_cast<int*>(nf);
+      for (int i = tid; i < (int)(sizeof(FrameCtr) / sizeof(int)); i += CTW_BS) z[i] = 0;
+      if (tid == 0) sm.pw[0] = sm.pw[1] = 0;
+    }
     src_total += n_src;
 
     // ---- emitting expansion, load-balanced over out-degree ----
-    {
+    const int lane_ = tid & 31, w = tid >> 5;
+    for (;;) {
       // warps grab 32 sources at a time and spread their emitting arcs over
-      // the lanes (warp scan of out-degrees; no block barriers)
-      const int lane = tid & 31, w = tid >> 5;
+      // the lanes (warp scan of out-degrees); sources with more than
+      // CTW_BIG arcs go to the arc-parallel list instead
+      int base = 0;
+      if (lane_ == 0) base = atomicAdd(&fc->work_e, 32);
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (base >= n_src) break;
+      const int nv = min(32, n_src - base);
+      int deg = 0;
+      if (lane_ < nv) {
+        const CtwSrc t = src[base + lane_];
+        const CtwStateRange r = g.ranges[t.state];
+        deg = (int)(r.emit_end - r.emit_beg);
+        if (deg > CTW_BIG) {
+          const int j = atomicAdd(&fc->nbig, 1);
+          if (j < big_cap) {
+            BigSrc bs;
+            bs.idx = base + lane_;
+            bs.beg = r.emit_beg;
+            bs.deg = deg;
+            bs.pad = 0;
+            bs.cost = t.cost;
+            bigl[j] = bs;
+            deg = 0;
+          }
+        }
+        sm.em.beg[w][lane_] = r.emit_beg;
+        sm.em.cost[w][lane_] = t.cost;
+      }
+      int incl = deg;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane_ >= o) incl += t;
+      }
+      sm.em.off[w][lane_] = incl - deg;
+      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (lane_ == 0) atomicAdd(&sm.arcs_f, total);
+      __syncwarp();
+      for (int k = lane_; k < total; k += 32) {
+        int lo = 0, hi = nv - 1;  // last source with off <= k
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.em.off[w][mid] <= k) lo = mid;
+          else hi = mid - 1;
+        }
+        emit_arc(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
+                 sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]), sm.em.cost[w][lo], (uint32_t)(base + lo));
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    if (tid == 0) sm.snap_slots = sm.n_slots;
+    csync(sm);  // (B)
+    if (tid == 0) sm.nbig = min(*((volatile int*)&fc->nbig), big_cap);
+    __syncthreads();
+    if (sm.nbig > 0 && sm.st_all < CTW_GROW_TABLE) {
+      // arc-parallel expansion of the high out-degree sources: 32-arc chunks
+      // over the degree prefix of the list
+      const int nb = sm.nbig;
+      for (int j0 = 0; j0 < nb; j0 += CTW_BS) {
+        const int j = j0 + tid;
+        int d = 0;
+        if (j < nb) {
+          const BigSrc bs = bigl[j];
+          d = bs.deg;
+          sm.bg.beg[j] = bs.beg;
+          sm.bg.idx[j] = bs.idx;
+          sm.bg.cost[j] = bs.cost;
+        }
+        const int carry = j0 == 0 ? 0 : sm.bg.pref[j0];
+        int ex, tt;
+        Smem::Scan(sm.scan).ExclusiveSum(d, ex, tt);
+        if (j < nb) sm.bg.pref[j] = carry + ex;
+        __syncthreads();
+        if (tid == 0) sm.bg.pref[min(j0 + CTW_BS, nb)] = carry + tt;
+        __syncthreads();
+      }
+      const int total = sm.bg.pref[nb];
+      if (rank == 0 && tid == 0) sm.arcs_f += total;
       for (;;) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(&sm.work, 32);
+        if (lane_ == 0) base = atomicAdd(&fc->work_b, 32);
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (base >= n_src) break;
-        const int nv = min(32, n_src - base);
-        int deg = 0;
-        if (lane < nv) {
-          const CtwSrc t = src[base + lane];
-          const CtwStateRange r = g.ranges[t.state];
-          deg = (int)(r.emit_end - r.emit_beg);
-          sm.em.beg[w][lane] = r.emit_beg;
-          sm.em.cost[w][lane] = t.cost;
-        }
-        int incl = deg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        sm.em.off[w][lane] = incl - deg;
-        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        if (lane == 0) atomicAdd(&sm.arcs_acc, (unsigned long long)total);
-        __syncwarp();
-        for (int k = lane; k < total; k += 32) {
-          int lo = 0, hi = nv - 1;  // last source with off <= k
+        if (base >= total) break;
+        const int k = base + lane_;
+        if (k < total) {
+          int lo = 0, hi = nb - 1;  // last listed source with pref <= k
           while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (sm.em.off[w][mid] <= k) lo = mid;
+            if (sm.bg.pref[mid] <= k) lo = mid;
             else hi = mid - 1;
           }
-          const uint32_t arc_i = sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]);
-          const CtwArc arc = g.arcs[arc_i];
-          double ac;
-          if (smem_ll) ac = nll_s[arc.ilabel - 1];
-          else {
-            const long long idx = row0 + arc.ilabel - 1;
-            const double x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
-            ac = __dmul_rn(neg_scale, x);
-          }
-          double nc = __dadd_rn(__dadd_rn(sm.em.cost[w][lo], ac), arc.weight);
-          if (boost) {
-            const int32_t ol = g.olabel[arc_i];
-            if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
-          }
-          if (!(nc < INF)) continue;
-          bool is_new = false;
-          ulonglong2 seen;
-          const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
-          if (d == CTW_EMPTY) {
-            atomicMax(&sm.status, CTW_GROW_TABLE);
-            continue;
-          }
-          if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
-          CtwTok* ed = &L.T[d];
-          // Gauss-Seidel slot position of an emitting-reached state = its
-          // first-arrival arc (_kernel.pyx:256-272)
-          gpos_min(ed, (unsigned long long)arc_i);
-          if (L.prune && nc > running_cut(sm, a.cfg.beam)) continue;  // cannot make the final beam
-          unsigned long long oldk;
-          const unsigned long long nk = d2key(nc);
-          if (tok_relax_from(L, ed, nk, arc_i, (uint32_t)(base + lo), 0ULL, seen, &oldk)) track_min(sm, nk);
+          emit_arc(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
+                   sm.bg.beg[lo] + (uint32_t)(k - sm.bg.pref[lo]), sm.bg.cost[lo], (uint32_t)sm.bg.idx[lo]);
         }
-        __syncwarp();
       }
       __syncthreads();
+      if (tid == 0) sm.snap_slots = sm.n_slots;
+      csync(sm);  // (C)
     }
 
-    {
+    if (rank == 0 && tid == 0) {
       const long long t = clock64();
       prof[0] += t - tclk;
       tclk = t;
     }
     // ---- epsilon closure ----
     int st = CTW_OK;
-    if (sm.status < CTW_GROW_TABLE)
-      st = eps_fixpoint(sm, L, g, lane.front, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
+    if (sm.st_all < CTW_GROW_TABLE)
+      st = eps_fixpoint(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
+    const int vote = sm.st_all;
+    if (tid == 0) {
+      int tot = 0, off = 0;
+      for (int k = 0; k < R; ++k) {
+        const int n = min(cl.map_shared_rank(&sm, k)->n_slots, (int)L.seg);
+        if (k < rank) off += n;
+        tot += n;
+      }
+      sm.n_all = tot;
+      sm.svoff = off;
+    }
     __syncthreads();
-    {
-      const long long t = clock64();
-      prof[1] += t - tclk;
-      prof[6] += sm.passes;
-      prof[8] += sm.n_slots;
+    const int n_all = sm.n_all;
+    const int n_own = min(sm.n_slots, (int)L.seg);
+    if (tid == 0) {
+      if (rank == 0) {
+        const long long t = clock64();
+        prof[1] += t - tclk;
+        tclk = t;
+        prof[6] += sm.passes;
+        prof[8] += n_all;
+      }
       prof[9] += sm.eps_items;
       prof[10] += sm.eps_arcs;
       prof[12] += sm.eps_ties > 0;
       prof[13] += sm.eps_ties;
       prof[14] += sm.eps_disc;
-      tclk = t;
+      prof[15] += sm.arcs_f;  // (moved to arcs_expanded at the end)
     }
-    const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
-    n_slots_max = max(n_slots_max, n_slots);
+    n_slots_max = max(n_slots_max, n_all);
     if (st != CTW_OK) status = st;
-    else if (sm.status >= CTW_GROW_TABLE) status = sm.status;
-    else if (n_slots == 0) status = CTW_ERR_NO_SURVIVORS;
+    else if (vote >= CTW_GROW_TABLE) status = vote;
+    else if (n_all == 0) status = CTW_ERR_NO_SURVIVORS;
+    else if ((uint32_t)n_all > (L.tcap >> 1)) status = CTW_GROW_TABLE;
 
     // ---- prune: beam cutoff from the frame minimum, exact max_active ----
     const double min_cost = key2d(sm.min_key);
     const double cutoff = __dadd_rn(min_cost, a.cfg.beam);
     const unsigned long long cut_key = d2key(cutoff);
     const double bin_scale = (double)CTW_NB / a.cfg.beam;
-    ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);  // frontier buffers are free now
+    ulonglong2* sv = reinterpret_cast<ulonglong2*>(L.front) + sm.svoff;  // frontier sets are free now
     if (status == CTW_OK)
-      status = count_pass(sm, L, sv, n_slots, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
-    {
+      status = count_pass(sm, L, fc, sv, n_own, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
+#ifdef CTW_DEBUG
+    if (status == CTW_OK && tid == 0) {
+      const unsigned long long gm = *((volatile unsigned long long*)&G->min_key);
+      if (gm != sm.min_key)
+        printf("min mismatch lane %d rank %d frame %d local %.17g rank0 %.17g passes %d\n", b, rank, f,
+               key2d(sm.min_key), key2d(gm), sm.passes);
+    }
+#endif
+    if (rank == 0 && tid == 0) {
       const long long t = clock64();
       prof[2] += t - tclk;
       tclk = t;
     }
-    prof[11] += sm.cnt;
     if (status == CTW_OK) {
-      const int in_beam = sm.cnt;
+      const int in_beam = sm.cnt_all;
+      if (rank == 0) prof[11] += in_beam;
       const bool select = (long long)in_beam > a.cfg.max_active;
       const int n_surv = select ? (int)a.cfg.max_active : in_beam;
-      if (select) select_threshold(sm, L, sv, n_slots, cut_key, min_cost, bin_scale, a.cfg.max_active);
-      __syncthreads();
-      {
+      if (select) select_threshold(sm, L, fc, sv, n_own, cut_key, min_cost, bin_scale, a.cfg.max_active);
+      if (rank == 0 && tid == 0) {
         const long long t = clock64();
         prof[3] += t - tclk;
         prof[7] += select;
@@ -1009,15 +1331,17 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
         status = CTW_GROW_HIST;
         rec_need = n_rec + n_surv;
       } else {
-        // ---- records + next sources: per-thread counts, one scan, then
-        // independent per-survivor writes (no per-tile barriers) ----
-        const bool radix = select && sm.sel_radix;
-        const int bsel = select ? sm.sel_bin : CTW_NB;
-        const unsigned long long tk = sm.thr_key;
-        const uint32_t ts = sm.thr_state;
-        const int depth = sm.sel_depth;
-        const unsigned long long ph = sm.sel_hi;
-        const uint32_t pl = sm.sel_lo;
+        // ---- records + next sources: per-thread counts, one block scan,
+        // one cluster counter for the rank's base, then independent
+        // per-survivor writes (record order inside a frame is free: the
+        // export orders by state) ----
+        const bool radix = select && sm.l_radix;
+        const int bsel = select ? sm.l_bin : CTW_NB;
+        const unsigned long long tk = sm.l_tk;
+        const uint32_t ts = sm.l_ts;
+        const int depth = sm.l_depth;
+        const unsigned long long ph = sm.l_ph;
+        const uint32_t pl = sm.l_pl;
         auto keep = [&](unsigned long long key, uint32_t state) -> bool {
           if (key > cut_key) return false;
           if (!select) return true;
@@ -1026,21 +1350,24 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
           return bb < bsel || (bb == bsel && (key < tk || (key == tk && state <= ts)));
         };
         int mine = 0;
-        for (int i = tid; i < n_slots; i += CTW_BS) mine += keep(sv[i].x, L.slots[i].y);
+        for (int i = tid; i < n_own; i += CTW_BS) mine += keep(sv[i].x, L.slots[i].y);
         int pos, tot;
         Smem::Scan(sm.scan).ExclusiveSum(mine, pos, tot);
-        const int hop_cap = n_slots + 2;
-        for (int i = tid; i < n_slots; i += CTW_BS) {
+        if (tid == 0) sm.rbase = atomicAdd(&fc->rec_ctr, tot);
+        __syncthreads();
+        pos += sm.rbase;
+        const int hop_cap = n_all + 2;
+        for (int i = tid; i < n_own; i += CTW_BS) {
           const ulonglong2 v0 = sv[i];
           const unsigned long long key = v0.x;
           const uint2 it = L.slots[i];
           const uint32_t h = it.x, st2 = it.y;
           if (!keep(key, st2)) continue;
-          const WalkEnd w = walk(L, g, v0, src, pend, hop_cap);
-          if (!w.ok) sm.hop_fail = 1;
-          const int32_t code = record_code(sm, L, g, h, w);
+          const WalkEnd wk = walk(L, g, v0, src, pend, hop_cap);
+          if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
+          const int32_t code = record_code(sm, L, g, h, wk);
           const long long r = n_rec + pos;
-          lane.rec_link[r] = make_int2(w.bp, code);
+          lane.rec_link[r] = make_int2(wk.bp, code);
           lane.rec_state[r] = (int32_t)st2;
           const double cost = key2d(key);
           lane.rec_cost[r] = cost;
@@ -1051,24 +1378,25 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
           nsrc[pos] = ns;
           ++pos;
         }
-        if (tid == 0) lane.frame_base[lane.frame_count + f] = n_rec;
-        n_rec += tot;
-        n_src = tot;
+        if (rank == 0 && tid == 0) lane.frame_base[lane.frame_count + f] = n_rec;
+        const int v2 = csync(sm);  // (H)
+        if (tid == 0) sm.tot_surv = *((volatile int*)&fc->rec_ctr);
         __syncthreads();
-        if (sm.status >= CTW_GROW_TABLE) status = sm.status;
-        else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
+        n_rec += sm.tot_surv;
+        n_src = sm.tot_surv;
+        if (v2 != CTW_OK) status = v2;  // grow request (>= 16) or a failed walk (ERR_EPS_ITERS)
       }
     }
-    {
+    if (rank == 0 && tid == 0) {
       const long long t = clock64();
       prof[4] += t - tclk;
       tclk = t;
     }
 
-    // ---- reset every touched table entry (also on failure) ----
-    reset_slots(L, n_slots);
+    // ---- reset every table entry this rank created (also on failure) ----
+    reset_slots(L, n_own);
     __syncthreads();
-    prof[5] += clock64() - tclk;
+    if (rank == 0 && tid == 0) prof[5] += clock64() - tclk;
     if (status != CTW_OK) {
       err_frame = f;
       break;
@@ -1077,15 +1405,35 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
     pend_valid = 0;
   }
 
-  if (tid == 0) {
+  // per-rank diagnostics -> rank 0 (plain stores + remote loads between two
+  // barriers; the second keeps every rank's shared memory alive until rank 0
+  // has read it)
+  if (tid == 0)
+    for (int k = 0; k < CTW_NPROF; ++k) sm.mydiag[k] = (unsigned long long)prof[k];
+  cl.sync();
+  long long dsum[6] = {0, 0, 0, 0, 0, 0};
+  if (rank == 0 && tid == 0)
+    for (int r = 0; r < R; ++r) {
+      const Smem* o = cl.map_shared_rank(&sm, r);
+      const int ks[6] = {9, 10, 12, 13, 14, 15};
+      for (int j = 0; j < 6; ++j) dsum[j] += (long long)o->mydiag[ks[j]];
+    }
+  cl.sync();
+  if (rank == 0 && tid == 0) {
     CtwLaneOut o;
     o.status = status;
     o.err_frame = err_frame;
     o.n_slots_max = n_slots_max;
-    o.arcs_expanded = (long long)sm.arcs_acc;
+    o.arcs_expanded = dsum[5];
     o.src_total = src_total;
     o.rec_need = rec_need;
     for (int k = 0; k < CTW_NPROF; ++k) o.prof[k] = prof[k];
+    o.prof[9] = dsum[0];
+    o.prof[10] = dsum[1];
+    o.prof[12] = dsum[2];
+    o.prof[13] = dsum[3];
+    o.prof[14] = dsum[4];
+    o.prof[15] = 0;
     if (status == CTW_OK) {
       lane.n_src = n_src;
       lane.src_buf = (F > 0) ? cur_buf : committed;
@@ -1109,44 +1457,55 @@ __global__ void __launch_bounds__(CTW_BS, 4) k_decode_chunk(CtwLane* lanes, Grap
 // Fresh channel: token at the start state plus its epsilon closure
 // (decoder.py:173-229, same pass discipline: the start slot is slot 0). All
 // closure states become sources with bp = -1 and their pending olabel chains
-// (no pruning at seed time, as in the reference).
+// (no pruning at seed time, as in the reference). One CTA per lane (a cluster
+// of one rank).
 __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, const int* lane_ids, int start,
                                                  CtwDecodeCfg cfg, CtwLaneOut* out) {
   __shared__ Smem sm;
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
-  CtwLane& lane = lanes[lane_ids[blockIdx.x]];
-  LaneCtx L = lane_ctx(lane);
+  const int R = (int)cl.num_blocks();
+  CtwLane& lane = lanes[lane_ids[blockIdx.x / R]];
+  LaneCtx L = lane_ctx(lane, 0, 1, &sm);
   L.prune = false;  // no beam at seed time: the whole closure is kept
+  if (R != 1) return;  // launched as single-CTA clusters only
+  FrameCtr* fc = &sm.fc[0];
   if (tid == 0) {
-    sm.status = CTW_OK;
+    sm.status_l = CTW_OK;
+    sm.epoch = 0;
+    sm.st_pub[0] = sm.st_pub[1] = 0;
+    sm.st_all = 0;
     sm.pool_used = 0;
     sm.n_slots = 0;
-    sm.hop_fail = 0;
     sm.min_key = ~0ULL;
-    sm.max_pd = 0;
-    sm.cnt = 0;
+    sm.pw[0] = sm.pw[1] = 0;
+    sm.eps_items = sm.eps_arcs = sm.eps_ties = sm.eps_disc = 0;
+    sm.min_pub[0] = sm.min_pub[1] = ~0ULL;
+    fc->cnt = 0;
+    fc->max_pd = 0;
     bool is_new = false;
     const uint32_t h = tok_insert(L, (uint32_t)start, is_new);
     slot_append(sm, L, h, (uint32_t)start);
     L.T[h].gpos = 0ULL;
     unsigned long long oldk;
     tok_relax(L, &L.T[h], d2key(0.0), CTW_SEED_TB, 0, 0ULL, &oldk);
+    sm.snap_slots = sm.n_slots;
   }
   __syncthreads();
-  int status = eps_fixpoint(sm, L, g, lane.front, lane.boost, cfg.relax_eps, cfg.beam,
+  int status = eps_fixpoint(sm, L, g, fc, lane.boost, cfg.relax_eps, cfg.beam,
                             divergence_cap(cfg.max_ne_iters, L.tcap));
-  __syncthreads();
-  const int n_slots = min((uint32_t)sm.n_slots, L.tcap);
-  if (status == CTW_OK && sm.status >= CTW_GROW_TABLE) status = sm.status;
+  const int n_own = min(sm.n_slots, (int)L.seg);
+  if (status == CTW_OK && sm.st_all >= CTW_GROW_TABLE) status = sm.st_all;
+  if (status == CTW_OK && (uint32_t)sm.n_slots > (L.tcap >> 1)) status = CTW_GROW_TABLE;
   ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);
-  if (status == CTW_OK) status = count_pass(sm, L, sv, n_slots, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
+  if (status == CTW_OK) status = count_pass(sm, L, fc, sv, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
   if (status == CTW_OK) {
     CtwSrc* dst = lane.src[0];
-    for (int i = tid; i < n_slots; i += CTW_BS) {
+    for (int i = tid; i < n_own; i += CTW_BS) {
       const uint32_t h = L.slots[i].x;
       const ulonglong2 v0 = sv[i];
-      const WalkEnd w = walk(L, g, v0, nullptr, nullptr, n_slots + 2);
-      if (!w.ok) sm.hop_fail = 1;
+      const WalkEnd w = walk(L, g, v0, nullptr, nullptr, n_own + 2);
+      if (!w.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
       CtwSrc s;
       s.state = (int32_t)L.slots[i].y;
       s.bp = -1;
@@ -1155,17 +1514,16 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
       lane.pend[i] = record_code(sm, L, g, h, w);
     }
     __syncthreads();
-    if (sm.status >= CTW_GROW_TABLE) status = sm.status;
-    else if (sm.hop_fail) status = CTW_ERR_EPS_ITERS;
+    if (sm.status_l != CTW_OK) status = sm.status_l;
   }
-  reset_slots(L, n_slots);
+  reset_slots(L, n_own);
   __syncthreads();
   if (tid == 0) {
     CtwLaneOut o = {};
     o.status = status;
     o.err_frame = -1;
     if (status == CTW_OK) {
-      lane.n_src = n_slots;
+      lane.n_src = n_own;
       lane.src_buf = 0;
       lane.frame_count = 0;
       lane.pool_used = sm.pool_used;
@@ -1181,6 +1539,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
     out[blockIdx.x] = o;
   }
 }
+
 
 // ------------------------------------------------------- best path -------
 
@@ -1270,6 +1629,19 @@ __global__ void k_clear_table(CtwTok* T, uint32_t n) {
 
 // ------------------------------------------------------ launch wrappers ---
 
+// Ranks (CTAs) per lane for a launch of n lanes: CTW_CLUSTER overrides;
+// otherwise CTW_DEFAULT_CLUSTER.
+static int cluster_size(int n) {
+  (void)n;
+  static int env = -1;
+  if (env < 0) {
+    const char* s = getenv("CTW_CLUSTER");
+    env = s ? atoi(s) : 0;
+    if (env < 0 || env > CTW_RMAX) env = 0;
+  }
+  return env ? env : CTW_DEFAULT_CLUSTER;
+}
+
 extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                  const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
                                  int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
@@ -1280,7 +1652,21 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
   if (dyn + sizeof(Smem) > 48 * 1024)
     cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   (void)cudaGetLastError();  // drop stale errors of unchecked calls
-  k_decode_chunk<<<n, CTW_BS, dyn, stream>>>(d_lanes, g, a, out);
+  const int R = cluster_size(n);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(n * R));
+  lc.blockDim = dim3(CTW_BS);
+  lc.dynamicSmemBytes = dyn;
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)R;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_decode_chunk, d_lanes, g, a, out);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
 
