@@ -182,7 +182,7 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   CtwLane& L = l->h[i];
   if (tlog2 > 24) return fail(-3, "token table would exceed 2^24 entries per lane");
   const uint64_t tcap = 1ull << tlog2;
-  const uint64_t scap = tcap / 2 + 1;
+  const uint64_t scap = CTW_LOAD(tcap) + 1;
   CtwTok* table;
   uint2 *slots, *front;
   CtwSrc* src[3];
@@ -1102,7 +1102,7 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
   CUDA_TRY(cudaSetDevice(device));
   CtwLane& L = l->h[0];
   // table must hold the external sources
-  while ((int64_t)((1ull << L.tlog2) / 2) < n_src)
+  while ((int64_t)CTW_LOAD(1ull << L.tlog2) < n_src)
     if (int r = alloc_table(l, 0, L.tlog2 + 1)) return r;
   if (boost && boost_len < c.g->max_ol + 1) return fail(-1, "boost vector shorter than max_olabel + 1");
   // load sources (bp = -2 - i refers back to act_bp[i]) and their pending chains
@@ -1110,7 +1110,9 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
   std::vector<int32_t> pend((size_t)n_src, 0), pool;
   bool any_pend = false;
   for (int64_t i = 0; i < n_src; ++i) {
-    srcs[i] = CtwSrc{act_state[i], (int32_t)(-2 - i), act_cost[i]};
+    if (act_state[i] < 0 || act_state[i] >= num_states) return fail(-1, "active state out of range");
+    const int32_t st = act_state[i];
+    srcs[i] = CtwSrc{st, (int32_t)(-2 - i), act_cost[i], (uint32_t)eps_end[st], (uint32_t)off[st + 1]};
     const int64_t a0 = act_chain_off[i], a1 = act_chain_off[i + 1];
     if (a1 - a0 == 1) pend[i] = act_chain_pool[a0];
     else if (a1 - a0 > 1) {
@@ -1119,7 +1121,6 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
       for (int64_t k = a0; k < a1; ++k) pool.push_back(act_chain_pool[k]);
     }
     any_pend |= a1 > a0;
-    if (act_state[i] < 0 || act_state[i] >= num_states) return fail(-1, "active state out of range");
   }
   if (int r = grow_pool(l, 0, (int64_t)pool.size() + 1)) return r;
   if (n_src) {

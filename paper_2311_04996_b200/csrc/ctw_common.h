@@ -68,11 +68,14 @@ struct __align__(32) CtwTok {
 #define CTW_EPS_BIT 0x80000000u
 #define CTW_SEED_TB 0x7FFFFFFFu
 
-// Active token (16 B): the frame's sources / survivors.
+// Active token (32 B): the frame's sources / survivors.
 struct __align__(16) CtwSrc {
   int32_t state;
   int32_t bp;  // record index in this lane's history, -1 root, <= -2: external (compat)
   double cost;
+  // the state's emitting arc range, cached with the token so the expansion
+  // reads arcs without a dependent range lookup
+  uint32_t emit_beg, emit_end;
 };
 
 // Device-side descriptor of one lane (= one decoding channel). The host owns
@@ -80,11 +83,13 @@ struct __align__(16) CtwSrc {
 // A lane is decoded by one thread-block cluster of up to CTW_RMAX CTAs
 // ("ranks"). Every rank appends the slots it creates to its own segment of
 // the slot list and the epsilon frontiers it produces to its own segments of
-// the frontier sets; segments hold tcap/2 entries (the table is grown before
-// it is half full, so a segment never needs more).
+// the frontier sets. The token table is grown once a frame fills more than
+// CTW_LOAD(tcap) entries (3/4 load), so a segment of CTW_LOAD(tcap) entries
+// never overflows in a frame that commits.
 #define CTW_RMAX 8
-#define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_RMAX * ((tcap) / 2))
-#define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_RMAX * ((tcap) / 2))
+#define CTW_LOAD(tcap) ((tcap) - (tcap) / 4)
+#define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_RMAX * CTW_LOAD(tcap))
+#define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_RMAX * CTW_LOAD(tcap))
 
 struct CtwLane {
   // token hash table: capacity 1 << tlog2

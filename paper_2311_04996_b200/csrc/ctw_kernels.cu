@@ -44,7 +44,7 @@
 #define CTW_BS 512
 #endif
 #ifndef CTW_MINB
-#define CTW_MINB (1024 / CTW_BS)
+#define CTW_MINB (2048 / CTW_BS)  // 64 resident warps per SM: the kernel is latency-bound, occupancy pays
 #endif
 #ifndef CTW_DEFAULT_CLUSTER
 #define CTW_DEFAULT_CLUSTER 8
@@ -115,7 +115,7 @@ __device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
 struct LaneCtx {
   CtwTok* T;
   uint32_t mask, shift, tcap;
-  uint32_t seg;        // entries per rank segment (tcap / 2)
+  uint32_t seg;        // entries per rank segment (CTW_LOAD(tcap))
   uint2* slots;        // this rank's slot segment: (table index, state)
   uint2* slots_base;   // rank 0's segment (rank k's starts at + k * seg)
   uint2* front;        // frontier sets (CTW_FRONT_LEN)
@@ -479,12 +479,13 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
         int s = 0;
         while (s + 1 < n_seg && sm.seg_pref[s + 1] <= i) ++s;
         const uint2 it = sm.seg_ptr[s][i - sm.seg_pref[s]];
+        // the range and the entry are independent loads: issue them together
+        const CtwTok* eu = &L.T[it.x];
         const CtwStateRange r = g.ranges[it.y];
+        const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
+        const unsigned long long gu = __ldcg(&eu->gpos);
         deg = (int)(r.emit_beg - r.eps_beg);
         if (deg > 0) {
-          const CtwTok* eu = &L.T[it.x];
-          const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
-          const unsigned long long gu = __ldcg(&eu->gpos);
           const double c = key2d(v.x);
           const bool valued = v.x != ~0ULL && !(L.prune && c > running_cut(sm, beam));
           uint32_t aux = CTW_DISC;
@@ -806,7 +807,7 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int n
   L.tcap = 1u << lane.tlog2;
   L.mask = L.tcap - 1;
   L.shift = 32 - lane.tlog2;
-  L.seg = L.tcap >> 1;
+  L.seg = CTW_LOAD(L.tcap);
   L.slots_base = lane.slots;
   L.slots = lane.slots + (size_t)rank * L.seg;
   L.front = lane.front;
@@ -824,7 +825,7 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int n
 // correcting passes than slots; beyond that the closure diverges (negative
 // cycle) and the reference's Gauss-Seidel loop hits max_ne_iters too.
 __device__ __forceinline__ long long divergence_cap(long long max_ne_iters, uint32_t tcap) {
-  return max(max_ne_iters, (long long)(tcap >> 1)) + 2;
+  return max(max_ne_iters, (long long)CTW_LOAD(tcap)) + 2;
 }
 
 __device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost, double bin_scale) {
@@ -1159,7 +1160,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       int deg = 0;
       if (lane_ < nv) {
         const CtwSrc t = src[base + lane_];
-        const CtwStateRange r = g.ranges[t.state];
+        const CtwStateRange r{0u, t.emit_beg, t.emit_end, 0u};  // cached with the token
         deg = (int)(r.emit_end - r.emit_beg);
         if (deg > CTW_BIG) {
           const int j = atomicAdd(&fc->nbig, 1);
@@ -1292,7 +1293,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     if (st != CTW_OK) status = st;
     else if (vote >= CTW_GROW_TABLE) status = vote;
     else if (n_all == 0) status = CTW_ERR_NO_SURVIVORS;
-    else if ((uint32_t)n_all > (L.tcap >> 1)) status = CTW_GROW_TABLE;
+    else if ((uint32_t)n_all > CTW_LOAD(L.tcap)) status = CTW_GROW_TABLE;
 
     // ---- prune: beam cutoff from the frame minimum, exact max_active ----
     const double min_cost = key2d(sm.min_key);
@@ -1363,6 +1364,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           const uint2 it = L.slots[i];
           const uint32_t h = it.x, st2 = it.y;
           if (!keep(key, st2)) continue;
+          const CtwStateRange rg = g.ranges[st2];  // independent of the walk: overlaps it
           const WalkEnd wk = walk(L, g, v0, src, pend, hop_cap);
           if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
           const int32_t code = record_code(sm, L, g, h, wk);
@@ -1375,6 +1377,8 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           ns.state = (int32_t)st2;
           ns.bp = (int32_t)r;
           ns.cost = cost;
+          ns.emit_beg = rg.emit_beg;
+          ns.emit_end = rg.emit_end;
           nsrc[pos] = ns;
           ++pos;
         }
@@ -1496,7 +1500,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
                             divergence_cap(cfg.max_ne_iters, L.tcap));
   const int n_own = min(sm.n_slots, (int)L.seg);
   if (status == CTW_OK && sm.st_all >= CTW_GROW_TABLE) status = sm.st_all;
-  if (status == CTW_OK && (uint32_t)sm.n_slots > (L.tcap >> 1)) status = CTW_GROW_TABLE;
+  if (status == CTW_OK && (uint32_t)sm.n_slots > CTW_LOAD(L.tcap)) status = CTW_GROW_TABLE;
   ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);
   if (status == CTW_OK) status = count_pass(sm, L, fc, sv, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
   if (status == CTW_OK) {
@@ -1510,6 +1514,9 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
       s.state = (int32_t)L.slots[i].y;
       s.bp = -1;
       s.cost = key2d(v0.x);
+      const CtwStateRange rg = g.ranges[s.state];
+      s.emit_beg = rg.emit_beg;
+      s.emit_end = rg.emit_end;
       dst[i] = s;
       lane.pend[i] = record_code(sm, L, g, h, w);
     }
