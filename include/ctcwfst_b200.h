@@ -156,6 +156,11 @@ int ctw_lanes_reset_stats(ctw_lanes* l);
  * [12] frames with an epsilon/epsilon tie between distinct predecessors,
  * [13] such ties, [14] epsilon arcs relaxed for discovery only, [15] reserved. */
 int ctw_lanes_profile(ctw_lanes* l, int64_t* out16);
+/* Host-side breakdown of ctw_advance since the last reset: out10 =
+ * {staging H2D s, capacity pre-sizing s, launch-to-completion wait s,
+ * post-processing s, grow re-runs, calls, lanes re-run for a bigger token
+ * table / history / olabel pool / source buffer}. Diagnostics. */
+int ctw_lanes_host_timing(ctw_lanes* l, double* out10);
 void* ctw_lanes_stream(ctw_lanes* l);
 
 /* The reference kernel contract (_pykernel.py:28-248) on the GPU: same inputs

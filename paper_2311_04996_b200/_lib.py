@@ -60,6 +60,7 @@ _SIGS = {
                               C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     "ctw_lanes_reset_stats": (I32, [P]),
     "ctw_lanes_profile": (I32, [P, P]),
+    "ctw_lanes_host_timing": (I32, [P, P]),
     "ctw_lanes_stream": (P, [P]),
     "ctw_advance_chunk_compat": (I32, [P] * 6 + [I64, I64] + [P] * 5 + [I64, P, I64, I64, F64, F64,
                                       I64, F64, I64, P, I64, I64, I32, C.POINTER(I64),

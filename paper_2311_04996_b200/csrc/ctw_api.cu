@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -117,6 +118,12 @@ struct ctw_lanes {
   std::vector<int64_t> boost_cap;
   std::vector<char> seeded;
   std::vector<double> surv_ema;  // survivors per frame estimate, for history sizing
+  // paged history: per-lane page lists (host) mirrored in device page tables;
+  // pages beyond a lane's first return to a free list when it is reset
+  std::vector<std::vector<CtwRecPage*>> hpages;
+  std::vector<int64_t> ptab_cap;
+  std::vector<CtwRecPage*> free_pages;
+  std::vector<CtwRecPage*> slabs;  // page allocations (CTW_SLAB pages each)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   // scratch
@@ -149,6 +156,11 @@ struct ctw_lanes {
   // stats
   int64_t launches = 0, decode_launches = 0, arcs = 0, srcs = 0, frames = 0, max_slots = 0;
   double decode_ms = 0.0;
+  // host-side breakdown of ctw_advance (seconds): staging H2D, capacity
+  // pre-sizing, launch-to-completion, post-processing; grow re-runs
+  double h_stage = 0, h_presize = 0, h_wait = 0, h_post = 0;
+  int64_t h_reruns = 0, h_calls = 0;
+  int64_t h_grow[4] = {0, 0, 0, 0};  // lanes re-run for: table, history, pool, sources
   int64_t prof[CTW_NPROF] = {0};
   uint32_t tlog2_hint = 0;  // largest token-table size any lane of this set grew to
   std::mutex mu;
@@ -169,20 +181,21 @@ void free_lane(CtwLane& L, cudaStream_t st) {
   sfree(L.front, st);
   for (auto& s : L.src) sfree(s, st);
   sfree(L.pend, st);
-  sfree(L.rec_link, st);
-  sfree(L.rec_state, st);
-  sfree(L.rec_cost, st);
+  sfree(L.pages, st);
   sfree(L.frame_base, st);
   sfree(L.pool, st);
 }
 
 // (Re)allocate the table-sized buffers of lane i at capacity 1 << tlog2,
-// preserving the committed sources (and their pending chains).
-int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
+// preserving the committed sources (and their pending chains). Sources hold
+// at most max_active survivors, or the seed closure (want_src).
+int alloc_table(ctw_lanes* l, int i, uint32_t tlog2, int64_t want_src = 0) {
   CtwLane& L = l->h[i];
   if (tlog2 > 24) return fail(-3, "token table would exceed 2^24 entries per lane");
   const uint64_t tcap = 1ull << tlog2;
-  const uint64_t scap = CTW_LOAD(tcap) + 1;
+  const int64_t want = std::max<int64_t>({want_src, (int64_t)L.scap, std::min<int64_t>(l->cfg.max_active, 1 << 30),
+                                          (int64_t)L.n_src, 256});
+  const uint64_t scap = (uint64_t)std::min<int64_t>(want, (int64_t)CTW_LOAD(tcap)) + 1;
   CtwTok* table;
   uint2 *slots, *front;
   CtwSrc* src[3];
@@ -213,6 +226,7 @@ int alloc_table(ctw_lanes* l, int i, uint32_t tlog2) {
   for (int b = 0; b < 3; ++b) L.src[b] = src[b];
   L.pend = pend;
   L.tlog2 = tlog2;
+  L.scap = (int32_t)(scap - 1);
   l->tlog2_hint = std::max(l->tlog2_hint, tlog2);
   return sync_lane(l, i);
 }
@@ -227,15 +241,46 @@ int grow_keep(cudaStream_t st, T*& p, int64_t keep, int64_t ncap) {
   return 0;
 }
 
+#define CTW_SLAB 16
+
+// History capacity: append pages (recycled ones first) until `need` records
+// fit; only the lane's page table is uploaded -- records are never copied.
 int grow_hist(ctw_lanes* l, int i, int64_t need) {
   CtwLane& L = l->h[i];
   if (need <= L.rcap) return 0;
-  int64_t ncap = std::max<int64_t>(need, 2 * L.rcap);
-  if (int r = grow_keep(l->stream, L.rec_link, L.n_rec, ncap)) return r;
-  if (int r = grow_keep(l->stream, L.rec_state, L.n_rec, ncap)) return r;
-  if (int r = grow_keep(l->stream, L.rec_cost, L.n_rec, ncap)) return r;
-  L.rcap = ncap;
+  auto& pg = l->hpages[i];
+  while ((int64_t)pg.size() * CTW_PAGE < need) {
+    CtwRecPage* p = nullptr;
+    if (l->free_pages.empty()) {
+      // pages come in slabs: one allocation per CTW_SLAB pages
+      CtwRecPage* slab = nullptr;
+      CUDA_TRY(salloc(&slab, CTW_SLAB, l->stream));
+      l->slabs.push_back(slab);
+      for (int k = CTW_SLAB - 1; k >= 0; --k) l->free_pages.push_back(slab + k);
+    }
+    p = l->free_pages.back();
+    l->free_pages.pop_back();
+    pg.push_back(p);
+  }
+  if ((int64_t)pg.size() > l->ptab_cap[i]) {
+    const int64_t nc = std::max<int64_t>((int64_t)pg.size(), 2 * l->ptab_cap[i]);
+    sfree(L.pages, l->stream);
+    CUDA_TRY(salloc(&L.pages, (size_t)nc, l->stream));
+    l->ptab_cap[i] = nc;
+  }
+  CUDA_TRY(cudaMemcpyAsync(L.pages, pg.data(), pg.size() * sizeof(CtwRecPage*), cudaMemcpyHostToDevice, l->stream));
+  L.rcap = (int64_t)pg.size() * CTW_PAGE;
   return sync_lane(l, i);
+}
+
+// A lane starts a new utterance: keep one history page, recycle the rest.
+void trim_hist(ctw_lanes* l, int i) {
+  auto& pg = l->hpages[i];
+  while (pg.size() > 1) {
+    l->free_pages.push_back(pg.back());
+    pg.pop_back();
+  }
+  l->h[i].rcap = (int64_t)pg.size() * CTW_PAGE;
 }
 
 int grow_frames(ctw_lanes* l, int i, int64_t need) {
@@ -266,16 +311,15 @@ int init_lane(ctw_lanes* l, int i) {
   const uint32_t tlog2 = std::max(std::min<uint32_t>(std::max<uint32_t>(6, ceil_log2(2 * S + 2)), 16),
                                   std::min<uint32_t>(l->tlog2_hint, ceil_log2(2 * S + 2)));
   if (int r = alloc_table(l, i, tlog2)) return r;
-  L.rcap = 1 << 12;
+  L.rcap = 0;
   L.fcap = 256;
   L.pcap = 1 << 10;
   cudaStream_t st = l->stream;
-  CUDA_TRY(salloc(&L.rec_link, (size_t)L.rcap, st));
-  CUDA_TRY(salloc(&L.rec_state, (size_t)L.rcap, st));
-  CUDA_TRY(salloc(&L.rec_cost, (size_t)L.rcap, st));
+  l->hpages[i].clear();
+  l->ptab_cap[i] = 0;
   CUDA_TRY(salloc(&L.frame_base, (size_t)L.fcap, st));
   CUDA_TRY(salloc(&L.pool, (size_t)L.pcap, st));
-  return sync_lane(l, i);
+  return grow_hist(l, i, 1);
 }
 
 int ensure_scratch(ctw_lanes* l, int n) {
@@ -322,6 +366,8 @@ int reserve_lanes(ctw_lanes* l, int n) {
     l->d = nd;
     l->cap = c;
   }
+  l->hpages.resize(n);
+  l->ptab_cap.resize(n, 0);
   for (int i = l->n; i < n; ++i) {
     if (int r = init_lane(l, i)) return r;
   }
@@ -393,6 +439,9 @@ int run_seed(ctw_lanes* l, std::vector<int> ids, std::vector<int>& st) {
       CtwLane& L = l->h[lane];
       if (o.status == CTW_GROW_TABLE) {
         if (int r = alloc_table(l, lane, L.tlog2 + 1)) return r;
+        again.push_back(lane);
+      } else if (o.status == CTW_GROW_SRC) {
+        if (int r = alloc_table(l, lane, L.tlog2, 2 * (int64_t)L.scap + 1)) return r;
         again.push_back(lane);
       } else if (o.status == CTW_GROW_POOL) {
         if (int r = grow_pool(l, lane, 2 * (int64_t)L.pcap)) return r;
@@ -541,6 +590,16 @@ int ctw_lanes_create(ctw_graph* g, int32_t n_lanes, const ctw_config* cfg, void*
   }
   cudaEventCreate(&l->ev0);
   cudaEventCreate(&l->ev1);
+  {
+    // lane buffers come from the stream-ordered pool; keep freed memory
+    // mapped in the pool (regrown tables / history pages reuse it instead of
+    // remapping at every synchronisation)
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, g->device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (int r = reserve_lanes(l, n_lanes)) {
     ctw_lanes_destroy(l);
     return r;
@@ -557,6 +616,7 @@ void ctw_lanes_destroy(ctw_lanes* l) {
     free_lane(l->h[i], l->stream);
     dfree(l->boost_buf[i]);
   }
+  for (CtwRecPage* p : l->slabs) sfree(p, l->stream);
   cudaStreamSynchronize(l->stream);
   if (l->h) cudaFreeHost(l->h);
   dfree(l->d);
@@ -622,6 +682,7 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
     L.pool_used = 0;
     L.n_rec = 0;
     L.pend_valid = 0;
+    trim_hist(l, lane);
     if (int r = sync_lane(l, lane)) return r;
   }
   std::vector<int> st;
@@ -667,6 +728,10 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
   ctw_graph* g = l->g;
   CUDA_TRY(cudaSetDevice(g->device));
   if (n <= 0) return 0;
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  const clk::time_point t0 = clk::now();
+  l->h_calls++;
   if (int r = check_ids(l, lane_ids, n)) return r;
   if (dtype != 0 && dtype != 1) return fail(-1, "dtype must be 0 (f32) or 1 (f64)");
   if (width < g->max_il) return fail(-1, "frame width smaller than the graph's max input label");
@@ -697,22 +762,30 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
                                l->stream));
     dev_ll = l->d_stage - lo * (int64_t)esz;
   }
+  const clk::time_point t1 = clk::now();
+  l->h_stage += secs(t0, t1);
   // pre-size per-lane frame / history capacity
   for (int i = 0; i < n; ++i) {
     const int lane = lane_ids[i];
     CtwLane& L = l->h[lane];
     if (int r = grow_frames(l, lane, (int64_t)L.frame_count + frames[i])) return r;
-    double est = l->surv_ema[lane];
-    if (est < 0) est = (double)std::min<int64_t>(l->cfg.max_active, 2048);
-    const int64_t need = L.n_rec + (int64_t)std::ceil(est * 1.25 * frames[i]) + 64;
+    // history is paged (growing never copies a record), so reserve for the
+    // worst case: max_active survivors per frame (or twice the observed
+    // rate when max_active is effectively unbounded)
+    const double ema = l->surv_ema[lane];
+    const double est = std::min<double>((double)l->cfg.max_active, std::max(ema < 0 ? 65536.0 : 2.0 * ema, 4096.0));
+    const int64_t need = L.n_rec + (int64_t)std::ceil(est * frames[i]) + 64;
     if (need > L.rcap)
       if (int r = grow_hist(l, lane, need)) return r;
   }
   std::vector<int> pos(l->n, -1);
   for (int i = 0; i < n; ++i) pos[lane_ids[i]] = i;
   std::vector<int> todo(lane_ids, lane_ids + n);
+  l->h_presize += secs(t1, clk::now());
   for (int round = 0; !todo.empty(); ++round) {
     if (round > 60) return fail(-1, "advance: grow loop did not converge");
+    if (round) l->h_reruns++;
+    const clk::time_point tl = clk::now();
     const int m = (int)todo.size();
     for (int k = 0; k < m; ++k) {
       const int i = pos[todo[k]];
@@ -732,6 +805,8 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     l->decode_launches++;
     CUDA_TRY(cudaMemcpyAsync(l->h_out, l->d_out, m * sizeof(CtwLaneOut), cudaMemcpyDeviceToHost, l->stream));
     CUDA_TRY(cudaStreamSynchronize(l->stream));
+    const clk::time_point tw = clk::now();
+    l->h_wait += secs(tl, tw);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, l->ev0, l->ev1);
     l->decode_ms += ms;
@@ -742,8 +817,12 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
       const CtwLaneOut& o = l->h_out[k];
       CtwLane& L = l->h[lane];
       l->max_slots = std::max<int64_t>(l->max_slots, o.n_slots_max);
+      if (o.status >= CTW_GROW_TABLE && o.status <= CTW_GROW_SRC) l->h_grow[o.status - CTW_GROW_TABLE]++;
       if (o.status == CTW_GROW_TABLE) {
         if (int r = alloc_table(l, lane, L.tlog2 + 1)) return r;
+        again.push_back(lane);
+      } else if (o.status == CTW_GROW_SRC) {
+        if (int r = alloc_table(l, lane, L.tlog2, std::max<int64_t>(o.rec_need, 2 * (int64_t)L.scap))) return r;
         again.push_back(lane);
       } else if (o.status == CTW_GROW_HIST) {
         const int64_t per = (o.rec_need - L.n_rec) / std::max(1, o.err_frame + 1) + 1;
@@ -770,7 +849,20 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
       }
     }
     todo.swap(again);
+    l->h_post += secs(tw, clk::now());
   }
+  return 0;
+}
+
+int ctw_lanes_host_timing(ctw_lanes* l, double* out) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  out[0] = l->h_stage;
+  out[1] = l->h_presize;
+  out[2] = l->h_wait;
+  out[3] = l->h_post;
+  out[4] = (double)l->h_reruns;
+  out[5] = (double)l->h_calls;
+  for (int k = 0; k < 4; ++k) out[6 + k] = (double)l->h_grow[k];
   return 0;
 }
 
@@ -926,13 +1018,16 @@ int ctw_lane_export(ctw_lanes* l, int32_t lane, int64_t frame_from, int64_t base
   std::vector<int2> link((size_t)R);
   std::vector<int32_t> st((size_t)R), pool((size_t)L.pool_used);
   std::vector<double> cost((size_t)R);
+  const auto& pages = l->hpages[lane];
   std::vector<CtwSrc> src((size_t)L.n_src);
   std::vector<int32_t> pend((size_t)(L.pend_valid ? L.n_src : 0));
   if (F) CUDA_TRY(cudaMemcpyAsync(fb.data(), L.frame_base, F * 8, cudaMemcpyDeviceToHost, l->stream));
-  if (R) {
-    CUDA_TRY(cudaMemcpyAsync(link.data(), L.rec_link, R * sizeof(int2), cudaMemcpyDeviceToHost, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(st.data(), L.rec_state, R * 4, cudaMemcpyDeviceToHost, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(cost.data(), L.rec_cost, R * 8, cudaMemcpyDeviceToHost, l->stream));
+  for (int64_t r0 = 0; r0 < R; r0 += CTW_PAGE) {
+    const CtwRecPage* p = pages[(size_t)(r0 >> CTW_PAGE_LOG2)];
+    const size_t m = (size_t)std::min<int64_t>(CTW_PAGE, R - r0);
+    CUDA_TRY(cudaMemcpyAsync(link.data() + r0, p->link, m * sizeof(int2), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(st.data() + r0, p->state, m * 4, cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaMemcpyAsync(cost.data() + r0, p->cost, m * 8, cudaMemcpyDeviceToHost, l->stream));
   }
   if (L.pool_used)
     CUDA_TRY(cudaMemcpyAsync(pool.data(), L.pool, L.pool_used * 4, cudaMemcpyDeviceToHost, l->stream));
@@ -1023,6 +1118,9 @@ int ctw_lanes_stats(ctw_lanes* l, int64_t* launches, int64_t* decode_launches, d
 int ctw_lanes_reset_stats(ctw_lanes* l) {
   std::lock_guard<std::mutex> lk(l->mu);
   l->launches = l->decode_launches = l->arcs = l->srcs = l->frames = l->max_slots = 0;
+  l->h_stage = l->h_presize = l->h_wait = l->h_post = 0;
+  l->h_reruns = l->h_calls = 0;
+  for (auto& x : l->h_grow) x = 0;
   for (int k = 0; k < CTW_NPROF; ++k) l->prof[k] = 0;
   l->decode_ms = 0.0;
   return 0;
@@ -1104,6 +1202,8 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
   // table must hold the external sources
   while ((int64_t)CTW_LOAD(1ull << L.tlog2) < n_src)
     if (int r = alloc_table(l, 0, L.tlog2 + 1)) return r;
+  if (L.scap < n_src)
+    if (int r = alloc_table(l, 0, L.tlog2, n_src)) return r;
   if (boost && boost_len < c.g->max_ol + 1) return fail(-1, "boost vector shorter than max_olabel + 1");
   // load sources (bp = -2 - i refers back to act_bp[i]) and their pending chains
   std::vector<CtwSrc> srcs((size_t)n_src);

@@ -19,6 +19,7 @@ enum {
   CTW_GROW_TABLE = 16,
   CTW_GROW_HIST = 17,
   CTW_GROW_POOL = 18,
+  CTW_GROW_SRC = 19,
 };
 
 // Per-state arc ranges (16 B, one vector load): epsilon arcs occupy
@@ -68,6 +69,17 @@ struct __align__(32) CtwTok {
 #define CTW_EPS_BIT 0x80000000u
 #define CTW_SEED_TB 0x7FFFFFFFu
 
+// Lattice history page: CTW_PAGE records in struct-of-arrays layout. A
+// lane's history is a table of pages, so it grows by appending pages (no
+// copy of the records already written).
+#define CTW_PAGE_LOG2 16
+#define CTW_PAGE (1 << CTW_PAGE_LOG2)
+struct CtwRecPage {
+  int2 link[CTW_PAGE];      // {prev record, olabel code}
+  int32_t state[CTW_PAGE];
+  double cost[CTW_PAGE];
+};
+
 // Active token (32 B): the frame's sources / survivors.
 struct __align__(16) CtwSrc {
   int32_t state;
@@ -81,33 +93,32 @@ struct __align__(16) CtwSrc {
 // Device-side descriptor of one lane (= one decoding channel). The host owns
 // the authoritative copy; kernels read it and write the committed fields back.
 // A lane is decoded by one thread-block cluster of up to CTW_RMAX CTAs
-// ("ranks"). Every rank appends the slots it creates to its own segment of
-// the slot list and the epsilon frontiers it produces to its own segments of
-// the frontier sets. The token table is grown once a frame fills more than
-// CTW_LOAD(tcap) entries (3/4 load), so a segment of CTW_LOAD(tcap) entries
-// never overflows in a frame that commits.
+// ("ranks") that share one slot list and four epsilon frontier sets
+// (warp-aggregated appends through counters in rank 0's shared memory). The
+// token table is grown once a frame fills more than CTW_LOAD(tcap) entries
+// (3/4 load), so lists of CTW_LOAD(tcap) entries never overflow in a frame
+// that commits.
 #define CTW_RMAX 8
 #define CTW_LOAD(tcap) ((tcap) - (tcap) / 4)
-#define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_RMAX * CTW_LOAD(tcap))
-#define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_RMAX * CTW_LOAD(tcap))
+#define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_LOAD(tcap))
+#define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_LOAD(tcap))
 
 struct CtwLane {
   // token hash table: capacity 1 << tlog2
   CtwTok* table;
-  uint2* slots;      // [CTW_SLOTS_LEN] (table index, state) per slot; rank r owns [r*tcap/2, (r+1)*tcap/2)
-  uint2* front;      // [CTW_FRONT_LEN] 4 frontier sets x CTW_RMAX rank segments (same pairs); also scratch
-  CtwSrc* src[3];    // [tcap/2 + 1] each: committed + two working buffers
-  int32_t* pend;     // [tcap/2 + 1] pending olabel segment of seeded sources
-  int2* rec_link;    // [rcap] {prev record, olabel code}
-  int32_t* rec_state;
-  double* rec_cost;
+  uint2* slots;      // [CTW_SLOTS_LEN] (table index, state) per slot of the frame
+  uint2* front;      // [CTW_FRONT_LEN] 4 frontier sets (same pairs); also scratch
+  CtwSrc* src[3];    // [scap] each: committed + two working buffers
+  int32_t* pend;     // [scap] pending olabel segment of seeded sources
+  CtwRecPage** pages;  // history pages: record r lives in pages[r >> CTW_PAGE_LOG2]
   int64_t* frame_base;  // [fcap] first record of each frame
   int32_t* pool;        // [pcap] multi-label olabel segments: [n, l1..ln]
   const double* boost;  // dense f64[boost_len] or null
   uint32_t tlog2;
   int32_t boost_len;
-  int64_t rcap;
+  int64_t rcap;        // records the pages hold (pages x CTW_PAGE)
   int32_t fcap, pcap;
+  int32_t scap;      // source capacity: >= max_active (survivors) and the seed closure
   // committed channel state
   int32_t n_src, src_buf, frame_count, pool_used;
   int64_t n_rec;

@@ -115,12 +115,13 @@ __device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
 struct LaneCtx {
   CtwTok* T;
   uint32_t mask, shift, tcap;
-  uint32_t seg;        // entries per rank segment (CTW_LOAD(tcap))
-  uint2* slots;        // this rank's slot segment: (table index, state)
-  uint2* slots_base;   // rank 0's segment (rank k's starts at + k * seg)
+  uint32_t seg;        // capacity of the slot list and of each frontier set (CTW_LOAD(tcap))
+  uint2* slots;        // the frame's slot list: (table index, state), cluster-wide, discovery order
   uint2* front;        // frontier sets (CTW_FRONT_LEN)
   Smem* G;             // rank 0's shared memory (cluster counters)
+  int* slot_ctr;       // cluster-wide slot allocation counter of the frame (rank 0)
   int rank, nranks;
+  int sw0, swstride;   // slot sweeps: this rank handles sw0 + tid + k * swstride
   int pool_cap;
   int32_t* pool;
   bool prune;    // CtwLane::prune_ok
@@ -264,7 +265,7 @@ struct FrameCtr {
   int max_pd;   // Gauss-Seidel pass depth of the closure
   int nbb;      // boundary-bin members collected
   int rec_ctr;  // survivors written (records of the frame)
-  int pad;
+  int nslot;    // slots allocated (the slot list's fill)
   uint32_t bhist[CTW_NB];      // cost histogram over [min, min + beam]
 };
 
@@ -305,6 +306,7 @@ struct __align__(16) Smem {
   // ---- cluster fields: meaningful in rank 0 only, reached through DSMEM ----
   FrameCtr fc[2];
   int pw[2];            // epsilon pass chunk counters (pass parity)
+  int pcnt[3][2];       // frontier pushes (next, tiny) of pass p, at [p % 3]
   int pool_used;        // olabel pool fill
   int sel_bin, sel_need, sel_bcount, sel_radix;
   unsigned long long thr_key;  // survivor iff bin < sel_bin or (bin == sel_bin and (key, state) <= thr)
@@ -324,16 +326,15 @@ struct __align__(16) Smem {
   int st_all;           // max status over the ranks at the last barrier
   int n_slots;          // slots this rank created in the frame
   int snap_slots;       // n_slots at the start of the epsilon stage
-  int pc_next[2], pc_tiny[2], pc_big[2];  // frontier pushes of this rank (pass parity)
-  int n_seg, n_cur, any_big;
-  int seg_pref[2 * CTW_RMAX + 1];  // input segments of the current epsilon pass
-  uint2* seg_ptr[2 * CTW_RMAX];
+  int pc_big[2];        // this rank made a big change in the pass (pass parity)
+  int n_cur, n_first, any_big;
+  uint2* in0;           // input of the current epsilon pass: in0[0, n_first) ++ in1[0, n_cur - n_first)
+  uint2* in1;
   int work;             // this rank's chunk counter (rank-local sweeps)
   unsigned long long min_key;  // running minimum seen by this rank (>= the cluster's)
   uint32_t hist[256];          // local digit histogram (radix select)
   uint32_t lbhist[CTW_NB];     // local cost histogram
   int n_all;            // slots of all ranks (after the closure)
-  int svoff;            // this rank's offset in the gathered value array
   int cnt_l, mpd_l, cnt_all, mpd_all;
   int nbig;
   int rbase;            // first survivor index of this rank in the frame
@@ -347,10 +348,22 @@ struct __align__(16) Smem {
   uint32_t l_ts, l_pl;
 };
 
-// Append a newly inserted table index to this rank's slot segment; request a
-// bigger table when the segment is full (the table is grown before half load).
+// Warp-aggregated append to a cluster-wide list: one DSMEM atomic per
+// converged group of appending threads; returns this thread's index.
+__device__ __forceinline__ int agg_alloc(int* ctr, int* local_ctr) {
+  cg::coalesced_group grp = cg::coalesced_threads();
+  int base = 0;
+  if (grp.thread_rank() == 0) {
+    base = atomicAdd(ctr, (int)grp.size());
+    if (local_ctr) atomicAdd(local_ctr, (int)grp.size());
+  }
+  return grp.shfl(base, 0) + (int)grp.thread_rank();
+}
+
+// Append a newly inserted table index to the frame's slot list; request a
+// bigger table when the list is full (the table is grown past 3/4 load).
 __device__ __forceinline__ void slot_append(Smem& sm, const LaneCtx& L, uint32_t h, uint32_t state) {
-  const int s = atomicAdd(&sm.n_slots, 1);
+  const int s = agg_alloc(L.slot_ctr, &sm.n_slots);
   if ((uint32_t)s < L.seg) L.slots[s] = make_uint2(h, state);
   else atomicMax(&sm.status_l, CTW_GROW_TABLE);
 }
@@ -425,43 +438,41 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
   for (long long pass = 1;; ++pass) {
     const int q = (int)(pass & 1);
     const int so = 2 * (int)((pass - 1) & 1);  // output sets of this pass
-    uint2* nxt = L.front + ((size_t)so * CTW_RMAX + rank) * L.seg;
-    uint2* tiny = L.front + ((size_t)(so + 1) * CTW_RMAX + rank) * L.seg;
+    uint2* nxt = L.front + (size_t)so * L.seg;
+    uint2* tiny = L.front + (size_t)(so + 1) * L.seg;
+    int* ctr_out = G->pcnt[pass % 3];
     if (tid == 0) {
-      int tot = 0, ns = 0;
       if (pass == 1) {
-        for (int k = 0; k < R; ++k) {
-          const Smem* o = cl.map_shared_rank(&sm, k);
-          sm.seg_pref[ns] = tot;
-          sm.seg_ptr[ns++] = L.slots_base + (size_t)k * L.seg;
-          tot += min(o->snap_slots, (int)L.seg);
-        }
+        // every slot created before the stage (the ranks' published counts)
+        int tot = 0;
+        for (int k = 0; k < R; ++k) tot += cl.map_shared_rank(&sm, k)->snap_slots;
+        sm.in0 = L.slots;
+        sm.n_first = min(tot, (int)L.seg);
+        sm.in1 = L.slots;
+        sm.n_cur = sm.n_first;
       } else {
-        const int qp = q ^ 1;
         const int si = 2 * (int)((pass - 2) & 1);
-        for (int k = 0; k < R; ++k) {
-          const Smem* o = cl.map_shared_rank(&sm, k);
-          const int nn = min(o->pc_next[qp], (int)L.seg), nt = min(o->pc_tiny[qp], (int)L.seg);
-          sm.seg_pref[ns] = tot;
-          sm.seg_ptr[ns++] = L.front + ((size_t)si * CTW_RMAX + k) * L.seg;
-          tot += nn;
-          sm.seg_pref[ns] = tot;
-          sm.seg_ptr[ns++] = L.front + ((size_t)(si + 1) * CTW_RMAX + k) * L.seg;
-          tot += nt;
-        }
+        const int* ci = G->pcnt[(pass - 1) % 3];
+        const int nn = min(*((volatile const int*)&ci[0]), (int)L.seg);
+        const int nt = min(*((volatile const int*)&ci[1]), (int)L.seg);
+        sm.in0 = L.front + (size_t)si * L.seg;
+        sm.n_first = nn;
+        sm.in1 = L.front + (size_t)(si + 1) * L.seg;
+        sm.n_cur = nn + nt;
       }
-      sm.seg_pref[ns] = tot;
-      sm.n_seg = ns;
-      sm.n_cur = tot;
-      sm.pc_next[q] = 0;
-      sm.pc_tiny[q] = 0;
       sm.pc_big[q] = 0;
-      if (rank == 0) sm.pw[q ^ 1] = 0;  // the next pass's chunk counter
+      if (rank == 0) {
+        sm.pw[q ^ 1] = 0;                          // the next pass's chunk counter
+        sm.pcnt[(pass + 1) % 3][0] = 0;            // written in pass + 1; last read in pass - 1
+        sm.pcnt[(pass + 1) % 3][1] = 0;
+      }
       sm.passes = (int)pass;
     }
     __syncthreads();
     if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
-    const int n_cur = sm.n_cur, n_seg = sm.n_seg;
+    const int n_cur = sm.n_cur, n_first = sm.n_first;
+    const uint2* in0 = sm.in0;
+    const uint2* in1 = sm.in1;
     const uint32_t epoch = (uint32_t)pass;
     // warps grab 32 frontier items at a time and spread the items' epsilon
     // arcs over their lanes
@@ -476,9 +487,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
       int deg = 0;
       if (lane < nv) {
         const int i = base + lane;
-        int s = 0;
-        while (s + 1 < n_seg && sm.seg_pref[s + 1] <= i) ++s;
-        const uint2 it = sm.seg_ptr[s][i - sm.seg_pref[s]];
+        const uint2 it = i < n_first ? in0[i] : in1[i - n_first];
         // the range and the entry are independent loads: issue them together
         const CtwTok* eu = &L.T[it.x];
         const CtwStateRange r = g.ranges[it.y];
@@ -577,15 +586,17 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
           first = atomicExch(&ed->stamp, epoch) != epoch;
         }
         if (first) {
-          if (big) {
-            const int p = atomicAdd(&sm.pc_next[q], 1);
-            if ((uint32_t)p < L.seg) nxt[p] = item;
-            else atomicMax(&sm.status_l, CTW_GROW_TABLE);
+          int p;
+          uint2* dst;
+          if (big) {  // one counter per coalesced group
+            p = agg_alloc(&ctr_out[0], nullptr);
+            dst = nxt;
           } else {
-            const int p = atomicAdd(&sm.pc_tiny[q], 1);
-            if ((uint32_t)p < L.seg) tiny[p] = item;
-            else atomicMax(&sm.status_l, CTW_GROW_TABLE);
+            p = agg_alloc(&ctr_out[1], nullptr);
+            dst = tiny;
           }
+          if ((uint32_t)p < L.seg) dst[p] = item;
+          else atomicMax(&sm.status_l, CTW_GROW_TABLE);
         }
       }
       __syncwarp();
@@ -705,7 +716,7 @@ __device__ __forceinline__ int cmp_prefix(unsigned long long key, uint32_t state
 // prefix bucket is taken whole. Every rank histograms its own slots into rank
 // 0's digit histogram; rank 0 fixes the digit. Leaves (l_ph, l_pl, l_depth)
 // in every rank.
-__device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, int n_own, unsigned long long cut_key,
+__device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, int n_all, unsigned long long cut_key,
                              long long k) {
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
@@ -730,7 +741,7 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, i
     __syncthreads();
     const unsigned long long ph = sm.l_ph;
     const uint32_t pl = sm.l_pl;
-    for (int i = tid; i < n_own; i += CTW_BS) {
+    for (int i = L.sw0 + tid; i < n_all; i += L.swstride) {
       const unsigned long long key = sv[i].x;
       if (key > cut_key) continue;
       const uint32_t st = L.slots[i].y;
@@ -808,12 +819,14 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int n
   L.mask = L.tcap - 1;
   L.shift = 32 - lane.tlog2;
   L.seg = CTW_LOAD(L.tcap);
-  L.slots_base = lane.slots;
-  L.slots = lane.slots + (size_t)rank * L.seg;
+  L.slots = lane.slots;
   L.front = lane.front;
   L.G = G;
+  L.slot_ctr = nullptr;
   L.rank = rank;
   L.nranks = nranks;
+  L.sw0 = rank * CTW_BS;
+  L.swstride = nranks * CTW_BS;
   L.pool = lane.pool;
   L.pool_cap = lane.pcap;
   L.prune = lane.prune_ok != 0;
@@ -843,7 +856,7 @@ __device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost,
 // CTW_ERR_EPS_ITERS), the in-beam count and (hist) the cost histogram over
 // [min, min + beam] for the max-active select; merges them into the frame
 // counters and meets the other ranks at a barrier.
-__device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* sv, int n_own, long long max_ne_iters,
+__device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* sv, int n_all, long long max_ne_iters,
                           unsigned long long cut_key, double min_cost, double bin_scale, bool hist) {
   const int tid = threadIdx.x;
   if (hist)
@@ -854,23 +867,23 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
   }
   __syncthreads();
   int c = 0, mpd = 0;
-  for (int i0 = tid; i0 < n_own; i0 += CTW_UNR * CTW_BS) {
+  for (int i0 = L.sw0 + tid; i0 < n_all; i0 += CTW_UNR * L.swstride) {
     uint32_t h[CTW_UNR];
     ulonglong2 v[CTW_UNR];
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
-      const int i = i0 + u * CTW_BS;
-      h[u] = i < n_own ? L.slots[i].x : 0u;
+      const int i = i0 + u * L.swstride;
+      h[u] = i < n_all ? L.slots[i].x : 0u;
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
-      const int i = i0 + u * CTW_BS;
-      if (i < n_own) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u]]));
+      const int i = i0 + u * L.swstride;
+      if (i < n_all) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u]]));
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
-      const int i = i0 + u * CTW_BS;
-      if (i >= n_own) break;
+      const int i = i0 + u * L.swstride;
+      if (i >= n_all) break;
       sv[i] = v[u];
       if (v[u].x <= cut_key) {
         ++c;
@@ -906,14 +919,15 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
   return (1 + (long long)sm.mpd_all > max_ne_iters) ? CTW_ERR_EPS_ITERS : CTW_OK;
 }
 
-// Reset every table entry this rank created; slot loads batched ahead of the stores.
-__device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_own) {
-  for (int i0 = threadIdx.x; i0 < n_own; i0 += CTW_UNR * CTW_BS) {
+// Reset this rank's share of the frame's table entries; slot loads batched
+// ahead of the stores.
+__device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_all) {
+  for (int i0 = L.sw0 + threadIdx.x; i0 < n_all; i0 += CTW_UNR * L.swstride) {
     uint32_t h[CTW_UNR];
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
-      const int i = i0 + u * CTW_BS;
-      h[u] = i < n_own ? L.slots[i].x : CTW_EMPTY;
+      const int i = i0 + u * L.swstride;
+      h[u] = i < n_all ? L.slots[i].x : CTW_EMPTY;
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u)
@@ -927,7 +941,7 @@ __device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_own) {
 // them exactly in shared memory (bitonic). Falls back to the cluster-wide
 // digit-wise radix select when the boundary bin overflows CTW_BBUF. Leaves
 // the threshold in every rank's l_* fields.
-__device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const ulonglong2* sv, int n_own,
+__device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const ulonglong2* sv, int n_all,
                                  unsigned long long cut_key, double min_cost, double bin_scale, long long k) {
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
@@ -980,10 +994,10 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
   if (bcount == need) return;  // the whole boundary bin survives
   if (bcount > CTW_BBUF) {
     if (tid == 0) sm.l_radix = 1;
-    radix_select(sm, L, sv, n_own, cut_key, k);
+    radix_select(sm, L, sv, n_all, cut_key, k);
     return;
   }
-  for (int i = tid; i < n_own; i += CTW_BS) {
+  for (int i = L.sw0 + tid; i < n_all; i += L.swstride) {
     const unsigned long long key = sv[i].x;
     if (key <= cut_key && cost_bin(key, min_cost, bin_scale) == bsel) {
       const int p = atomicAdd(&fc->nbb, 1);
@@ -1080,8 +1094,8 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
   const double neg_scale = -a.cfg.acoustic_scale;
   const long long pass_cap = divergence_cap(a.cfg.max_ne_iters, L.tcap);
-  BigSrc* bigl = reinterpret_cast<BigSrc*>(L.front + (size_t)3 * CTW_RMAX * L.seg);  // set 3: free until pass 2
-  const int big_cap = (int)min((size_t)CTW_NBIG, ((size_t)CTW_RMAX * L.seg * sizeof(uint2)) / sizeof(BigSrc));
+  BigSrc* bigl = reinterpret_cast<BigSrc*>(L.front + (size_t)3 * L.seg);  // set 3: free until pass 2
+  const int big_cap = (int)min((size_t)CTW_NBIG, ((size_t)L.seg * sizeof(uint2)) / sizeof(BigSrc));
 
   int n_src = lane.n_src;
   int cur_buf = lane.src_buf;
@@ -1103,6 +1117,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     if (rank == 0) {
       sm.pool_used = lane.pool_used;
       sm.pw[0] = sm.pw[1] = 0;
+      for (int j = 0; j < 3; ++j) sm.pcnt[j][0] = sm.pcnt[j][1] = 0;
     }
   }
   if (rank == 0) {
@@ -1114,6 +1129,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   for (int f = 0; f < F; ++f) {
     long long tclk = clock64();
     FrameCtr* fc = &G->fc[f & 1];
+    L.slot_ctr = &fc->nslot;
     const CtwSrc* src = lane.src[cur_buf];
     const int32_t* pend = pend_valid ? lane.pend : nullptr;
     const int nxt_buf = (f & 1) ? w1 : w0;
@@ -1142,7 +1158,10 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       FrameCtr* nf = &sm.fc[(f + 1) & 1];
       int* z = reinterpret_cast<int*>(nf);
       for (int i = tid; i < (int)(sizeof(FrameCtr) / sizeof(int)); i += CTW_BS) z[i] = 0;
-      if (tid == 0) sm.pw[0] = sm.pw[1] = 0;
+      if (tid == 0) {
+        sm.pw[0] = sm.pw[1] = 0;
+        for (int j = 0; j < 3; ++j) sm.pcnt[j][0] = sm.pcnt[j][1] = 0;
+      }
     }
     src_total += n_src;
 
@@ -1262,18 +1281,13 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       st = eps_fixpoint(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
     const int vote = sm.st_all;
     if (tid == 0) {
-      int tot = 0, off = 0;
-      for (int k = 0; k < R; ++k) {
-        const int n = min(cl.map_shared_rank(&sm, k)->n_slots, (int)L.seg);
-        if (k < rank) off += n;
-        tot += n;
-      }
+      int tot = 0;  // slots allocated by all ranks (stable: the closure is over)
+      for (int k = 0; k < R; ++k) tot += cl.map_shared_rank(&sm, k)->n_slots;
       sm.n_all = tot;
-      sm.svoff = off;
     }
     __syncthreads();
-    const int n_all = sm.n_all;
-    const int n_own = min(sm.n_slots, (int)L.seg);
+    const int n_alloc = sm.n_all;
+    const int n_all = min(n_alloc, (int)L.seg);
     if (tid == 0) {
       if (rank == 0) {
         const long long t = clock64();
@@ -1292,17 +1306,17 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     n_slots_max = max(n_slots_max, n_all);
     if (st != CTW_OK) status = st;
     else if (vote >= CTW_GROW_TABLE) status = vote;
-    else if (n_all == 0) status = CTW_ERR_NO_SURVIVORS;
-    else if ((uint32_t)n_all > CTW_LOAD(L.tcap)) status = CTW_GROW_TABLE;
+    else if (n_alloc == 0) status = CTW_ERR_NO_SURVIVORS;
+    else if ((uint32_t)n_alloc > L.seg) status = CTW_GROW_TABLE;
 
     // ---- prune: beam cutoff from the frame minimum, exact max_active ----
     const double min_cost = key2d(sm.min_key);
     const double cutoff = __dadd_rn(min_cost, a.cfg.beam);
     const unsigned long long cut_key = d2key(cutoff);
     const double bin_scale = (double)CTW_NB / a.cfg.beam;
-    ulonglong2* sv = reinterpret_cast<ulonglong2*>(L.front) + sm.svoff;  // frontier sets are free now
+    ulonglong2* sv = reinterpret_cast<ulonglong2*>(L.front);  // gathered values; the frontier sets are free now
     if (status == CTW_OK)
-      status = count_pass(sm, L, fc, sv, n_own, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
+      status = count_pass(sm, L, fc, sv, n_all, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
 #ifdef CTW_DEBUG
     if (status == CTW_OK && tid == 0) {
       const unsigned long long gm = *((volatile unsigned long long*)&G->min_key);
@@ -1321,7 +1335,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       if (rank == 0) prof[11] += in_beam;
       const bool select = (long long)in_beam > a.cfg.max_active;
       const int n_surv = select ? (int)a.cfg.max_active : in_beam;
-      if (select) select_threshold(sm, L, fc, sv, n_own, cut_key, min_cost, bin_scale, a.cfg.max_active);
+      if (select) select_threshold(sm, L, fc, sv, n_all, cut_key, min_cost, bin_scale, a.cfg.max_active);
       if (rank == 0 && tid == 0) {
         const long long t = clock64();
         prof[3] += t - tclk;
@@ -1331,6 +1345,9 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       if (n_rec + n_surv > lane.rcap) {
         status = CTW_GROW_HIST;
         rec_need = n_rec + n_surv;
+      } else if (n_surv > lane.scap) {
+        status = CTW_GROW_SRC;
+        rec_need = n_surv;
       } else {
         // ---- records + next sources: per-thread counts, one block scan,
         // one cluster counter for the rank's base, then independent
@@ -1351,14 +1368,14 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           return bb < bsel || (bb == bsel && (key < tk || (key == tk && state <= ts)));
         };
         int mine = 0;
-        for (int i = tid; i < n_own; i += CTW_BS) mine += keep(sv[i].x, L.slots[i].y);
+        for (int i = L.sw0 + tid; i < n_all; i += L.swstride) mine += keep(sv[i].x, L.slots[i].y);
         int pos, tot;
         Smem::Scan(sm.scan).ExclusiveSum(mine, pos, tot);
         if (tid == 0) sm.rbase = atomicAdd(&fc->rec_ctr, tot);
         __syncthreads();
         pos += sm.rbase;
         const int hop_cap = n_all + 2;
-        for (int i = tid; i < n_own; i += CTW_BS) {
+        for (int i = L.sw0 + tid; i < n_all; i += L.swstride) {
           const ulonglong2 v0 = sv[i];
           const unsigned long long key = v0.x;
           const uint2 it = L.slots[i];
@@ -1369,10 +1386,12 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
           const int32_t code = record_code(sm, L, g, h, wk);
           const long long r = n_rec + pos;
-          lane.rec_link[r] = make_int2(wk.bp, code);
-          lane.rec_state[r] = (int32_t)st2;
+          CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
+          const int ro = (int)(r & (CTW_PAGE - 1));
+          pg->link[ro] = make_int2(wk.bp, code);
+          pg->state[ro] = (int32_t)st2;
           const double cost = key2d(key);
-          lane.rec_cost[r] = cost;
+          pg->cost[ro] = cost;
           CtwSrc ns;
           ns.state = (int32_t)st2;
           ns.bp = (int32_t)r;
@@ -1398,7 +1417,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     }
 
     // ---- reset every table entry this rank created (also on failure) ----
-    reset_slots(L, n_own);
+    reset_slots(L, n_all);
     __syncthreads();
     if (rank == 0 && tid == 0) prof[5] += clock64() - tclk;
     if (status != CTW_OK) {
@@ -1474,6 +1493,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
   L.prune = false;  // no beam at seed time: the whole closure is kept
   if (R != 1) return;  // launched as single-CTA clusters only
   FrameCtr* fc = &sm.fc[0];
+  L.slot_ctr = &fc->nslot;
   if (tid == 0) {
     sm.status_l = CTW_OK;
     sm.epoch = 0;
@@ -1485,8 +1505,10 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
     sm.pw[0] = sm.pw[1] = 0;
     sm.eps_items = sm.eps_arcs = sm.eps_ties = sm.eps_disc = 0;
     sm.min_pub[0] = sm.min_pub[1] = ~0ULL;
+    for (int j = 0; j < 3; ++j) sm.pcnt[j][0] = sm.pcnt[j][1] = 0;
     fc->cnt = 0;
     fc->max_pd = 0;
+    fc->nslot = 0;
     bool is_new = false;
     const uint32_t h = tok_insert(L, (uint32_t)start, is_new);
     slot_append(sm, L, h, (uint32_t)start);
@@ -1500,7 +1522,8 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
                             divergence_cap(cfg.max_ne_iters, L.tcap));
   const int n_own = min(sm.n_slots, (int)L.seg);
   if (status == CTW_OK && sm.st_all >= CTW_GROW_TABLE) status = sm.st_all;
-  if (status == CTW_OK && (uint32_t)sm.n_slots > CTW_LOAD(L.tcap)) status = CTW_GROW_TABLE;
+  if (status == CTW_OK && (uint32_t)sm.n_slots > L.seg) status = CTW_GROW_TABLE;
+  if (status == CTW_OK && n_own > lane.scap) status = CTW_GROW_SRC;
   ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);
   if (status == CTW_OK) status = count_pass(sm, L, fc, sv, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
   if (status == CTW_OK) {
@@ -1605,7 +1628,7 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
   total_cost[warp] = best;
   int count = 0;
   for (int r = src[best_i].bp; r >= 0;) {
-    const int2 lk = lane.rec_link[r];
+    const int2 lk = lane.pages[r >> CTW_PAGE_LOG2]->link[r & (CTW_PAGE - 1)];
     count += code_len(lane.pool, lk.y);
     r = lk.x;
   }
@@ -1614,7 +1637,7 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
   int32_t* w = words + woff[warp];
   int pos = count;
   for (int r = src[best_i].bp; r >= 0;) {
-    const int2 lk = lane.rec_link[r];
+    const int2 lk = lane.pages[r >> CTW_PAGE_LOG2]->link[r & (CTW_PAGE - 1)];
     const int c = lk.y;
     if (c > 0) w[--pos] = c;
     else if (c < 0) {

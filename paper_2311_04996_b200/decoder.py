@@ -300,6 +300,14 @@ class LanePool:
                  "slots", "eps_items", "eps_arcs", "in_beam", "tie_frames", "ties", "eps_disc_arcs", "r15")
         return dict(zip(names, (int(x) for x in v)))
 
+    def host_timing(self) -> dict:
+        """Host-side breakdown of the advance calls (ctw_lanes_host_timing)."""
+        v = np.zeros(10, np.float64)
+        _lib.load().ctw_lanes_host_timing(self.handle, _lib.ptr(v))
+        return {"stage_s": float(v[0]), "presize_s": float(v[1]), "wait_s": float(v[2]), "post_s": float(v[3]),
+                "reruns": int(v[4]), "calls": int(v[5]),
+                "grow_lanes": {"table": int(v[6]), "history": int(v[7]), "pool": int(v[8]), "sources": int(v[9])}}
+
     def reset_stats(self) -> None:
         _lib.load().ctw_lanes_reset_stats(self.handle)
 
