@@ -40,6 +40,10 @@ sys.path.insert(0, str(ROOT))
 FRAME_S = 0.04
 C2 = dict(num_units=129, blank_id=128, num_words=4000, order=3, seed=1, min_pron=1, max_pron=4,
           followers=40, tri_contexts=0.3, tri_followers=8)
+# BASELINE config 3: the large 4-gram TLG (~50M arcs) for the utterance-sharded runs
+C3 = dict(num_units=129, blank_id=128, num_words=10000, order=4, seed=1, min_pron=1, max_pron=4,
+          followers=60, tri_contexts=0.3, tri_followers=8)
+BOOST_WORDS, BOOST_MAG = 100, (0.5, 8.5)  # BASELINE config 5: 100-word table per utterance, |boost| <= beam/2
 LP = dict(delta=6.0, sigma=1.5)
 BEAM, MAX_ACTIVE = 17.0, 10_000
 
@@ -58,16 +62,41 @@ def parse():
     ap.add_argument("--streams", type=int, default=2000, help="C4 streaming channels (0 = skip)")
     ap.add_argument("--stream-seconds", type=float, default=5.0, help="audio per stream in the C4 run")
     ap.add_argument("--cpu-streams", type=int, default=32, help="streams in the CPU reference C4 run")
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"],
+                    help="c2: 3-gram TLG (default, the headline); c3: 4-gram ~50M-arc TLG; "
+                         "c5: c2 + a 100-word boost table per utterance")
     return ap.parse_args()
 
 
-def system(small: bool):
+def system(small: bool, config: str = "c2"):
     from paper_2311_04996_b200 import synth
 
-    spec = dict(C2)
+    spec = dict(C3 if config == "c3" else C2)
     if small:
         spec.update(num_words=300, followers=10)
     return synth.build_system(synth.SystemSpec(**spec))
+
+
+def boost_tables(s, n, seed):
+    """Per-utterance boost vectors (BASELINE config 5): 100 distinct
+    in-vocabulary words, magnitude U(0.5, 8.5), stored as cost -magnitude
+    (reference boosting.py:33-67); dense over olabels like boost_costs()."""
+    rng = np.random.default_rng(seed)
+    nw = s.spec.num_words
+    out = []
+    for _ in range(n):
+        b = np.zeros(s.graph.max_olabel + 1, np.float64)
+        words = rng.choice(np.arange(1, nw + 1), size=min(BOOST_WORDS, nw), replace=False)
+        b[words] = -rng.uniform(*BOOST_MAG, size=len(words))
+        out.append(b)
+    return out
+
+
+def describe(config, fg, n, F):
+    kind = {"c2": "C2: synthetic 3-gram TLG", "c3": "C3: synthetic 4-gram TLG",
+            "c5": "C5: synthetic 3-gram TLG + per-utterance 100-word boost tables"}[config]
+    return ("%s (%d states, %d arcs), Conformer-CTC-shaped log-probs V=129 (blank 128), %d utts x %d frames "
+            "(40 ms) per GPU, beam 17, max_active 10k" % (kind, fg.num_states, fg.num_arcs, n, F))
 
 
 def workload(s, n, frames, rank):
@@ -148,12 +177,23 @@ def ref_flatgraph(ctcwfst, fg):
     return r
 
 
-def cpu_decode(utts, fg, cores):
+def cpu_decode(utts, fg, cores, boosts=None):
+    """The reference's decode_batch on all cores; with per-utterance boosts
+    (config 5) its decode_utterance(boost=...) on the same thread-pool shape
+    (decode_batch takes one boost for the whole batch, decoder.py:436-463)."""
     ctcwfst = ref_module()
     rfg = ref_flatgraph(ctcwfst, fg)
     cfg = ctcwfst.DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE)
+    mats = [u.astype(np.float64) for u in utts]
     t0 = time.perf_counter()
-    hyps = ctcwfst.decode_batch(rfg, cfg, [u.astype(np.float64) for u in utts], workers=cores)
+    if boosts is None:
+        hyps = ctcwfst.decode_batch(rfg, cfg, mats, workers=cores)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            hyps = list(ex.map(lambda i: ctcwfst.decode_utterance(rfg, cfg, mats[i], boost=boosts[i]),
+                               range(len(mats))))
     return hyps, time.perf_counter() - t0
 
 
@@ -256,15 +296,16 @@ def reference_arm(args):
     world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
     if rank != 0:
         return
-    s = system(args.small)
+    s = system(args.small, args.config)
     n = args.cpu_sample
     utts = list(workload(s, n, args.frames, 0))
+    boosts = boost_tables(s, n, 0) if args.config == "c5" else None
     cores = cores_available()
     for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_decode(utts[: max(1, cores)], s.graph, cores)
+        cpu_decode(utts[: max(1, cores)], s.graph, cores, None if boosts is None else boosts[: max(1, cores)])
     times = []
     for _ in range(args.steps):
-        _, dt = cpu_decode(utts, s.graph, cores)
+        _, dt = cpu_decode(utts, s.graph, cores, boosts)
         times.append(dt)
     audio = n * args.frames * FRAME_S
     value = audio * len(times) / sum(times)
@@ -273,9 +314,7 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: 3-gram TLG %d states / %d arcs, V=129, 250-frame utts (10 s), beam 17, "
-                               "max_active 10k; CPU sample of %d utts per step" % (s.graph.num_states,
-                                                                                  s.graph.num_arcs, n)},
+        "config": {"workload": describe(args.config, s.graph, n, args.frames) + "; CPU sample per step"},
         "cpu_baseline": {"value": value, "unit": "x realtime", "cores": cores, "kind": "reference",
                          "sample": f"{n} utterances x {args.frames} frames per step", "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "x realtime", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -295,10 +334,11 @@ def main():
     torch.cuda.set_device(dev)
     from paper_2311_04996_b200 import DecoderConfig, Hypothesis, decode_batch
 
-    s = system(args.small)
+    s = system(args.small, args.config)
     fg = s.graph
     cfg = DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE)
     n, F, V = args.batch, args.frames, s.num_units
+    boosts = boost_tables(s, n, rank) if args.config == "c5" else None
     host = torch.from_numpy(workload(s, n, F, rank)).pin_memory()
     host_np = host.numpy()
     dev_ll = host.to(f"cuda:{dev}")
@@ -312,7 +352,7 @@ def main():
             dist.barrier()
 
     for _ in range(args.warmup):
-        out = decode_batch(fg, cfg, dev_ll, device=dev)
+        out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts)
     assert all(isinstance(h, Hypothesis) for h in out), [h for h in out if not isinstance(h, Hypothesis)][:2]
 
     # ---- value: inputs resident in HBM ----
@@ -325,7 +365,7 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record()
-            out = decode_batch(fg, cfg, dev_ll, device=dev)
+            out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts)
             ev[i][1].record()
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -351,7 +391,7 @@ def main():
     for i in range(args.steps):
         flush.zero_()
         ev2[i][0].record()
-        out_e2e = decode_batch(fg, cfg, host_np, device=dev)
+        out_e2e = decode_batch(fg, cfg, host_np, device=dev, boost=boosts)
         ev2[i][1].record()
     torch.cuda.synchronize()
     e2e_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps
@@ -385,9 +425,7 @@ def main():
         "metric": "decode RTFx (audio s / decode s)", "value": value, "unit": "x realtime", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: synthetic 3-gram TLG (%d states, %d arcs), Conformer-CTC-shaped log-probs "
-                               "V=129 (blank 128), %d utts x %d frames (40 ms) per GPU, beam 17, max_active 10k"
-                               % (fg.num_states, fg.num_arcs, n, F),
+        "config": {"workload": describe(args.config, fg, n, F),
                    "global_batch": world * n, "frames": F, "parallelism": f"utterance-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every step"},
         "utterances_per_s": world * n / (ms_max / 1e3),
@@ -405,7 +443,7 @@ def main():
         "clocks": clk.summary(),
         "stage_profile": _stage_profile(prof, st),
     }
-    if args.streams > 0:
+    if args.streams > 0 and args.config == "c2":
         # warm-up: the same number of channels for one second (lane tables and
         # histories grow to their steady-state sizes; lanes are then recycled)
         streaming_run(s, args.streams, 1.0, rank + 100, device=dev)
@@ -423,10 +461,12 @@ def main():
     if world == 1 and not args.no_cpu:
         k = min(args.cpu_sample, n)
         cores = cores_available()
-        hyps, dt = cpu_decode([host_np[i] for i in range(k)], fg, cores)
+        hyps, dt = cpu_decode([host_np[i] for i in range(k)], fg, cores, None if boosts is None else boosts[:k])
         cpu_rtfx = k * F * FRAME_S / dt
         line["cpu_baseline"] = {"value": cpu_rtfx, "unit": "x realtime", "cores": cores, "kind": "reference",
-                                "sample": f"first {k} of the {n} utterances, reference decode_batch(workers={cores})",
+                                "sample": f"first {k} of the {n} utterances, reference " + (
+                                    f"decode_batch(workers={cores})" if boosts is None else
+                                    f"decode_utterance(boost=...) on {cores} threads"),
                                 "cpu": cpu_model()}
         same = all(getattr(h, "words", None) == g.words for h, g in zip(hyps, out[:k]))
         rel = max(abs(h.total_cost - g.total_cost) / max(1.0, abs(h.total_cost)) for h, g in zip(hyps, out[:k]))

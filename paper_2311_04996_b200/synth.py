@@ -239,6 +239,19 @@ class NgramModel:
         return "\n".join(lines)
 
 
+def _backoff_route(m: NgramModel, ctx: tuple, w: int, lp1: dict, bows: dict) -> float:
+    """log10 p(w | ctx) by the standard backoff recursion over the n-grams
+    generated so far (explicit entry, else backoff(ctx) + p(w | ctx[1:]))."""
+    if not ctx:
+        return lp1[w]
+    e = m.orders.get(len(ctx) + 1, {}).get(ctx + (w,))
+    if e is not None:
+        return e[0]
+    ce = m.orders.get(len(ctx), {}).get(ctx)
+    bo = (ce[1] if ce is not None and ce[1] is not None else 0.0) if len(ctx) > 1 else bows.get(ctx[0], 0.0)
+    return bo + _backoff_route(m, ctx[1:], w, lp1, bows)
+
+
 def random_ngram(rng, vocab: int, order: int, followers: float = 0.6, tri_contexts: float = 0.3,
                  tri_followers: int = 8) -> NgramModel:
     """Random non-uniform backoff LM over word ids 1..vocab (conftest.py:66-107
@@ -272,27 +285,35 @@ def random_ngram(rng, vocab: int, order: int, followers: float = 0.6, tri_contex
         for w, qq in zip(fol.tolist(), q):
             lp2 = max(math.log10(max(mass * qq, 1e-6)), bows[h] + lp1[w] + 0.05)
             big[(h, w)] = [lp2, None]
-    if order >= 3:
-        hist = [g for g in big if g[1] != EOS]
-        n_ctx = int(tri_contexts * len(hist))
+    m.orders[2] = big
+    # orders 3..order: a fraction of the (k-1)-gram histories become contexts
+    # (with a backoff weight) and get Poisson(ho_followers) explicit k-grams,
+    # clamped above their backoff route like the bigrams
+    for k in range(3, order + 1):
+        lower = m.orders[k - 1]
+        hist = [g for g in lower if g[-1] != EOS]
+        frac = tri_contexts if k == 3 else tri_contexts * 0.5
+        foll = tri_followers if k == 3 else max(1, tri_followers // 2)
+        n_ctx = int(frac * len(hist))
         pick = rng.choice(len(hist), size=n_ctx, replace=False) if n_ctx else []
-        tri = {}
+        cur = {}
         for i in sorted(pick):
-            h1, h2 = hist[i]
+            h = hist[i]
             bo = math.log10(rng.uniform(0.2, 0.8))
-            big[(h1, h2)][1] = bo
-            k = int(min(len(cand), max(1, rng.poisson(tri_followers))))
-            fol = rng.choice(cand, size=k, replace=False)
+            lower[h][1] = bo
+            kk = int(min(len(cand), max(1, rng.poisson(foll))))
+            fol = rng.choice(cand, size=kk, replace=False)
             mass = rng.uniform(0.4, 0.9)
-            q = rng.dirichlet(np.ones(k))
+            q = rng.dirichlet(np.ones(kk))
             for w, qq in zip(fol.tolist(), q):
-                e2 = big.get((h2, w))
-                route2 = e2[0] if e2 is not None else bows.get(h2, 0.0) + lp1[w]
-                lp3 = max(math.log10(max(mass * qq, 1e-6)), bo + route2 + 0.05)
-                tri[(h1, h2, w)] = (lp3, None)
-        m.orders[3] = tri
-    m.orders[2] = {g: (v[0], v[1]) for g, v in big.items()}
-    m.max_order = 3 if order >= 3 else 2
+                route = _backoff_route(m, h[1:], w, lp1, bows)
+                lp = max(math.log10(max(mass * qq, 1e-6)), bo + route + 0.05)
+                cur[h + (w,)] = [lp, None]
+        m.orders[k] = cur
+    for kk in list(m.orders):
+        if kk >= 2:
+            m.orders[kk] = {g: (v[0], v[1]) for g, v in m.orders[kk].items()}
+    m.max_order = max(2, order)
     return m
 
 

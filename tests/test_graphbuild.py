@@ -60,7 +60,7 @@ def test_native_compose_matches_reference_build_tlg(seed):
     assert _same(got, want)
 
 
-@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("order", [1, 2, 3, 4])
 def test_grammar_fst_matches_reference_parser(order):
     from ctcwfst.arpa import build_grammar_fst, parse_arpa
     from ctcwfst.wfst import SymbolTable
