@@ -413,6 +413,74 @@ __device__ __forceinline__ int csync(Smem& sm) {
   return sm.st_all;
 }
 
+// Relax one epsilon arc a (loaded: arc) of the frontier item lo of warp w:
+// (c + w) (+ boost), find-or-insert the destination, update its slot
+// position, install the candidate if it wins the Gauss-Seidel order, and
+// queue the destination for the next pass when it changed.
+__device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const double* boost,
+                                        double relax_eps, uint32_t epoch, int q, int* ctr_out, uint2* nxt,
+                                        uint2* tiny, int w, int lo, uint32_t o, uint32_t a, const CtwArc& arc) {
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const uint32_t aux = sm.ep.aux[w][lo];
+  const bool valued = aux != CTW_DISC;
+  double nc = arc.weight;
+  if (valued) {
+    nc = __dadd_rn(sm.ep.cost[w][lo], arc.weight);
+    if (boost) {
+      const int32_t ol = g.olabel[a];
+      if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+    }
+  }
+  if (!(nc < INF)) return;
+  bool is_new = false;
+  ulonglong2 seen;
+  const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
+  if (d == CTW_EMPTY) {
+    atomicMax(&sm.status_l, CTW_GROW_TABLE);
+    return;
+  }
+  if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
+  CtwTok* ed = &L.T[d];
+  gpos_min(ed, sm.ep.gb[w][lo] | min(o, 15u));
+  const uint2 item = make_uint2(d, (uint32_t)arc.nextstate);
+  bool push = false, big = false;
+  if (valued) {
+    unsigned long long oldk;
+    const unsigned long long nk = d2key(nc);
+    if (tok_relax_from(L, ed, nk, CTW_EPS_BIT | a, aux, sm.ep.gu[w][lo], seen, &oldk)) {
+      track_min(sm, nk);
+      push = true;
+      big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
+    } else {
+      push = big = is_new;
+    }
+  } else {
+    push = big = is_new;  // discovery only: successors are discovered next pass
+  }
+  if (!push) return;
+  if (big) sm.pc_big[q] = 1;
+  bool first;
+  if (is_new) {  // this thread created the slot: first to touch its stamp
+    ed->stamp = epoch;
+    first = true;
+  } else {
+    first = atomicExch(&ed->stamp, epoch) != epoch;
+  }
+  if (first) {
+    int p;
+    uint2* dst;
+    if (big) {  // one counter per coalesced group
+      p = agg_alloc(&ctr_out[0], nullptr);
+      dst = nxt;
+    } else {
+      p = agg_alloc(&ctr_out[1], nullptr);
+      dst = tiny;
+    }
+    if ((uint32_t)p < L.seg) dst[p] = item;
+    else atomicMax(&sm.status_l, CTW_GROW_TABLE);
+  }
+}
+
 // ------------------------------------------------------- epsilon fixpoint --
 
 // Label-correcting fixpoint over epsilon arcs, frontier by frontier; the
@@ -539,65 +607,8 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
         }
         const uint32_t o = (uint32_t)(k - sm.ep.off[w][lo]);
         const uint32_t a = sm.ep.beg[w][lo] + o;
-        const uint32_t aux = sm.ep.aux[w][lo];
-        const bool valued = aux != CTW_DISC;
         const CtwArc arc = g.arcs[a];
-        double nc = arc.weight;
-        if (valued) {
-          nc = __dadd_rn(sm.ep.cost[w][lo], arc.weight);
-          if (boost) {
-            const int32_t ol = g.olabel[a];
-            if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
-          }
-        }
-        if (!(nc < INF)) continue;
-        bool is_new = false;
-        ulonglong2 seen;
-        const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
-        if (d == CTW_EMPTY) {
-          atomicMax(&sm.status_l, CTW_GROW_TABLE);
-          continue;
-        }
-        if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
-        CtwTok* ed = &L.T[d];
-        gpos_min(ed, sm.ep.gb[w][lo] | min(o, 15u));
-        const uint2 item = make_uint2(d, (uint32_t)arc.nextstate);
-        bool push = false, big = false;
-        if (valued) {
-          unsigned long long oldk;
-          const unsigned long long nk = d2key(nc);
-          if (tok_relax_from(L, ed, nk, CTW_EPS_BIT | a, aux, sm.ep.gu[w][lo], seen, &oldk)) {
-            track_min(sm, nk);
-            push = true;
-            big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
-          } else {
-            push = big = is_new;
-          }
-        } else {
-          push = big = is_new;  // discovery only: successors are discovered next pass
-        }
-        if (!push) continue;
-        if (big) sm.pc_big[q] = 1;
-        bool first;
-        if (is_new) {  // this thread created the slot: first to touch its stamp
-          ed->stamp = epoch;
-          first = true;
-        } else {
-          first = atomicExch(&ed->stamp, epoch) != epoch;
-        }
-        if (first) {
-          int p;
-          uint2* dst;
-          if (big) {  // one counter per coalesced group
-            p = agg_alloc(&ctr_out[0], nullptr);
-            dst = nxt;
-          } else {
-            p = agg_alloc(&ctr_out[1], nullptr);
-            dst = tiny;
-          }
-          if ((uint32_t)p < L.seg) dst[p] = item;
-          else atomicMax(&sm.status_l, CTW_GROW_TABLE);
-        }
+        eps_arc(sm, L, g, boost, relax_eps, epoch, q, ctr_out, nxt, tiny, w, lo, o, a, arc);
       }
       __syncwarp();
     }
@@ -1042,11 +1053,11 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
 // Relax one emitting arc: ((c + (-scale * ll)) + w) (+ boost), then
 // find-or-insert the destination and install the candidate if it wins
 // (_kernel.pyx:243-287).
-__device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
-                                         const double* nll_s, bool smem_ll, long long row0, double neg_scale,
-                                         const double* boost, uint32_t arc_i, double cost, uint32_t src_idx) {
+__device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
+                                                const double* nll_s, bool smem_ll, long long row0, double neg_scale,
+                                                const double* boost, uint32_t arc_i, double cost, uint32_t src_idx,
+                                                const CtwArc& arc) {
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
-  const CtwArc arc = g.arcs[arc_i];
   double ac;
   if (smem_ll) ac = nll_s[arc.ilabel - 1];
   else {
@@ -1076,6 +1087,13 @@ __device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const Graph
   unsigned long long oldk;
   const unsigned long long nk = d2key(nc);
   if (tok_relax_from(L, ed, nk, arc_i, src_idx, 0ULL, seen, &oldk)) track_min(sm, nk);
+}
+
+__device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
+                                         const double* nll_s, bool smem_ll, long long row0, double neg_scale,
+                                         const double* boost, uint32_t arc_i, double cost, uint32_t src_idx) {
+  const CtwArc arc = g.arcs[arc_i];
+  emit_arc_loaded(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, arc_i, cost, src_idx, arc);
 }
 
 __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
