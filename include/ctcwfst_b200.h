@@ -74,6 +74,33 @@ typedef struct {
   int64_t n_chain;
 } ctw_export;
 
+/* Pruned lattice of one decoded lane (ctw_lane_lattice).
+ * Nodes: seeds 0..n_seeds-1 (the start closure), then n_seeds + record index.
+ * Arrays are malloc'd by the library and released by ctw_lattice_free. */
+typedef struct {
+  int32_t status;      /* 0 ok; 1/2 buffers (internal); 3 closure overflow; 4 no complete path */
+  int32_t final_mode;  /* 1: the last layer holds final states (their weights end paths) */
+  int32_t frame_count;
+  double best;         /* best complete path cost (== best_path's total_cost) */
+  double lattice_beam;
+  int64_t n_seeds;
+  int32_t* seed_state;
+  double* seed_cost;
+  int64_t* seed_lab_off; /* [n_seeds + 1] pending output labels of each seed */
+  int32_t* seed_lab;
+  int64_t n_arcs;
+  int32_t* arc_src;
+  int32_t* arc_dst;
+  int32_t* arc_frame;     /* layer of dst */
+  int32_t* arc_src_state;
+  int32_t* arc_dst_state;
+  double* arc_w;
+  double* arc_dst_final;  /* final weight of dst when arc_frame is the last layer, else +inf */
+  int64_t* arc_lab_off;   /* [n_arcs + 1] */
+  int32_t* arc_lab;
+  int64_t closure_items, closure_pruned;
+} ctw_lattice;
+
 int ctw_abi_version(void);
 const char* ctw_last_error(void);
 int ctw_device_count(void);
@@ -140,6 +167,24 @@ int ctw_lane_info(ctw_lanes* l, int32_t lane, int64_t* frame_count, int64_t* n_t
 int ctw_lane_export(ctw_lanes* l, int32_t lane, int64_t frame_from, int64_t base, const int64_t* ext_bp,
                     int64_t n_ext, ctw_export* out);
 void ctw_export_free(ctw_export* e);
+
+/* Lattice generation + pruning for lanes that have decoded a whole
+ * utterance (no reference counterpart: SPEC.md:312).
+ * `loglik` / `ll_offsets` / `width` / `dtype` / `location` address the same
+ * log-likelihood rows the lanes were advanced over (frame 0 .. frame_count-1
+ * contiguous per lane). out[i] receives lane i's pruned lattice: arcs with
+ * alpha(src) + w + beta(dst) <= best + lattice_beam. */
+int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                int32_t location, const int64_t* ll_offsets, int32_t width, double lattice_beam,
+                ctw_lattice* out);
+void ctw_lattice_free(ctw_lattice* lat);
+
+/* n lowest-cost DISTINCT word sequences of a lattice (A* over the kept arcs
+ * with exact remaining costs; at most max_pops partial paths expanded).
+ * words[word_off[k] .. word_off[k+1]) and costs[k] for k < *n_found; returns
+ * -2 when words_cap is too small (word_off[n] then holds the need). */
+int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32_t* words, int64_t words_cap,
+                      int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops);
 
 /* Counters since creation (or the last reset): all kernel launches, launches
  * of the frame kernel and their total device milliseconds (CUDA events on the

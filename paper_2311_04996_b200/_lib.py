@@ -39,6 +39,20 @@ class CtwExport(C.Structure):
     ]
 
 
+class CtwLattice(C.Structure):
+    """ctw_lattice (include/ctcwfst_b200.h)."""
+    _fields_ = [
+        ("status", I32), ("final_mode", I32), ("frame_count", I32), ("best", F64), ("lattice_beam", F64),
+        ("n_seeds", I64), ("seed_state", C.POINTER(I32)), ("seed_cost", C.POINTER(F64)),
+        ("seed_lab_off", C.POINTER(I64)), ("seed_lab", C.POINTER(I32)),
+        ("n_arcs", I64), ("arc_src", C.POINTER(I32)), ("arc_dst", C.POINTER(I32)),
+        ("arc_frame", C.POINTER(I32)), ("arc_src_state", C.POINTER(I32)), ("arc_dst_state", C.POINTER(I32)),
+        ("arc_w", C.POINTER(F64)),
+        ("arc_dst_final", C.POINTER(F64)), ("arc_lab_off", C.POINTER(I64)), ("arc_lab", C.POINTER(I32)),
+        ("closure_items", I64), ("closure_pruned", I64),
+    ]
+
+
 _SIGS = {
     "ctw_abi_version": (I32, []),
     "ctw_last_error": (C.c_char_p, []),
@@ -62,6 +76,9 @@ _SIGS = {
     "ctw_lanes_profile": (I32, [P, P]),
     "ctw_lanes_host_timing": (I32, [P, P]),
     "ctw_lanes_stream": (P, [P]),
+    "ctw_lane_lattice": (I32, [P, P, I32, P, I32, I32, P, I32, F64, P]),
+    "ctw_lattice_free": (None, [C.POINTER(CtwLattice)]),
+    "ctw_lattice_nbest": (I32, [C.POINTER(CtwLattice), I32, I64, P, I64, P, P, C.POINTER(I32), C.POINTER(I64)]),
     "ctw_advance_chunk_compat": (I32, [P] * 6 + [I64, I64] + [P] * 5 + [I64, P, I64, I64, F64, F64,
                                       I64, F64, I64, P, I64, I64, I32, C.POINTER(I64),
                                       C.POINTER(CtwExport)]),

@@ -36,6 +36,8 @@ extern "C" int ctw_launch_best(const CtwLane*, const CtwStateRange*, const CtwAr
                                const double*, const int*, int, int32_t*, const long long*, const int*,
                                int*, double*, int*, cudaStream_t);
 extern "C" int ctw_launch_clear(CtwTok*, uint32_t, cudaStream_t);
+extern "C" int ctw_launch_lattice(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
+                                  CtwLatEntry*, int, const void*, int, int, double, double, cudaStream_t);
 
 namespace {
 
@@ -124,6 +126,10 @@ struct ctw_lanes {
   std::vector<int64_t> ptab_cap;
   std::vector<CtwRecPage*> free_pages;
   std::vector<CtwRecPage*> slabs;  // page allocations (CTW_SLAB pages each)
+  // seed tokens of each lane's current utterance (the lattice's first layer)
+  std::vector<CtwSrc*> seed_src;
+  std::vector<int32_t*> seed_pend;
+  std::vector<int32_t> seed_n, seed_cap;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   // scratch
@@ -368,6 +374,10 @@ int reserve_lanes(ctw_lanes* l, int n) {
   }
   l->hpages.resize(n);
   l->ptab_cap.resize(n, 0);
+  l->seed_src.resize(n, nullptr);
+  l->seed_pend.resize(n, nullptr);
+  l->seed_n.resize(n, 0);
+  l->seed_cap.resize(n, 0);
   for (int i = l->n; i < n; ++i) {
     if (int r = init_lane(l, i)) return r;
   }
@@ -409,6 +419,31 @@ int check_ids(ctw_lanes* l, const int32_t* ids, int n) {
     if (seen[ids[i]]) return fail(-1, "duplicate lane id in one batch");
     seen[ids[i]] = 1;
   }
+  return 0;
+}
+
+// Device view of log-likelihood rows: device buffers pass through; host rows
+// are staged into HBM with one copy covering every lane's span.
+int stage_rows(ctw_lanes* l, const void* loglik, int32_t location, size_t esz, const int64_t* ll_offsets,
+               const int32_t* frames, int n, int32_t width, const char** dev_ll) {
+  *dev_ll = (const char*)loglik;
+  if (location != 0) return 0;
+  int64_t lo = INT64_MAX, hi = 0;
+  for (int i = 0; i < n; ++i) {
+    if (frames[i] == 0) continue;
+    lo = std::min<int64_t>(lo, ll_offsets[i]);
+    hi = std::max<int64_t>(hi, ll_offsets[i] + (int64_t)frames[i] * width);
+  }
+  if (lo == INT64_MAX) lo = hi = 0;
+  const size_t bytes = (size_t)(hi - lo) * esz;
+  if (bytes > l->stage_bytes) {
+    dfree(l->d_stage);
+    CUDA_TRY(dalloc(&l->d_stage, bytes + bytes / 4));
+    l->stage_bytes = bytes + bytes / 4;
+  }
+  if (bytes)
+    CUDA_TRY(cudaMemcpyAsync(l->d_stage, (const char*)loglik + lo * esz, bytes, cudaMemcpyHostToDevice, l->stream));
+  *dev_ll = l->d_stage - lo * (int64_t)esz;
   return 0;
 }
 
@@ -615,6 +650,8 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   for (int i = 0; i < l->n; ++i) {
     free_lane(l->h[i], l->stream);
     dfree(l->boost_buf[i]);
+    sfree(l->seed_src[i], l->stream);
+    sfree(l->seed_pend[i], l->stream);
   }
   for (CtwRecPage* p : l->slabs) sfree(p, l->stream);
   cudaStreamSynchronize(l->stream);
@@ -690,6 +727,25 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
   for (int i = 0; i < n; ++i) {
     status[i] = st[i];
     l->seeded[ids[i]] = st[i] == CTW_OK;
+    if (st[i] != CTW_OK) continue;
+    // keep the seed tokens (device copy, stream-ordered) for lattices
+    const int lane = ids[i];
+    const CtwLane& L = l->h[lane];
+    if (L.n_src > l->seed_cap[lane]) {
+      sfree(l->seed_src[lane], l->stream);
+      sfree(l->seed_pend[lane], l->stream);
+      const int32_t c = std::max<int32_t>(L.n_src, 64);
+      CUDA_TRY(salloc(&l->seed_src[lane], (size_t)c, l->stream));
+      CUDA_TRY(salloc(&l->seed_pend[lane], (size_t)c, l->stream));
+      l->seed_cap[lane] = c;
+    }
+    l->seed_n[lane] = L.n_src;
+    if (L.n_src) {
+      CUDA_TRY(cudaMemcpyAsync(l->seed_src[lane], L.src[L.src_buf], (size_t)L.n_src * sizeof(CtwSrc),
+                               cudaMemcpyDeviceToDevice, l->stream));
+      CUDA_TRY(cudaMemcpyAsync(l->seed_pend[lane], L.pend, (size_t)L.n_src * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice, l->stream));
+    }
   }
   return 0;
 }
@@ -741,27 +797,9 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     if (frames[i] < 0) return fail(-1, "negative frame count");
   }
   // stage host rows into HBM (one copy when the chunks are contiguous)
-  const char* dev_ll = (const char*)loglik;
+  const char* dev_ll = nullptr;
   if (int r = ensure_scratch(l, n)) return r;
-  if (location == 0) {
-    int64_t lo = INT64_MAX, hi = 0;
-    for (int i = 0; i < n; ++i) {
-      if (frames[i] == 0) continue;
-      lo = std::min<int64_t>(lo, ll_offsets[i]);
-      hi = std::max<int64_t>(hi, ll_offsets[i] + (int64_t)frames[i] * width);
-    }
-    if (lo == INT64_MAX) lo = hi = 0;
-    const size_t bytes = (size_t)(hi - lo) * esz;
-    if (bytes > l->stage_bytes) {
-      dfree(l->d_stage);
-      CUDA_TRY(dalloc(&l->d_stage, bytes + bytes / 4));
-      l->stage_bytes = bytes + bytes / 4;
-    }
-    if (bytes)
-      CUDA_TRY(cudaMemcpyAsync(l->d_stage, (const char*)loglik + lo * esz, bytes, cudaMemcpyHostToDevice,
-                               l->stream));
-    dev_ll = l->d_stage - lo * (int64_t)esz;
-  }
+  if (int r = stage_rows(l, loglik, location, esz, ll_offsets, frames, n, width, &dev_ll)) return r;
   const clk::time_point t1 = clk::now();
   l->h_stage += secs(t0, t1);
   // pre-size per-lane frame / history capacity
@@ -1282,6 +1320,312 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
   L.n_rec = 0;
   L.frame_count = 0;
   return st;
+}
+
+
+// ---------------------------------------------------------------- lattice --
+
+void ctw_lattice_free(ctw_lattice* lat) {
+  if (!lat) return;
+  for (void* p : {(void*)lat->seed_state, (void*)lat->seed_cost, (void*)lat->seed_lab_off, (void*)lat->seed_lab,
+                  (void*)lat->arc_src, (void*)lat->arc_dst, (void*)lat->arc_frame, (void*)lat->arc_dst_state,
+                  (void*)lat->arc_src_state,
+                  (void*)lat->arc_w, (void*)lat->arc_dst_final, (void*)lat->arc_lab_off, (void*)lat->arc_lab})
+    free(p);
+  std::memset(lat, 0, sizeof(*lat));
+}
+
+int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                int32_t location, const int64_t* ll_offsets, int32_t width, double lattice_beam,
+                ctw_lattice* out) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  ctw_graph* g = l->g;
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n <= 0) return 0;
+  if (int r = check_ids(l, lane_ids, n)) return r;
+  if (dtype != 0 && dtype != 1) return fail(-1, "dtype must be 0 (f32) or 1 (f64)");
+  if (!(lattice_beam >= 0)) return fail(-1, "lattice_beam must be >= 0");
+  for (int i = 0; i < n; ++i) {
+    std::memset(&out[i], 0, sizeof(out[i]));
+    if (!l->seeded[lane_ids[i]]) return fail(-1, "lane not seeded (call ctw_lane_reset first)");
+  }
+  const size_t esz = dtype ? 8 : 4;
+  std::vector<int32_t> frames(n);
+  for (int i = 0; i < n; ++i) frames[i] = l->h[lane_ids[i]].frame_count;
+  const char* dev_ll = nullptr;
+  if (int r = stage_rows(l, loglik, location, esz, ll_offsets, frames.data(), n, width, &dev_ll)) return r;
+  // per-entry buffers; arc / label capacities grow and the lane re-runs on overflow
+  std::vector<CtwLatEntry> ent(n);
+  std::vector<int32_t> arc_cap(n), lab_cap(n);
+  for (int i = 0; i < n; ++i) {
+    arc_cap[i] = 1024 + 64 * frames[i];
+    lab_cap[i] = 4 * arc_cap[i];
+  }
+  CtwLatEntry* d_ent = nullptr;
+  CUDA_TRY(salloc(&d_ent, (size_t)n, l->stream));
+  std::vector<int> todo(n);
+  std::iota(todo.begin(), todo.end(), 0);
+  std::vector<CtwLatArc*> d_arcs(n, nullptr);
+  std::vector<int32_t*> d_lab(n, nullptr);
+  std::vector<unsigned long long*> d_beta(n, nullptr);
+  auto release = [&]() {
+    for (int i = 0; i < n; ++i) {
+      sfree(d_arcs[i], l->stream);
+      sfree(d_lab[i], l->stream);
+      sfree(d_beta[i], l->stream);
+    }
+    sfree(d_ent, l->stream);
+  };
+  for (int round = 0; !todo.empty(); ++round) {
+    if (round > 6) {
+      release();
+      return fail(-1, "lattice: buffer growth did not converge");
+    }
+    const int m = (int)todo.size();
+    for (int k = 0; k < m; ++k) {
+      const int i = todo[k];
+      const int lane = lane_ids[i];
+      const CtwLane& L = l->h[lane];
+      sfree(d_arcs[i], l->stream);
+      sfree(d_lab[i], l->stream);
+      if (!d_beta[i]) CUDA_TRY(salloc(&d_beta[i], (size_t)(l->seed_n[lane] + L.n_rec + 1), l->stream));
+      CUDA_TRY(salloc(&d_arcs[i], (size_t)arc_cap[i], l->stream));
+      CUDA_TRY(salloc(&d_lab[i], (size_t)lab_cap[i], l->stream));
+      CtwLatEntry e{};
+      e.lane = lane;
+      e.n_seeds = l->seed_n[lane];
+      e.seeds = l->seed_src[lane];
+      e.ll_off = (long long)ll_offsets[i];
+      e.arcs = d_arcs[i];
+      e.arc_cap = arc_cap[i];
+      e.lpool = d_lab[i];
+      e.lpool_cap = lab_cap[i];
+      e.beta = d_beta[i];
+      ent[k] = e;
+    }
+    CUDA_TRY(cudaMemcpyAsync(d_ent, ent.data(), m * sizeof(CtwLatEntry), cudaMemcpyHostToDevice, l->stream));
+    if (ctw_launch_lattice(l->d, g->ranges, g->arcs, g->olabel, g->final_w, d_ent, m, dev_ll, dtype, width,
+                           l->cfg.acoustic_scale, lattice_beam, l->stream)) {
+      release();
+      return fail(-1, std::string("lattice launch: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+    l->launches++;
+    CUDA_TRY(cudaMemcpyAsync(ent.data(), d_ent, m * sizeof(CtwLatEntry), cudaMemcpyDeviceToHost, l->stream));
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    std::vector<int> again;
+    for (int k = 0; k < m; ++k) {
+      const int i = todo[k];
+      const CtwLatEntry& e = ent[k];
+      if (e.status == 1 || e.status == 2) {
+        arc_cap[i] = std::max<int32_t>(4 * arc_cap[i], e.n_arcs + 1024);
+        lab_cap[i] = std::max<int32_t>(4 * lab_cap[i], e.lpool_used + 4096);
+        again.push_back(i);
+        continue;
+      }
+      // ---- host copy of the kept lattice
+      const int lane = lane_ids[i];
+      const CtwLane& L = l->h[lane];
+      ctw_lattice& o = out[i];
+      o.status = e.status;
+      o.final_mode = e.final_mode;
+      o.frame_count = L.frame_count;
+      o.best = e.best;
+      o.lattice_beam = lattice_beam;
+      o.closure_items = e.closure_items;
+      o.closure_pruned = e.closure_pruned;
+      std::vector<CtwLatArc> arcs((size_t)e.n_arcs);
+      std::vector<int32_t> lab((size_t)e.lpool_used);
+      const int ns = l->seed_n[lane];
+      std::vector<CtwSrc> seeds((size_t)ns);
+      std::vector<int32_t> spend((size_t)ns), pool((size_t)L.pool_used);
+      if (e.n_arcs)
+        CUDA_TRY(cudaMemcpyAsync(arcs.data(), d_arcs[i], arcs.size() * sizeof(CtwLatArc), cudaMemcpyDeviceToHost,
+                                 l->stream));
+      if (e.lpool_used)
+        CUDA_TRY(cudaMemcpyAsync(lab.data(), d_lab[i], lab.size() * 4, cudaMemcpyDeviceToHost, l->stream));
+      if (ns) {
+        CUDA_TRY(cudaMemcpyAsync(seeds.data(), l->seed_src[lane], ns * sizeof(CtwSrc), cudaMemcpyDeviceToHost,
+                                 l->stream));
+        CUDA_TRY(cudaMemcpyAsync(spend.data(), l->seed_pend[lane], ns * 4, cudaMemcpyDeviceToHost, l->stream));
+      }
+      if (L.pool_used)
+        CUDA_TRY(cudaMemcpyAsync(pool.data(), L.pool, pool.size() * 4, cudaMemcpyDeviceToHost, l->stream));
+      CUDA_TRY(cudaStreamSynchronize(l->stream));
+      o.n_seeds = ns;
+      o.seed_state = cmalloc<int32_t>(ns);
+      o.seed_cost = cmalloc<double>(ns);
+      o.seed_lab_off = cmalloc<int64_t>(ns + 1);
+      std::vector<int32_t> sl;
+      o.seed_lab_off[0] = 0;
+      for (int k2 = 0; k2 < ns; ++k2) {
+        o.seed_state[k2] = seeds[k2].state;
+        o.seed_cost[k2] = seeds[k2].cost;
+        expand_code(pool, spend[k2], sl);
+        o.seed_lab_off[k2 + 1] = (int64_t)sl.size();
+      }
+      o.seed_lab = cmalloc<int32_t>(sl.size());
+      std::copy(sl.begin(), sl.end(), o.seed_lab);
+      const int64_t na = e.n_arcs;
+      o.n_arcs = na;
+      o.arc_src = cmalloc<int32_t>(na);
+      o.arc_dst = cmalloc<int32_t>(na);
+      o.arc_frame = cmalloc<int32_t>(na);
+      o.arc_dst_state = cmalloc<int32_t>(na);
+      o.arc_src_state = cmalloc<int32_t>(na);
+      o.arc_w = cmalloc<double>(na);
+      o.arc_dst_final = cmalloc<double>(na);
+      o.arc_lab_off = cmalloc<int64_t>(na + 1);
+      // canonical order: by (frame, src, dst, w) so results do not depend on
+      // the kernel's append order
+      std::vector<int64_t> ord((size_t)na);
+      std::iota(ord.begin(), ord.end(), 0);
+      std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+        const CtwLatArc &a = arcs[x], &b = arcs[y];
+        if (a.frame != b.frame) return a.frame < b.frame;
+        if (a.src != b.src) return a.src < b.src;
+        if (a.dst != b.dst) return a.dst < b.dst;
+        return a.w < b.w;
+      });
+      std::vector<int32_t> al;
+      o.arc_lab_off[0] = 0;
+      const double INF = HUGE_VAL;
+      const int T = L.frame_count;
+      for (int64_t k2 = 0; k2 < na; ++k2) {
+        const CtwLatArc& a = arcs[ord[k2]];
+        o.arc_src[k2] = a.src;
+        o.arc_dst[k2] = a.dst;
+        o.arc_frame[k2] = a.frame;
+        o.arc_dst_state[k2] = a.dst_state;
+        o.arc_src_state[k2] = a.src_state;
+        o.arc_w[k2] = a.w;
+        double fw = INF;
+        if (a.frame == T - 1) fw = e.final_mode ? g->h_final[a.dst_state] : 0.0;
+        o.arc_dst_final[k2] = fw;
+        if (a.code > 0) al.push_back(a.code);
+        else if (a.code < 0) {
+          const int64_t off = -(int64_t)a.code - 1;
+          for (int32_t j = 0; j < lab[off]; ++j) al.push_back(lab[off + 1 + j]);
+        }
+        o.arc_lab_off[k2 + 1] = (int64_t)al.size();
+      }
+      o.arc_lab = cmalloc<int32_t>(al.size());
+      std::copy(al.begin(), al.end(), o.arc_lab);
+    }
+    todo.swap(again);
+  }
+  release();
+  return 0;
+}
+
+int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32_t* words, int64_t words_cap,
+                      int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops) {
+  *n_found = 0;
+  if (pops) *pops = 0;
+  word_off[0] = 0;
+  if (n <= 0 || lat->status == 4) return 0;
+  const double INF = HUGE_VAL;
+  const int64_t na = lat->n_arcs, ns = lat->n_seeds;
+  // node ids -> dense indices
+  std::vector<int32_t> ids;
+  ids.reserve((size_t)(2 * na + ns));
+  for (int64_t k = 0; k < ns; ++k) ids.push_back((int32_t)k);
+  for (int64_t k = 0; k < na; ++k) {
+    ids.push_back(lat->arc_src[k]);
+    ids.push_back(lat->arc_dst[k]);
+  }
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  auto idx = [&](int32_t node) { return (int)(std::lower_bound(ids.begin(), ids.end(), node) - ids.begin()); };
+  const int nn = (int)ids.size();
+  std::vector<double> fin((size_t)nn, INF), beta((size_t)nn, INF);
+  std::vector<int> out_off((size_t)nn + 1, 0);
+  std::vector<int> asrc((size_t)na), adst((size_t)na);
+  for (int64_t k = 0; k < na; ++k) {
+    asrc[k] = idx(lat->arc_src[k]);
+    adst[k] = idx(lat->arc_dst[k]);
+    out_off[asrc[k] + 1]++;
+    if (lat->arc_dst_final[k] < fin[adst[k]]) fin[adst[k]] = lat->arc_dst_final[k];
+  }
+  for (int v = 0; v < nn; ++v) out_off[v + 1] += out_off[v];
+  std::vector<int> adj((size_t)na);
+  {
+    std::vector<int> fill(out_off.begin(), out_off.end() - 1);
+    for (int64_t k = 0; k < na; ++k) adj[fill[asrc[k]]++] = (int)k;
+  }
+  // exact remaining cost over the kept arcs (layers backwards: arcs are
+  // sorted by frame)
+  for (int v = 0; v < nn; ++v) beta[v] = fin[v];
+  for (int64_t k = na - 1; k >= 0; --k) {
+    const double c = lat->arc_w[k] + beta[adst[k]];
+    if (c < beta[asrc[k]]) beta[asrc[k]] = c;
+  }
+  // A*: partial paths in a persistent tree; priority = g + beta (exact)
+  struct P {
+    int parent;
+    int node;
+    int arc;
+    double g;
+  };
+  std::vector<P> tree;
+  typedef std::pair<double, int> QE;
+  std::vector<QE> heap;
+  auto push = [&](const P& p) {
+    tree.push_back(p);
+    heap.push_back(QE(p.g + beta[p.node], (int)tree.size() - 1));
+    std::push_heap(heap.begin(), heap.end(), std::greater<QE>());
+  };
+  for (int64_t k = 0; k < ns; ++k) {
+    const int v = idx((int32_t)k);
+    if (beta[v] < INF) push(P{-1, v, -1, lat->seed_cost[k]});
+  }
+  std::vector<std::vector<int32_t>> seen;
+  std::vector<double> found_cost;
+  int64_t npop = 0;
+  while (!heap.empty() && (int)found_cost.size() < n && npop < max_pops) {
+    std::pop_heap(heap.begin(), heap.end(), std::greater<QE>());
+    const QE top = heap.back();
+    heap.pop_back();
+    ++npop;
+    const P cur = tree[top.second];
+    if (fin[cur.node] < INF && out_off[cur.node] == out_off[cur.node + 1] && cur.arc >= 0) {
+      // complete path: words = seed labels + arc labels, oldest first
+      std::vector<int> arcs_rev;
+      int t = top.second, seed_node = -1;
+      while (t >= 0) {
+        if (tree[t].arc >= 0) arcs_rev.push_back(tree[t].arc);
+        else seed_node = ids[tree[t].node];
+        t = tree[t].parent;
+      }
+      std::vector<int32_t> w;
+      for (int64_t j = lat->seed_lab_off[seed_node]; j < lat->seed_lab_off[seed_node + 1]; ++j)
+        w.push_back(lat->seed_lab[j]);
+      for (auto it = arcs_rev.rbegin(); it != arcs_rev.rend(); ++it)
+        for (int64_t j = lat->arc_lab_off[*it]; j < lat->arc_lab_off[*it + 1]; ++j) w.push_back(lat->arc_lab[j]);
+      if (std::find(seen.begin(), seen.end(), w) == seen.end()) {
+        seen.push_back(w);
+        found_cost.push_back(cur.g + fin[cur.node]);
+      }
+      continue;
+    }
+    for (int q = out_off[cur.node]; q < out_off[cur.node + 1]; ++q) {
+      const int k = adj[q];
+      if (beta[adst[k]] < INF) push(P{top.second, adst[k], k, cur.g + lat->arc_w[k]});
+    }
+  }
+  if (pops) *pops = npop;
+  int64_t need = 0;
+  for (auto& w : seen) need += (int64_t)w.size();
+  *n_found = (int32_t)seen.size();
+  int64_t pos = 0;
+  for (size_t k = 0; k < seen.size(); ++k) {
+    costs[k] = found_cost[k];
+    word_off[k] = pos;
+    if (pos + (int64_t)seen[k].size() <= words_cap)
+      std::copy(seen[k].begin(), seen[k].end(), words + pos);
+    pos += (int64_t)seen[k].size();
+  }
+  word_off[seen.size()] = pos;
+  return need > words_cap ? -2 : 0;
 }
 
 }  // extern "C"

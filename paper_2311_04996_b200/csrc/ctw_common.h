@@ -158,3 +158,36 @@ struct CtwDecodeCfg {
   long long max_active;
   long long max_ne_iters;
 };
+
+// ------------------------------------------------------------- lattice ----
+
+// One kept lattice arc (ctw_lattice.cu): nodes are numbered seeds first
+// (0 .. n_seeds-1), then n_seeds + record index.
+struct CtwLatArc {
+  int32_t src, dst;
+  double w;       // emitting arc + epsilon continuation cost (reference operation order)
+  int32_t code;   // output labels: 0 none, > 0 one label, < 0 segment -(off+1) [n, l1..ln] of the lattice pool
+  int32_t frame;  // layer of dst
+  int32_t dst_state;
+  int32_t src_state;
+};
+
+// Per batch entry (lane) arguments and outputs, device pointers.
+struct CtwLatEntry {
+  int32_t lane;
+  int32_t n_seeds;
+  const CtwSrc* seeds;        // seed tokens (state, cost)
+  long long ll_off;           // element offset of frame 0 in the log-likelihood buffer
+  CtwLatArc* arcs;            // kept arcs
+  int32_t arc_cap;
+  int32_t* lpool;             // label segments [n, l1..ln]
+  int32_t lpool_cap;
+  unsigned long long* beta;   // per node (seeds first, then records): sortable key
+  // outputs
+  int32_t n_arcs, lpool_used;
+  int32_t status;             // 0 ok, 1 arc buffer full, 2 label pool full, 3 closure overflow, 4 no final path
+  int32_t final_mode;         // 1 = final states present at the last layer
+  double best;                // best complete path cost (alpha + final)
+  long long closure_items, closure_pruned;  // diagnostics
+};
+

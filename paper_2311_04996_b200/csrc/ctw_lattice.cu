@@ -1,0 +1,361 @@
+// ctw_lattice.cu -- lattice generation and lattice pruning on the device
+// (the reference has no lattice).
+//
+// Definition. After a lane has decoded an utterance,
+// its lattice nodes are the seed tokens (layer -1: the start state's epsilon
+// closure, decoder.py:173-229) and the per-frame records (layer f: the
+// survivors of frame f, _kernel.pyx:392-427). Between consecutive layers
+// there is one lattice arc for every (source node s in layer f-1, emitting
+// arc e leaving state(s), destination node d in layer f) such that some path
+// e, eps, eps, ... leads from state(s) to state(d); its weight is the minimum
+// over those epsilon continuations of
+//     (-scale * ll[f, il(e) - 1]) + w(e) (+ boost[ol(e)]) + sum (w + boost)
+// with the reference's operation order (_kernel.pyx:249-253, :307-310), and
+// its output labels are those of the minimising path. alpha(node) is the
+// node's decoder cost; beta(node) the minimum over complete continuations
+// (final weight at the last layer: final states if any survive, else 0 --
+// the best_path rule of decoder.py:384-400). An arc is kept iff
+// alpha(s) + w + beta(d) <= best + lattice_beam.
+//
+// The kernel walks the layers backwards so beta is known when a layer's
+// arcs are generated and pruning happens as arcs are produced (a full
+// unpruned lattice would be ~10^7 arcs per utterance). One CTA per lane:
+// per layer, the surviving destination nodes go into the lane's (empty)
+// token table as a state -> node map, every (source, emitting arc) pair is a
+// work item that runs its own small epsilon closure, and kept arcs are
+// appended to the lane's arc buffer.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ctw_common.h"
+
+#define LAT_BS 256
+#define LAT_CL 48       // local epsilon-closure capacity per work item
+#define LAT_QL 128      // local relaxation budget per work item
+
+namespace {
+
+struct LatGraph {
+  const CtwStateRange* ranges;
+  const CtwArc* arcs;
+  const int32_t* olabel;
+  const double* final_w;
+};
+
+__device__ __forceinline__ unsigned long long lat_d2key(double x) {
+  x = __dadd_rn(x, 0.0);
+  long long b = __double_as_longlong(x);
+  return (unsigned long long)(b ^ ((b >> 63) | (long long)0x8000000000000000ULL));
+}
+
+__device__ __forceinline__ double lat_key2d(unsigned long long k) {
+  long long b = (k & 0x8000000000000000ULL) ? (long long)(k ^ 0x8000000000000000ULL) : (long long)~k;
+  return __longlong_as_double(b);
+}
+
+__device__ __forceinline__ uint32_t lat_hash(uint32_t s, uint32_t shift) { return (s * 0x9E3779B1u) >> shift; }
+
+}  // namespace
+
+namespace {
+
+struct LatArgs {
+  CtwLane* lanes;
+  LatGraph g;
+  CtwLatEntry* ent;
+  const void* loglik;
+  int width;
+  int is_f64;
+  double acoustic_scale;
+  double lattice_beam;
+};
+
+__device__ __forceinline__ void lat_rec(const CtwLane& lane, long long r, int32_t* state, double* cost) {
+  const CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
+  const int o = (int)(r & (CTW_PAGE - 1));
+  *state = pg->state[o];
+  *cost = pg->cost[o];
+}
+
+// Insert state -> node into the (empty) lane table; the node id rides in tb.
+// Returns the table index.
+__device__ __forceinline__ uint32_t lat_put(const CtwLane& lane, uint32_t shift, uint32_t mask, uint32_t s,
+                                            uint32_t node) {
+  uint32_t h = lat_hash(s, shift);
+  for (uint32_t p = 0; p <= mask; ++p) {
+    const uint32_t old = atomicCAS(&lane.table[h].state, CTW_EMPTY, s);
+    if (old == CTW_EMPTY || old == s) {
+      lane.table[h].tb = node;
+      return h;
+    }
+    h = (h + 1) & mask;
+  }
+  return CTW_EMPTY;
+}
+
+__device__ __forceinline__ int lat_get(const CtwLane& lane, uint32_t shift, uint32_t mask, uint32_t s) {
+  uint32_t h = lat_hash(s, shift);
+  for (uint32_t p = 0; p <= mask; ++p) {
+    const uint32_t k = __ldcg(&lane.table[h].state);
+    if (k == s) return (int)__ldcg(&lane.table[h].tb);
+    if (k == CTW_EMPTY) return -1;
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
+struct __align__(16) LatSmem {
+  int n_arcs, lpool_used, status, nput;
+  unsigned long long min_beta;
+  unsigned long long best;
+  int final_mode;
+  int deg_tot;
+  unsigned long long items, pruned;
+};
+
+__global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
+  __shared__ LatSmem sm;
+  const int tid = threadIdx.x;
+  CtwLatEntry& E = a.ent[blockIdx.x];
+  const CtwLane& lane = a.lanes[E.lane];
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const uint32_t tlog2 = lane.tlog2;
+  const uint32_t mask = (1u << tlog2) - 1, shift = 32 - tlog2;
+  const int T = lane.frame_count;
+  const long long R = lane.n_rec;
+  const int S0 = E.n_seeds;
+  const double neg_scale = -a.acoustic_scale;
+  const double* boost = lane.boost;
+  if (tid == 0) {
+    sm.n_arcs = 0;
+    sm.lpool_used = 0;
+    sm.status = 0;
+    sm.best = ~0ULL;
+    sm.final_mode = 0;
+    sm.items = 0;
+    sm.pruned = 0;
+  }
+  for (long long i = tid; i < S0 + R; i += LAT_BS) E.beta[i] = ~0ULL;
+  __syncthreads();
+  if (T == 0) {
+    if (tid == 0) E.status = 4;
+    return;
+  }
+  // ---- last layer: beta = final weight (final states if any survive, else 0)
+  const long long lf0 = lane.frame_base[T - 1], lf1 = R;
+  for (long long r = lf0 + tid; r < lf1; r += LAT_BS) {
+    int32_t st;
+    double c;
+    lat_rec(lane, r, &st, &c);
+    if (a.g.final_w[st] != INF) sm.final_mode = 1;  // benign race: all writers store 1
+  }
+  __syncthreads();
+  const bool fm = sm.final_mode != 0;
+  for (long long r = lf0 + tid; r < lf1; r += LAT_BS) {
+    int32_t st;
+    double c;
+    lat_rec(lane, r, &st, &c);
+    const double fw = fm ? a.g.final_w[st] : 0.0;
+    if (fm && fw == INF) continue;
+    E.beta[S0 + r] = lat_d2key(fw);
+    atomicMin(&sm.best, lat_d2key(c + fw));
+  }
+  __syncthreads();
+  const double best = lat_key2d(sm.best);
+  const double cutoff = __dadd_rn(best, a.lattice_beam);
+  const bool cut_ok = lane.prune_ok != 0;  // epsilon continuations never lower a cost
+
+  for (int f = T - 1; f >= 0; --f) {
+    const long long d0 = lane.frame_base[f], d1 = (f + 1 < T) ? lane.frame_base[f + 1] : R;
+    // ---- destination map: nodes of layer f that can lie on a kept path
+    if (tid == 0) {
+      sm.min_beta = ~0ULL;
+      sm.nput = 0;
+    }
+    __syncthreads();
+    for (long long r = d0 + tid; r < d1; r += LAT_BS) {
+      const unsigned long long bk = E.beta[S0 + r];
+      if (bk == ~0ULL) continue;
+      int32_t st;
+      double c;
+      lat_rec(lane, r, &st, &c);
+      if (c + lat_key2d(bk) > cutoff) continue;
+      const uint32_t h = lat_put(lane, shift, mask, (uint32_t)st, (uint32_t)(S0 + r));
+      if (h != CTW_EMPTY) lane.slots[atomicAdd(&sm.nput, 1)] = make_uint2(h, (uint32_t)st);  // for the clear
+      atomicMin(&sm.min_beta, bk);
+    }
+    __syncthreads();
+    const double min_beta = sm.min_beta == ~0ULL ? INF : lat_key2d(sm.min_beta);
+    // ---- sources: layer f-1 (records) or the seeds
+    const long long s0 = f > 0 ? lane.frame_base[f - 1] : 0;
+    const long long s1 = f > 0 ? d0 : S0;
+    const long long nsrc = s1 - s0;
+    const long long row0 = E.ll_off + (long long)f * a.width;
+    if (min_beta != INF) {
+      // work items = (source, emitting arc): each thread takes sources and
+      // runs every emitting arc of its source
+      for (long long t0 = 0; t0 < nsrc; t0 += LAT_BS) {
+        const long long si = t0 + tid;
+        int deg = 0;
+        uint32_t beg = 0;
+        int32_t sst = 0;
+        double sc = INF;
+        int node = -1;
+        if (si < nsrc) {
+          if (f > 0) {
+            lat_rec(lane, s0 + si, &sst, &sc);
+            node = (int)(S0 + s0 + si);
+          } else {
+            sst = E.seeds[si].state;
+            sc = E.seeds[si].cost;
+            node = (int)si;
+          }
+          const CtwStateRange rg = a.g.ranges[sst];
+          beg = rg.emit_beg;
+          deg = (int)(rg.emit_end - rg.emit_beg);
+        }
+        for (int k = 0; k < deg; ++k) {
+          const uint32_t ai = beg + (uint32_t)k;
+          const CtwArc arc = a.g.arcs[ai];
+          double x;
+          {
+            const long long idx = row0 + arc.ilabel - 1;
+            x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+          }
+          double c0 = __dadd_rn(__dmul_rn(neg_scale, x), arc.weight);
+          int32_t ol0 = a.g.olabel[ai];
+          if (boost && ol0 != 0) c0 = __dadd_rn(c0, boost[ol0]);
+          if (!(c0 < INF)) continue;
+          if (cut_ok && sc + c0 + min_beta > cutoff) {
+            atomicAdd(&sm.pruned, 1ULL);
+            continue;
+          }
+          atomicAdd(&sm.items, 1ULL);
+          // local epsilon closure from nextstate(e): (state, cost, pred, olabel)
+          int32_t cst[LAT_CL];
+          double ccost[LAT_CL];
+          int8_t cpred[LAT_CL];
+          int32_t colab[LAT_CL];
+          int n = 1;
+          cst[0] = arc.nextstate;
+          ccost[0] = c0;
+          cpred[0] = -1;
+          colab[0] = ol0;
+          uint8_t queue[LAT_QL];
+          int qh = 0, qt = 1;
+          queue[0] = 0;
+          bool overflow = false;
+          while (qh < qt) {
+            const int u = queue[qh++];
+            const CtwStateRange ru = a.g.ranges[cst[u]];
+            for (uint32_t b = ru.eps_beg; b < ru.emit_beg; ++b) {
+              const CtwArc ea = a.g.arcs[b];
+              double cy = __dadd_rn(ccost[u], ea.weight);
+              const int32_t oly = a.g.olabel[b];
+              if (boost && oly != 0) cy = __dadd_rn(cy, boost[oly]);
+              if (!(cy < INF)) continue;
+              if (cut_ok && sc + cy + min_beta > cutoff) continue;
+              int j = 0;
+              while (j < n && cst[j] != ea.nextstate) ++j;
+              if (j < n) {
+                if (!(cy < ccost[j])) continue;
+              } else {
+                if (n == LAT_CL) {
+                  overflow = true;
+                  continue;
+                }
+                ++n;
+                cst[j] = ea.nextstate;
+              }
+              ccost[j] = cy;
+              cpred[j] = (int8_t)u;
+              colab[j] = oly;
+              if (qt == LAT_QL) {
+                overflow = true;
+                continue;
+              }
+              queue[qt++] = (uint8_t)j;
+            }
+          }
+          if (overflow) atomicMax(&sm.status, 3);
+          // arcs to the surviving destinations
+          for (int j = 0; j < n; ++j) {
+            const int dn = lat_get(lane, shift, mask, (uint32_t)cst[j]);
+            if (dn < 0) continue;
+            const double bd = lat_key2d(__ldcg(&E.beta[dn]));
+            const double tail = __dadd_rn(ccost[j], bd);
+            atomicMin(&E.beta[node], lat_d2key(tail));
+            if (__dadd_rn(sc, tail) > cutoff) continue;
+            // labels of the minimising path, oldest first
+            int nl = 0;
+            int32_t last = 0;
+            for (int u = j; u >= 0; u = cpred[u])
+              if (colab[u] != 0) {
+                ++nl;
+                last = colab[u];
+              }
+            int32_t code = 0;
+            if (nl == 1) code = last;
+            else if (nl > 1) {
+              const int po = atomicAdd(&sm.lpool_used, nl + 1);
+              if (po + nl + 1 > E.lpool_cap) {
+                atomicMax(&sm.status, 2);
+                continue;
+              }
+              int32_t* seg = E.lpool + po;
+              seg[0] = nl;
+              int pos = nl;
+              for (int u = j; u >= 0; u = cpred[u])
+                if (colab[u] != 0) seg[pos--] = colab[u];
+              code = -(po + 1);
+            }
+            const int ia = atomicAdd(&sm.n_arcs, 1);
+            if (ia >= E.arc_cap) {
+              atomicMax(&sm.status, 1);
+              continue;
+            }
+            CtwLatArc la;
+            la.src = node;
+            la.dst = dn;
+            la.w = ccost[j];
+            la.code = code;
+            la.frame = f;
+            la.dst_state = cst[j];
+            la.src_state = sst;
+            E.arcs[ia] = la;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- clear the destination map (the decoder's tok_clear image)
+    for (int i = tid; i < sm.nput; i += LAT_BS) {
+      ulonglong2* q = reinterpret_cast<ulonglong2*>(&lane.table[lane.slots[i].x]);
+      __stcg(q, make_ulonglong2(~0ULL, 0xFFFFFFFFULL));
+      __stcg(q + 1, make_ulonglong2(~0ULL, (unsigned long long)CTW_EMPTY));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    E.n_arcs = sm.n_arcs;
+    E.lpool_used = sm.lpool_used;
+    E.status = sm.status ? sm.status : (sm.best == ~0ULL ? 4 : 0);
+    E.final_mode = sm.final_mode;
+    E.best = best;
+    E.closure_items = (long long)sm.items;
+    E.closure_pruned = (long long)sm.pruned;
+  }
+}
+
+}  // namespace
+
+extern "C" int ctw_launch_lattice(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                                  const int32_t* olabel, const double* final_w, CtwLatEntry* d_ent, int n,
+                                  const void* loglik, int is_f64, int width, double acoustic_scale,
+                                  double lattice_beam, cudaStream_t stream) {
+  LatArgs a{d_lanes, LatGraph{ranges, arcs, olabel, final_w}, d_ent, loglik, width, is_f64, acoustic_scale,
+            lattice_beam};
+  (void)cudaGetLastError();
+  k_lattice<<<n, LAT_BS, 0, stream>>>(a);
+  return (int)cudaGetLastError();
+}

@@ -590,6 +590,35 @@ def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: 
     width = int(mats[0].shape[1])
     status = np.zeros(n, np.int32)
     err = np.zeros(n, np.int32)
+    buf, offs, base, dcode, loc = _pack_rows(mats, on_dev, packed, frames, width)
+    keep = buf
+    _lib.check(_lib.load().ctw_advance(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc,
+                                       _lib.ptr(offs), _lib.ptr(frames), width, _lib.ptr(status),
+                                       _lib.ptr(err)), "advance")
+    del keep
+    errors = []
+    for i, s in enumerate(states):
+        s._cache = None
+        if status[i] == _lib.OK:
+            s.frame_count += int(frames[i])
+            errors.append(None)
+        else:
+            try:
+                _raise_status(int(status[i]), s.frame_count + int(err[i]))
+            except (DecodeError, MemoryError) as e:
+                errors.append(e)
+    if raise_first:
+        for e in errors:
+            if e is not None:
+                raise e
+    return errors
+
+
+def _pack_rows(mats, on_dev, packed, frames, width):
+    """(buffer, element offsets, base pointer, dtype code, location) of the
+    log-likelihood rows of several channels: one contiguous host or device
+    buffer (an already-packed (n, F, V) block is used as is)."""
+    n = len(mats)
     if packed is not None:
         buf, offs = packed
         offs = np.asarray(offs, np.int64)
@@ -615,27 +644,7 @@ def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: 
         base, dcode, loc = buf.data_ptr(), (1 if buf.dtype == torch.float64 else 0), 1
     else:
         base, dcode, loc = buf.ctypes.data, (1 if buf.dtype == np.float64 else 0), 0
-    keep = buf
-    _lib.check(_lib.load().ctw_advance(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc,
-                                       _lib.ptr(offs), _lib.ptr(frames), width, _lib.ptr(status),
-                                       _lib.ptr(err)), "advance")
-    del keep
-    errors = []
-    for i, s in enumerate(states):
-        s._cache = None
-        if status[i] == _lib.OK:
-            s.frame_count += int(frames[i])
-            errors.append(None)
-        else:
-            try:
-                _raise_status(int(status[i]), s.frame_count + int(err[i]))
-            except (DecodeError, MemoryError) as e:
-                errors.append(e)
-    if raise_first:
-        for e in errors:
-            if e is not None:
-                raise e
-    return errors
+    return buf, offs, base, dcode, loc
 
 
 def _best_lanes(pool: LanePool, states: Sequence[DecodeState]) -> list:
@@ -742,7 +751,7 @@ def decode_utterance(graph, config: DecoderConfig, loglik, boost: np.ndarray | N
 
 
 def decode_batch(graph, config: DecoderConfig, utterances: Sequence, workers: int = 1, boost=None,
-                 *, device: int | None = None, max_lanes: int | None = None) -> list:
+                 *, device: int | None = None, max_lanes: int | None = None, lattice_beam: float | None = None) -> list:
     """Decode utterances independently; results keep the input order,
     failures are reported per index (decoder.py:436-463).
 
@@ -763,7 +772,7 @@ def decode_batch(graph, config: DecoderConfig, utterances: Sequence, workers: in
     pool = fg.device_graph(device).pool(config, fg.num_states)
     for g0 in range(0, n, group):
         idx = list(range(g0, min(n, g0 + group)))
-        _decode_group(fg, config, pool, utterances, idx, boost, per_utt, results)
+        _decode_group(fg, config, pool, utterances, idx, boost, per_utt, results, lattice_beam)
     return results
 
 
@@ -786,7 +795,7 @@ def _packed_source(utterances):
     return None
 
 
-def _decode_group(fg, config, pool: LanePool, utterances, idx, boost, per_utt, results):
+def _decode_group(fg, config, pool: LanePool, utterances, idx, boost, per_utt, results, lattice_beam=None):
     lanes = pool.acquire(len(idx))
     packed_src = _packed_source(utterances)
     try:
@@ -834,5 +843,18 @@ def _decode_group(fg, config, pool: LanePool, utterances, idx, boost, per_utt, r
                 hyps = _best_lanes(pool, [chans[k] for k in ok])
                 for k, h in zip(ok, hyps):
                     results[order[k]] = DecodeFailure(order[k], h) if isinstance(h, Exception) else h
+                if lattice_beam is not None:
+                    from .lattice import build_lattices
+
+                    lk = [k for k, h in zip(ok, hyps) if not isinstance(h, Exception)]
+                    if lk:
+                        pk = None
+                        if packed is not None:
+                            pos = {k: j for j, k in enumerate(ks)}
+                            pk = (packed[0], [packed[1][pos[k]] for k in lk])
+                        lats = build_lattices(pool, [chans[k] for k in lk], [mats[k] for k in lk], on_dev, pk,
+                                              [results[order[k]] for k in lk], lattice_beam)
+                        for k, lat in zip(lk, lats):
+                            results[order[k]] = lat
     finally:
         pool.release(lanes)

@@ -1,0 +1,131 @@
+"""Lattices and n-best lists (the reference has none,
+SPEC.md:312).
+
+A lattice is built on the device after a lane has decoded a whole utterance
+(``csrc/ctw_lattice.cu``, definition in DESIGN.md "Lattice"): its nodes are
+the seed tokens and the per-frame survivors the decoder recorded (the
+reference's history records, bit-identical to the reference); between two
+consecutive layers there is one arc per (source token, emitting arc,
+surviving destination) with the minimum epsilon continuation's cost and
+output labels; arcs whose best complete path is more than ``lattice_beam``
+above the best path are pruned. ``Lattice.nbest(n)`` returns the n lowest-cost
+distinct word sequences (A* over the kept arcs with exact remaining costs).
+
+    lats = decode_lattices(graph, config, utterances, lattice_beam=6.0)
+    for lat in lats:
+        print(lat.best_path.words, [h.words for h in lat.nbest(5)])
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .decoder import DecodeFailure, Hypothesis, decode_batch
+
+
+class Lattice:
+    """Pruned lattice of one utterance (host copy of ``ctw_lattice``).
+
+    Node ids: seeds ``0 .. n_seeds-1`` (the start state's epsilon closure),
+    then ``n_seeds + record index``. Arc arrays are sorted by (frame, src,
+    dst, weight)."""
+
+    def __init__(self, c: _lib.CtwLattice, best_path: Hypothesis):
+        self._c = c
+        self._fin = weakref.finalize(self, _lib.load().ctw_lattice_free, C.byref(c))
+        self.best_path = best_path
+        self.status = int(c.status)
+        self.final_mode = bool(c.final_mode)
+        self.frame_count = int(c.frame_count)
+        self.best_cost = float(c.best)
+        self.lattice_beam = float(c.lattice_beam)
+        self.closure_items = int(c.closure_items)
+        self.closure_pruned = int(c.closure_pruned)
+        ns, na = int(c.n_seeds), int(c.n_arcs)
+
+        def arr(p, n, dt):
+            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True) if n else np.zeros(0, dt)
+
+        self.seed_state = arr(c.seed_state, ns, np.int32)
+        self.seed_cost = arr(c.seed_cost, ns, np.float64)
+        soff = arr(c.seed_lab_off, ns + 1, np.int64)
+        slab = arr(c.seed_lab, int(soff[-1]) if ns else 0, np.int32)
+        self.seed_labels = [tuple(int(x) for x in slab[soff[k]:soff[k + 1]]) for k in range(ns)]
+        self.src = arr(c.arc_src, na, np.int32)
+        self.dst = arr(c.arc_dst, na, np.int32)
+        self.frame = arr(c.arc_frame, na, np.int32)
+        self.dst_state = arr(c.arc_dst_state, na, np.int32)
+        self.src_state = arr(c.arc_src_state, na, np.int32)
+        self.weight = arr(c.arc_w, na, np.float64)
+        self.dst_final = arr(c.arc_dst_final, na, np.float64)
+        aoff = arr(c.arc_lab_off, na + 1, np.int64)
+        alab = arr(c.arc_lab, int(aoff[-1]) if na else 0, np.int32)
+        self.labels = [tuple(int(x) for x in alab[aoff[k]:aoff[k + 1]]) for k in range(na)]
+
+    @property
+    def num_arcs(self) -> int:
+        return len(self.src)
+
+    def nbest(self, n: int, max_pops: int = 2_000_000) -> list[Hypothesis]:
+        """The n lowest-cost distinct word sequences, best first."""
+        if n <= 0:
+            return []
+        L = _lib.load()
+        cap = 1024
+        while True:
+            words = np.zeros(cap, np.int32)
+            off = np.zeros(n + 1, np.int64)
+            costs = np.zeros(n, np.float64)
+            found = C.c_int32()
+            pops = C.c_int64()
+            rc = L.ctw_lattice_nbest(C.byref(self._c), n, max_pops, _lib.ptr(words), cap, _lib.ptr(off),
+                                     _lib.ptr(costs), C.byref(found), C.byref(pops))
+            if rc == -2:
+                cap = int(off[int(found.value)]) + 16
+                continue
+            _lib.check(rc, "lattice n-best")
+            self.last_pops = int(pops.value)
+            return [Hypothesis(tuple(int(x) for x in words[off[k]:off[k + 1]]), float(costs[k]), self.frame_count)
+                    for k in range(int(found.value))]
+
+
+def decode_lattices(graph, config, utterances: Sequence, lattice_beam: float = 6.0, boost=None, *,
+                    device: int | None = None, max_lanes: int | None = None) -> list:
+    """decode_batch plus a pruned lattice per utterance: a list of Lattice
+    (``.best_path`` is decode_batch's Hypothesis) or DecodeFailure, in input
+    order."""
+    if not (lattice_beam >= 0):
+        raise ValueError("lattice_beam must be >= 0")
+    return decode_batch(graph, config, utterances, boost=boost, device=device, max_lanes=max_lanes,
+                        lattice_beam=float(lattice_beam))
+
+
+def build_lattices(pool, states, mats, on_dev, packed, hyps, lattice_beam: float) -> list:
+    """ctw_lane_lattice over lanes that decoded their whole utterance."""
+    from .decoder import _pack_rows
+
+    n = len(states)
+    ids = np.asarray([s._lane for s in states], np.int32)
+    frames = np.asarray([m.shape[0] for m in mats], np.int32)
+    width = int(mats[0].shape[1])
+    buf, offs, base, dcode, loc = _pack_rows(mats, on_dev, packed, frames, width)
+    outs = (_lib.CtwLattice * n)()
+    keep = buf
+    _lib.check(_lib.load().ctw_lane_lattice(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc,
+                                            _lib.ptr(offs), width, float(lattice_beam), C.cast(outs, C.c_void_p)),
+               "lattice")
+    del keep
+    res = []
+    for k in range(n):
+        c = _lib.CtwLattice()
+        C.memmove(C.byref(c), C.byref(outs[k]), C.sizeof(_lib.CtwLattice))
+        res.append(Lattice(c, hyps[k]))
+    return res
+
+
+__all__ = ["Lattice", "decode_lattices", "DecodeFailure"]

@@ -1,0 +1,183 @@
+"""Lattice generation / pruning / n-best on the GPU against the CPU
+restatement of the lattice definition (oracle/lattice_oracle.py) and a
+brute-force path enumeration. The lattice's nodes are the decoder's records
+(pinned to the reference), its best complete path must be best_path's, and
+n-best scores must match the enumeration within 1e-3 absolute (BASELINE.json
+north_star)."""
+
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "oracle"))
+
+NBEST_TOL = 1e-3  # north_star: lattice / n-best scores within 1e-3 absolute
+W_TOL = 1e-9      # arc weights: same operation order, only closure paths may differ in rounding
+
+
+def _system(**kw):
+    from paper_2311_04996_b200 import synth
+
+    return synth.build_system(synth.SystemSpec(**kw))
+
+
+def _oracle_lattice(s, cfg, frames, beam, boost=None):
+    import lattice_oracle as lo
+    import oracle as orc
+
+    ch = orc.OracleChannel.from_config(s.graph, cfg, boost=boost)
+    seeds = [(int(st), float(c), tuple(int(x) for x in ch.act_chain_pool[ch.act_chain_off[k]:ch.act_chain_off[k + 1]]))
+             for k, (st, c) in enumerate(zip(ch.act_state, ch.act_cost))]
+    ch.advance_frames(frames)
+    recs = [[(r[2], r[3]) for r in fr] for fr in ch.history_records()]
+    lat = lo.lattice(s.graph, cfg.acoustic_scale, np.asarray(frames, np.float64), seeds, recs, beam, boost)
+    return lat, seeds, ch.best_path()
+
+
+def _key(layer, state):
+    return (layer, state)
+
+
+def _gpu_arcs(lat):
+    seed_state = {k: int(s) for k, s in enumerate(lat.seed_state)}
+    out = []
+    for k in range(lat.num_arcs):
+        f = int(lat.frame[k])
+        src = (f - 1, int(lat.src_state[k]))
+        if int(lat.src[k]) < len(seed_state):
+            assert f == 0 and seed_state[int(lat.src[k])] == int(lat.src_state[k])
+        out.append((f, src, (f, int(lat.dst_state[k])), float(lat.weight[k]), lat.labels[k]))
+    return out
+
+
+def _oracle_arcs(arcs, alpha_state):
+    return [(f, alpha_state[src], (f, y), w, labs) for f, src, d, y, w, labs, score in arcs]
+
+
+def _match(gpu, ora):
+    """Multisets of (frame, src key, dst key, labels) with weights within W_TOL."""
+    from collections import defaultdict
+
+    g, o = defaultdict(list), defaultdict(list)
+    for f, s, d, w, l in gpu:
+        g[(f, s, d, l)].append(w)
+    for f, s, d, w, l in ora:
+        o[(f, s, d, l)].append(w)
+    return g, o
+
+
+SPECS = [
+    dict(num_units=8, num_words=20, order=2, seed=1),
+    dict(num_units=12, num_words=40, order=3, seed=4, min_pron=1, max_pron=4),
+    dict(num_units=10, num_words=30, order=2, seed=7, min_pron=1, max_pron=3),
+]
+
+
+@pytest.mark.parametrize("k", range(len(SPECS)))
+@pytest.mark.parametrize("beam", [0.0, 3.0, 8.0])
+def test_lattice_matches_oracle(k, beam):
+    import lattice_oracle as lo
+
+    from paper_2311_04996_b200 import DecoderConfig, decode_lattices, synth
+
+    s = _system(**SPECS[k])
+    frames = synth.planted_utterances(s, 1, 30, seed=10 + k, gap=3.0, noise=1.0)[0]
+    cfg = DecoderConfig(beam=14.0, max_active=400)
+    lat = decode_lattices(s.graph, cfg, [frames], lattice_beam=beam)[0]
+    ora, seeds, (ow, oc, _) = _oracle_lattice(s, cfg, frames, beam)
+    assert lat.status == 0
+    # the lattice's best complete path is the decoder's best path
+    assert math.isclose(lat.best_cost, lat.best_path.total_cost, rel_tol=0, abs_tol=1e-9)
+    assert lat.best_path.words == ow and abs(oc - lat.best_cost) <= 1e-9
+    assert abs(ora["best"] - lat.best_cost) <= 1e-9
+    # node identity: (layer, state); oracle node id -> key
+    node_key = {}
+    for i, (st, _, _) in enumerate(seeds):
+        node_key[i] = (-1, st)
+    for f, src, d, y, w, labs, score in ora["arcs"]:
+        node_key[d] = (f, y)
+    # GPU arcs must contain every oracle arc inside the beam (minus rounding
+    # slack) and only oracle arcs inside the beam (plus slack)
+    inner = lo.kept(ora, beam, -1e-7)
+    outer = lo.kept(ora, beam, +1e-7)
+    gpu = _gpu_arcs(lat)
+    gset = {}
+    for f, s_, d, w, l in gpu:
+        gset.setdefault((f, s_, d, l), []).append(w)
+    oset_outer = {}
+    for f, src, d, y, w, labs, score in outer:
+        oset_outer.setdefault((f, node_key.get(src, (f - 1, None)), (f, y), labs), []).append(w)
+    for f, src, d, y, w, labs, score in inner:
+        key = (f, node_key.get(src, (f - 1, None)), (f, y), labs)
+        assert key in gset, ("missing arc", key, w, score)
+        assert min(abs(w - x) for x in gset[key]) <= W_TOL
+    for key, ws in gset.items():
+        assert key in oset_outer, ("extra arc", key, ws)
+    assert len(gpu) >= len(inner)
+    assert len(gpu) <= len(outer)
+
+
+@pytest.mark.parametrize("k", range(len(SPECS)))
+def test_nbest_matches_enumeration(k):
+    import lattice_oracle as lo
+
+    from paper_2311_04996_b200 import DecoderConfig, decode_lattices, synth
+
+    s = _system(**SPECS[k])
+    frames = synth.planted_utterances(s, 1, 10, seed=20 + k, gap=3.0, noise=1.0)[0]
+    cfg = DecoderConfig(beam=12.0, max_active=200)
+    beam = 3.0
+    lat = decode_lattices(s.graph, cfg, [frames], lattice_beam=beam)[0]
+    got = lat.nbest(8)
+    ora, seeds, _ = _oracle_lattice(s, cfg, frames, beam)
+    want = lo.nbest(ora, lo.kept(ora, beam), seeds, 8, np.asarray(s.graph.final, np.float64),
+                    bound=ora["best"] + beam)
+    got = [h for h in got if h.total_cost <= ora["best"] + beam - 1e-6]
+    assert got and want
+    # best first, the decoder's best path on top
+    assert got[0].words == lat.best_path.words
+    assert abs(got[0].total_cost - lat.best_path.total_cost) <= 1e-9
+    assert all(a.total_cost <= b.total_cost + 1e-12 for a, b in zip(got, got[1:]))
+    # same word sequences with scores within the north-star tolerance
+    # (sequences whose scores tie within the tolerance may swap places)
+    wmap = dict(want)
+    for h in got:
+        if h.words in wmap:
+            assert abs(wmap[h.words] - h.total_cost) <= NBEST_TOL
+    common = [h for h in got if h.words in wmap]
+    assert len(common) >= min(len(got), len(want)) - 1
+    for (w1, c1), h in zip(want, got):
+        assert abs(c1 - h.total_cost) <= NBEST_TOL
+
+
+def test_lattice_batch_and_boost():
+    """A batch of utterances in one launch (some boosted): every lattice's best
+    path equals decode_batch's, 1-best of n-best equals the best path."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_batch, decode_lattices, synth
+
+    s = _system(num_units=12, num_words=40, order=3, seed=4, min_pron=1, max_pron=4)
+    utts = synth.planted_utterances(s, 6, 40, seed=3, gap=3.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=300)
+    rng = np.random.default_rng(0)
+    boosts = []
+    for i in range(6):
+        if i % 2:
+            b = np.zeros(s.graph.max_olabel + 1)
+            b[rng.choice(np.arange(1, 41), 5, replace=False)] = -rng.uniform(0.5, 3.0, 5)
+            boosts.append(b)
+        else:
+            boosts.append(None)
+    lats = decode_lattices(s.graph, cfg, utts, lattice_beam=5.0, boost=boosts)
+    hyps = decode_batch(s.graph, cfg, utts, boost=boosts)
+    for lat, h in zip(lats, hyps):
+        assert lat.best_path == h
+        assert abs(lat.best_cost - h.total_cost) <= 1e-9
+        nb = lat.nbest(3)
+        assert nb[0].words == h.words
+        assert lat.num_arcs > 0
