@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=2000, help="C4 streaming channels (0 = skip)")
     ap.add_argument("--stream-seconds", type=float, default=5.0, help="audio per stream in the C4 run")
     ap.add_argument("--cpu-streams", type=int, default=32, help="streams in the CPU reference C4 run")
+    ap.add_argument("--lattice", type=int, default=64,
+                    help="utterances in the lattice leg (decode + lattice + 10-best; 0 = skip)")
+    ap.add_argument("--lattice-beam", type=float, default=6.0)
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"],
                     help="c2: 3-gram TLG (default, the headline); c3: 4-gram ~50M-arc TLG; "
                          "c5: c2 + a 100-word boost table per utterance")
@@ -279,6 +282,38 @@ def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cor
     return st, res.finals, utts
 
 
+def lattice_run(fg, cfg, dev_ll, beam, dev):
+    """Lattice leg: the same utterances decoded with a
+    pruned lattice (device) and a 10-best list (host A*) per utterance.
+    Reports throughput of decode+lattice and of the lattice stage alone."""
+    import torch
+
+    from paper_2311_04996_b200 import decode_batch, decode_lattices
+
+    n = int(dev_ll.shape[0])
+    decode_lattices(fg, cfg, dev_ll, lattice_beam=beam, device=dev)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hyps = decode_batch(fg, cfg, dev_ll, device=dev)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    lats = decode_lattices(fg, cfg, dev_ll, lattice_beam=beam, device=dev)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    nb = [lat.nbest(10) for lat in lats]
+    t3 = time.perf_counter()
+    audio = n * int(dev_ll.shape[1]) * FRAME_S
+    arcs = [lat.num_arcs for lat in lats]
+    return {"utterances": n, "lattice_beam": beam,
+            "decode_s": t1 - t0, "decode_lattice_s": t2 - t1, "nbest10_host_s": t3 - t2,
+            "rtfx_decode_plus_lattice": audio / (t2 - t1),
+            "lattice_stage_s": max(0.0, (t2 - t1) - (t1 - t0)),
+            "arcs_per_utt_mean": float(np.mean(arcs)), "arcs_per_frame_mean": float(np.mean(arcs)) / int(dev_ll.shape[1]),
+            "nbest_mean_found": float(np.mean([len(x) for x in nb])),
+            "best_equals_decode": all(l.best_path == h for l, h in zip(lats, hyps)),
+            "nbest1_equals_best": all(x and x[0].words == h.words for x, h in zip(nb, hyps))}
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -443,6 +478,8 @@ def main():
         "clocks": clk.summary(),
         "stage_profile": _stage_profile(prof, st),
     }
+    if args.lattice > 0 and world == 1:
+        line["lattice"] = lattice_run(fg, cfg, dev_ll[: args.lattice], args.lattice_beam, dev)
     if args.streams > 0 and args.config == "c2":
         # warm-up: the same number of channels for one second (lane tables and
         # histories grow to their steady-state sizes; lanes are then recycled)

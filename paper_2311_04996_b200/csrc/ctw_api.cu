@@ -20,6 +20,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <unordered_set>
 #include <string>
 #include <vector>
 
@@ -98,6 +99,7 @@ struct ctw_graph {
   int refs = 1;  // the creator + one per lane set (lanes keep their graph alive)
   int device = 0;
   bool eps_nonneg = true;  // every epsilon arc weight >= 0
+  double w_min_emit = 0.0;  // min(0, smallest emitting arc weight): lattice source bound
   bool eps_olabel = false; // some epsilon arc carries an output label (boost applies)
   int64_t S = 0, A = 0, start = 0, max_il = 0, max_ol = 0;
   CtwStateRange* ranges = nullptr;
@@ -524,6 +526,7 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
   }
   std::vector<CtwArc> arcs((size_t)std::max<int64_t>(num_arcs, 1));
   bool eps_nonneg = true, eps_olabel = false;
+  double w_min_emit = 0.0;
   for (int64_t s = 0; s < num_states; ++s) {
     for (int64_t a = off[s]; a < off[s + 1]; ++a) {
       const bool eps = a < eps_end[s];
@@ -534,6 +537,8 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
       if (eps) {
         if (!(weight[a] >= 0.0)) eps_nonneg = false;
         if (olabel[a] != 0) eps_olabel = true;
+      } else if (weight[a] < w_min_emit) {
+        w_min_emit = weight[a];
       }
       max_il = std::max<int64_t>(max_il, ilabel[a]);
       max_ol = std::max<int64_t>(max_ol, olabel[a]);
@@ -549,6 +554,7 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
   g->h_final.assign(final_w, final_w + num_states);
   g->eps_nonneg = eps_nonneg;
   g->eps_olabel = eps_olabel;
+  g->w_min_emit = w_min_emit;
   auto bail = [&](int code) {
     ctw_graph_destroy(g);
     return code;
@@ -1358,7 +1364,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
   std::vector<CtwLatEntry> ent(n);
   std::vector<int32_t> arc_cap(n), lab_cap(n);
   for (int i = 0; i < n; ++i) {
-    arc_cap[i] = 1024 + 64 * frames[i];
+    arc_cap[i] = 4096 + 256 * frames[i];  // ~40 kept arcs per frame at lattice beam 6 on C2
     lab_cap[i] = 4 * arc_cap[i];
   }
   CtwLatEntry* d_ent = nullptr;
@@ -1401,6 +1407,15 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       e.lpool = d_lab[i];
       e.lpool_cap = lab_cap[i];
       e.beta = d_beta[i];
+      // lower bound of any emitting step's graph part: min arc weight plus the
+      // most negative boost (source-level pruning in the kernel)
+      double bmin = 0.0;
+      if (L.boost) {
+        std::vector<double> hb((size_t)L.boost_len);
+        CUDA_TRY(cudaMemcpy(hb.data(), L.boost, hb.size() * 8, cudaMemcpyDeviceToHost));
+        for (double x : hb) bmin = std::min(bmin, x);
+      }
+      e.emit_lb = g->w_min_emit + bmin;
       ent[k] = e;
     }
     CUDA_TRY(cudaMemcpyAsync(d_ent, ent.data(), m * sizeof(CtwLatEntry), cudaMemcpyHostToDevice, l->stream));
@@ -1559,38 +1574,63 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
     const double c = lat->arc_w[k] + beta[adst[k]];
     if (c < beta[asrc[k]]) beta[asrc[k]] = c;
   }
-  // A*: partial paths in a persistent tree; priority = g + beta (exact)
+  // A*: partial paths in a persistent tree; priority = g + beta (exact
+  // remaining cost), deeper first among ties. A partial path is dominated
+  // when an earlier-popped one reached the same node with the same word
+  // prefix (same continuations, no higher cost): (node, prefix hash) is
+  // expanded once -- exact for distinct word sequences and it keeps
+  // equal-cost alignment variants from exploding.
   struct P {
     int parent;
     int node;
     int arc;
+    int depth;
     double g;
+    uint64_t h;  // hash of the word prefix
+  };
+  struct QE {
+    double f;
+    int depth;
+    int idx;
+    bool operator>(const QE& o) const {
+      if (f != o.f) return f > o.f;
+      if (depth != o.depth) return depth < o.depth;
+      return idx > o.idx;
+    }
+  };
+  auto mix = [](uint64_t h, int32_t w) {
+    h ^= (uint64_t)(uint32_t)w + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    return h * 0xBF58476D1CE4E5B9ull;
   };
   std::vector<P> tree;
-  typedef std::pair<double, int> QE;
   std::vector<QE> heap;
   auto push = [&](const P& p) {
     tree.push_back(p);
-    heap.push_back(QE(p.g + beta[p.node], (int)tree.size() - 1));
+    heap.push_back(QE{p.g + beta[p.node], p.depth, (int)tree.size() - 1});
     std::push_heap(heap.begin(), heap.end(), std::greater<QE>());
   };
   for (int64_t k = 0; k < ns; ++k) {
     const int v = idx((int32_t)k);
-    if (beta[v] < INF) push(P{-1, v, -1, lat->seed_cost[k]});
+    uint64_t h = 0x12345678ull;
+    for (int64_t j = lat->seed_lab_off[k]; j < lat->seed_lab_off[k + 1]; ++j) h = mix(h, lat->seed_lab[j]);
+    if (beta[v] < INF) push(P{-1, v, -1, 0, lat->seed_cost[k], h});
   }
   std::vector<std::vector<int32_t>> seen;
   std::vector<double> found_cost;
+  std::unordered_set<uint64_t> expanded;
   int64_t npop = 0;
   while (!heap.empty() && (int)found_cost.size() < n && npop < max_pops) {
     std::pop_heap(heap.begin(), heap.end(), std::greater<QE>());
     const QE top = heap.back();
     heap.pop_back();
     ++npop;
-    const P cur = tree[top.second];
+    const P cur = tree[top.idx];
+    const uint64_t key = mix(cur.h, cur.node) ^ ((uint64_t)cur.node << 1);
+    if (!expanded.insert(key).second) continue;  // dominated (same node, same words so far)
     if (fin[cur.node] < INF && out_off[cur.node] == out_off[cur.node + 1] && cur.arc >= 0) {
       // complete path: words = seed labels + arc labels, oldest first
       std::vector<int> arcs_rev;
-      int t = top.second, seed_node = -1;
+      int t = top.idx, seed_node = -1;
       while (t >= 0) {
         if (tree[t].arc >= 0) arcs_rev.push_back(tree[t].arc);
         else seed_node = ids[tree[t].node];
@@ -1609,7 +1649,10 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
     }
     for (int q = out_off[cur.node]; q < out_off[cur.node + 1]; ++q) {
       const int k = adj[q];
-      if (beta[adst[k]] < INF) push(P{top.second, adst[k], k, cur.g + lat->arc_w[k]});
+      if (!(beta[adst[k]] < INF)) continue;
+      uint64_t h = cur.h;
+      for (int64_t j = lat->arc_lab_off[k]; j < lat->arc_lab_off[k + 1]; ++j) h = mix(h, lat->arc_lab[j]);
+      push(P{top.idx, adst[k], k, cur.depth + 1, cur.g + lat->arc_w[k], h});
     }
   }
   if (pops) *pops = npop;

@@ -183,6 +183,7 @@ struct CtwLatEntry {
   int32_t* lpool;             // label segments [n, l1..ln]
   int32_t lpool_cap;
   unsigned long long* beta;   // per node (seeds first, then records): sortable key
+  double emit_lb;             // lower bound of an emitting arc's weight (+ boost), <= 0
   // outputs
   int32_t n_arcs, lpool_used;
   int32_t status;             // 0 ok, 1 arc buffer full, 2 label pool full, 3 closure overflow, 4 no final path

@@ -25,11 +25,12 @@
 // work item that runs its own small epsilon closure, and kept arcs are
 // appended to the lane's arc buffer.
 #include <cuda_runtime.h>
+#include <cub/block/block_scan.cuh>
 #include <stdint.h>
 
 #include "ctw_common.h"
 
-#define LAT_BS 256
+#define LAT_BS 512
 #define LAT_CL 48       // local epsilon-closure capacity per work item
 #define LAT_QL 128      // local relaxation budget per work item
 
@@ -105,7 +106,17 @@ __device__ __forceinline__ int lat_get(const CtwLane& lane, uint32_t shift, uint
 }
 
 struct __align__(16) LatSmem {
+  typedef cub::BlockScan<int, LAT_BS> Scan;
+  typename Scan::TempStorage scan;
+  // the current tile of sources: (source, emitting arc) items are spread
+  // over all threads by the degree prefix
+  int off[LAT_BS + 1];
+  uint32_t beg[LAT_BS];
+  int32_t sst[LAT_BS];
+  int32_t node[LAT_BS];
+  double sc[LAT_BS];
   int n_arcs, lpool_used, status, nput;
+  unsigned long long ac_min;  // min over the frame row of -scale * ll (sortable key)
   unsigned long long min_beta;
   unsigned long long best;
   int final_mode;
@@ -171,8 +182,17 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
     if (tid == 0) {
       sm.min_beta = ~0ULL;
       sm.nput = 0;
+      sm.ac_min = ~0ULL;
     }
     __syncthreads();
+    {
+      // smallest acoustic term of the frame (source-level pruning bound)
+      const long long rr = E.ll_off + (long long)f * a.width;
+      for (int v = tid; v < a.width; v += LAT_BS) {
+        const double x = a.is_f64 ? ((const double*)a.loglik)[rr + v] : (double)((const float*)a.loglik)[rr + v];
+        atomicMin(&sm.ac_min, lat_d2key(__dmul_rn(neg_scale, x)));
+      }
+    }
     for (long long r = d0 + tid; r < d1; r += LAT_BS) {
       const unsigned long long bk = E.beta[S0 + r];
       if (bk == ~0ULL) continue;
@@ -197,25 +217,44 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
       for (long long t0 = 0; t0 < nsrc; t0 += LAT_BS) {
         const long long si = t0 + tid;
         int deg = 0;
-        uint32_t beg = 0;
-        int32_t sst = 0;
-        double sc = INF;
-        int node = -1;
+        const double step_lb = lat_key2d(sm.ac_min) + E.emit_lb;  // any emitting step costs at least this
         if (si < nsrc) {
+          int32_t st0;
+          double c0s;
+          int nd;
           if (f > 0) {
-            lat_rec(lane, s0 + si, &sst, &sc);
-            node = (int)(S0 + s0 + si);
+            lat_rec(lane, s0 + si, &st0, &c0s);
+            nd = (int)(S0 + s0 + si);
           } else {
-            sst = E.seeds[si].state;
-            sc = E.seeds[si].cost;
-            node = (int)si;
+            st0 = E.seeds[si].state;
+            c0s = E.seeds[si].cost;
+            nd = (int)si;
           }
-          const CtwStateRange rg = a.g.ranges[sst];
-          beg = rg.emit_beg;
+          const CtwStateRange rg = a.g.ranges[st0];
           deg = (int)(rg.emit_end - rg.emit_beg);
+          // no arc of this source can be kept (epsilon continuations only add)
+          if (cut_ok && c0s + step_lb + min_beta > cutoff + 1e-9 * fabs(cutoff)) deg = 0;
+          sm.beg[tid] = rg.emit_beg;
+          sm.sst[tid] = st0;
+          sm.sc[tid] = c0s;
+          sm.node[tid] = nd;
         }
-        for (int k = 0; k < deg; ++k) {
-          const uint32_t ai = beg + (uint32_t)k;
+        int ex, tot;
+        LatSmem::Scan(sm.scan).ExclusiveSum(deg, ex, tot);
+        sm.off[tid] = ex;
+        __syncthreads();
+        const int nv = (int)min((long long)LAT_BS, nsrc - t0);
+        for (int item = tid; item < tot; item += LAT_BS) {
+          int lo = 0, hi = nv - 1;  // last source with off <= item
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.off[mid] <= item) lo = mid;
+            else hi = mid - 1;
+          }
+          const int32_t sst = sm.sst[lo];
+          const double sc = sm.sc[lo];
+          const int node = sm.node[lo];
+          const uint32_t ai = sm.beg[lo] + (uint32_t)(item - sm.off[lo]);
           const CtwArc arc = a.g.arcs[ai];
           double x;
           {
@@ -325,6 +364,7 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
             E.arcs[ia] = la;
           }
         }
+        __syncthreads();  // the tile's smem is reused by the next tile
       }
     }
     __syncthreads();
