@@ -113,6 +113,11 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
                      const int32_t* olabel, const double* weight, const int32_t* nextstate,
                      const double* final_w, int64_t num_states, int64_t num_arcs, int64_t start,
                      int32_t device, ctw_graph** out);
+/* The same from a binary .ctwg file (paper_2311_04996_b200/graphio.py
+ * layout: "CTWGRAPH", version 1, then the flattened CSR arrays), memory-
+ * mapped -- the graph load path without text parsing (replaces
+ * read_fst_text + flatten, wfst.py:213-268, decoder.py:130-138). */
+int ctw_graph_load(const char* path, int32_t device, ctw_graph** out);
 void ctw_graph_destroy(ctw_graph* g);
 /* bytes: device bytes of the resident graph. */
 int ctw_graph_info(const ctw_graph* g, int64_t* num_states, int64_t* num_arcs, int64_t* max_ilabel,

@@ -58,6 +58,7 @@ _SIGS = {
     "ctw_last_error": (C.c_char_p, []),
     "ctw_device_count": (I32, []),
     "ctw_graph_create": (I32, [P] * 7 + [I64, I64, I64, I32, C.POINTER(P)]),
+    "ctw_graph_load": (I32, [C.c_char_p, I32, C.POINTER(P)]),
     "ctw_graph_destroy": (None, [P]),
     "ctw_graph_info": (I32, [P] + [C.POINTER(I64)] * 5),
     "ctw_lanes_create": (I32, [P, I32, C.POINTER(CtwConfig), P, C.POINTER(P)]),

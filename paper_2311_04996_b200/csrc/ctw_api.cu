@@ -11,6 +11,10 @@
 //   history_records / active_tokens          decoder.py:240-260
 //   kernel plug-in contract                  _pykernel.py:28-248
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -570,6 +574,61 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
     return bail(fail(-3, "graph upload failed"));
   *out = g;
   return 0;
+}
+
+int ctw_graph_load(const char* path, int32_t device, ctw_graph** out) {
+  *out = nullptr;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(-1, std::string("cannot open graph file ") + path);
+  struct stat st;
+  if (fstat(fd, &st) != 0 || st.st_size < 64) {
+    close(fd);
+    return fail(-1, "graph file too small");
+  }
+  const size_t size = (size_t)st.st_size;
+  void* base = mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+  close(fd);
+  if (base == MAP_FAILED) return fail(-1, "mmap of the graph file failed");
+  const char* b = (const char*)base;
+  int rc = 0;
+  do {
+    if (std::memcmp(b, "CTWGRAPH", 8) != 0) {
+      rc = fail(-1, "not a CTWGRAPH file");
+      break;
+    }
+    uint32_t ver;
+    std::memcpy(&ver, b + 8, 4);
+    if (ver != 1) {
+      rc = fail(-1, "unsupported CTWGRAPH version");
+      break;
+    }
+    int64_t h[5];
+    std::memcpy(h, b + 16, sizeof(h));
+    const int64_t S = h[0], A = h[1], start = h[2];
+    if (S <= 0 || A < 0 || start < 0 || start >= S) {
+      rc = fail(-1, "bad CTWGRAPH header");
+      break;
+    }
+    // graphio.py layout: arrays in order, each 8-byte aligned
+    size_t pos = 64;
+    auto take = [&](size_t bytes) {
+      const size_t at = pos;
+      pos = (pos + bytes + 7) & ~(size_t)7;
+      return at;
+    };
+    const size_t o_off = take((size_t)(S + 1) * 8), o_eps = take((size_t)S * 8), o_il = take((size_t)A * 4),
+                 o_ol = take((size_t)A * 4), o_w = take((size_t)A * 8), o_ns = take((size_t)A * 4),
+                 o_fin = take((size_t)S * 8);
+    if (pos > size) {
+      rc = fail(-1, "truncated CTWGRAPH file");
+      break;
+    }
+    rc = ctw_graph_create((const int64_t*)(b + o_off), (const int64_t*)(b + o_eps), (const int32_t*)(b + o_il),
+                          (const int32_t*)(b + o_ol), (const double*)(b + o_w), (const int32_t*)(b + o_ns),
+                          (const double*)(b + o_fin), S, A, start, device, out);
+  } while (false);
+  munmap(base, size);
+  return rc;
 }
 
 void ctw_graph_destroy(ctw_graph* g) {
