@@ -504,9 +504,9 @@ def main():
     if args.lattice > 0 and world == 1:
         line["lattice"] = lattice_run(fg, cfg, dev_ll[: args.lattice], args.lattice_beam, dev)
     if args.streams > 0 and args.config == "c2":
-        # warm-up: the same number of channels for one second (lane tables and
-        # histories grow to their steady-state sizes; lanes are then recycled)
-        streaming_run(s, args.streams, 1.0, rank + 100, device=dev)
+        # warm-up: one full run of the same shape (a serving process's steady
+        # state: lane tables grown, history pages mapped and recycled)
+        streaming_run(s, args.streams, args.stream_seconds, rank + 100, device=dev)
         st, finals, sutts = streaming_run(s, args.streams, args.stream_seconds, rank, device=dev)
         line["streaming"] = {"gpu": st}
         if world == 1 and not args.no_cpu and args.cpu_streams > 0:

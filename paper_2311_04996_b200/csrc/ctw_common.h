@@ -98,7 +98,7 @@ struct __align__(16) CtwSrc {
 // token table is grown once a frame fills more than CTW_LOAD(tcap) entries
 // (3/4 load), so lists of CTW_LOAD(tcap) entries never overflow in a frame
 // that commits.
-#define CTW_RMAX 8
+#define CTW_RMAX 16  // 8 portable; 16 with the non-portable cluster attribute
 #define CTW_LOAD(tcap) ((tcap) - (tcap) / 4)
 #define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_LOAD(tcap))
 #define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_LOAD(tcap))

@@ -539,6 +539,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
     __syncthreads();
     if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
     const int n_cur = sm.n_cur, n_first = sm.n_first;
+    const int tail = 32 * CTW_WARPS * R;  // items left when chunks shrink
     const uint2* in0 = sm.in0;
     const uint2* in1 = sm.in1;
     const uint32_t epoch = (uint32_t)pass;
@@ -546,11 +547,17 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
     // arcs over their lanes
     const int lane = tid & 31, w = tid >> 5;
     for (;;) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&G->pw[q], 32);
+      // guided chunks: 32 items, 8 near the end of the pass (shorter tail
+      // before the barrier)
+      int base = 0, gsz = 32;
+      if (lane == 0) {
+        if (n_cur - *((volatile int*)&G->pw[q]) < tail) gsz = 8;
+        base = atomicAdd(&G->pw[q], gsz);
+      }
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      gsz = __shfl_sync(0xFFFFFFFFu, gsz, 0);
       if (base >= n_cur) break;
-      const int nv = min(32, n_cur - base);
+      const int nv = min(gsz, n_cur - base);
       if (lane == 0) atomicAdd(&sm.eps_items, nv);
       int deg = 0;
       if (lane < nv) {
@@ -1189,11 +1196,15 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       // warps grab 32 sources at a time and spread their emitting arcs over
       // the lanes (warp scan of out-degrees); sources with more than
       // CTW_BIG arcs go to the arc-parallel list instead
-      int base = 0;
-      if (lane_ == 0) base = atomicAdd(&fc->work_e, 32);
+      int base = 0, gsz = 32;
+      if (lane_ == 0) {
+        if (n_src - *((volatile int*)&fc->work_e) < 32 * CTW_WARPS * R) gsz = 8;  // guided tail
+        base = atomicAdd(&fc->work_e, gsz);
+      }
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      gsz = __shfl_sync(0xFFFFFFFFu, gsz, 0);
       if (base >= n_src) break;
-      const int nv = min(32, n_src - base);
+      const int nv = min(gsz, n_src - base);
       int deg = 0;
       if (lane_ < nv) {
         const CtwSrc t = src[base + lane_];
@@ -1677,17 +1688,27 @@ __global__ void k_clear_table(CtwTok* T, uint32_t n) {
 
 // ------------------------------------------------------ launch wrappers ---
 
-// Ranks (CTAs) per lane for a launch of n lanes: CTW_CLUSTER overrides;
-// otherwise CTW_DEFAULT_CLUSTER.
+// Ranks (CTAs) per lane for a launch of n lanes: CTW_CLUSTER overrides.
+// Otherwise 8 (best throughput when lanes fill the GPU: 71 clusters
+// resident), or 16 when even 16-CTA clusters leave SMs idle -- small
+// streaming steps, where per-lane latency is the metric (a 16-CTA lane runs
+// a frame in ~0.67 M cycles vs ~1.3 M with 8).
 static int cluster_size(int n) {
-  (void)n;
   static int env = -1;
   if (env < 0) {
     const char* s = getenv("CTW_CLUSTER");
     env = s ? atoi(s) : 0;
     if (env < 0 || env > CTW_RMAX) env = 0;
   }
-  return env ? env : CTW_DEFAULT_CLUSTER;
+  if (env) return env;
+  static int resident = 0;  // CTAs resident on the device
+  if (!resident) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = sms * CTW_MINB;
+  }
+  return (long long)n * 16 <= resident ? 16 : CTW_DEFAULT_CLUSTER;
 }
 
 extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
@@ -1701,6 +1722,7 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
     cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   (void)cudaGetLastError();  // drop stale errors of unchecked calls
   const int R = cluster_size(n);
+  if (R > 8) cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(n * R));
   lc.blockDim = dim3(CTW_BS);
