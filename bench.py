@@ -323,6 +323,16 @@ def lattice_run(fg, cfg, dev_ll, beam, dev):
     t2 = time.perf_counter()
     nb = [lat.nbest(10) for lat in lats]
     t3 = time.perf_counter()
+    # multi-word boosting by lattice rescoring: 100 random two-word phrases
+    from paper_2311_04996_b200 import PhraseBoost
+
+    rng = np.random.default_rng(5)
+    nw = int(fg.max_olabel)
+    pb = PhraseBoost({(int(a), int(b)): float(m) for a, b, m in
+                      zip(rng.integers(1, nw + 1, 100), rng.integers(1, nw + 1, 100), rng.uniform(0.5, 8.5, 100))})
+    t4 = time.perf_counter()
+    nbp = [lat.nbest(10, phrases=pb) for lat in lats]
+    t5 = time.perf_counter()
     audio = n * int(dev_ll.shape[1]) * FRAME_S
     arcs = [lat.num_arcs for lat in lats]
     return {"utterances": n, "lattice_beam": beam,
@@ -331,6 +341,8 @@ def lattice_run(fg, cfg, dev_ll, beam, dev):
             "lattice_stage_s": max(0.0, (t2 - t1) - (t1 - t0)),
             "arcs_per_utt_mean": float(np.mean(arcs)), "arcs_per_frame_mean": float(np.mean(arcs)) / int(dev_ll.shape[1]),
             "nbest_mean_found": float(np.mean([len(x) for x in nb])),
+            "phrase_nbest10_host_s": t5 - t4, "phrase_fsa_states": pb.num_states,
+            "phrase_nbest_mean_found": float(np.mean([len(x) for x in nbp])),
             "best_equals_decode": all(l.best_path == h for l, h in zip(lats, hyps)),
             "nbest1_equals_best": all(x and x[0].words == h.words for x, h in zip(nb, hyps))}
 

@@ -191,6 +191,17 @@ void ctw_lattice_free(ctw_lattice* lat);
 int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32_t* words, int64_t words_cap,
                       int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops);
 
+/* The same over the lattice composed with a phrase automaton (multi-word
+ * boosting by lattice rescoring): a deterministic
+ * Aho-Corasick automaton over word ids -- state 0 the root, per state a
+ * goto list sorted by word (goto_off[fsa_states + 1], goto_word, goto_next),
+ * a failure link and out_cost[state] = summed cost of the phrases completed
+ * on entering it (negative = boost). */
+int ctw_lattice_nbest_phrases(const ctw_lattice* lat, int32_t fsa_states, const int32_t* goto_off,
+                              const int32_t* goto_word, const int32_t* goto_next, const int32_t* fail_link,
+                              const double* out_cost, int32_t n, int64_t max_pops, int32_t* words,
+                              int64_t words_cap, int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops);
+
 /* Counters since creation (or the last reset): all kernel launches, launches
  * of the frame kernel and their total device milliseconds (CUDA events on the
  * lane stream around each launch), emitting arcs relaxed (E_emit), source

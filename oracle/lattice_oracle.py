@@ -97,7 +97,19 @@ def kept(lat, beam, slack=0.0):
     return [a for a in lat["arcs"] if a[6] <= cut]
 
 
-def nbest(lat, arcs, seeds, n, final, bound=None, max_paths=500_000):
+def phrase_cost(words, phrases):
+    """Brute force: every occurrence of every phrase (overlapping, nested)
+    pays -magnitude."""
+    c = 0.0
+    for ph, mag in phrases.items():
+        k = len(ph)
+        for i in range(len(words) - k + 1):
+            if tuple(words[i:i + k]) == tuple(ph):
+                c += -float(mag)
+    return c
+
+
+def nbest(lat, arcs, seeds, n, final, bound=None, max_paths=500_000, phrases=None):
     """Brute force: every complete path through `arcs` (seed -> last layer)
     with total cost <= bound (default best + lattice beam of the arcs'
     scores, i.e. all paths that can matter), total = seed cost + sum w +
@@ -132,7 +144,7 @@ def nbest(lat, arcs, seeds, n, final, bound=None, max_paths=500_000):
         if layer == T:
             fw = fin(node)
             if fw < INF:
-                paths.append((cost + fw, words))
+                paths.append((cost + fw + (phrase_cost(words, phrases) if phrases else 0.0), words))
             return
         for a in out_arcs.get(node, []):
             dfs(a[2], cost + a[4], words + a[5], layer + 1)

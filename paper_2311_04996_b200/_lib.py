@@ -80,6 +80,8 @@ _SIGS = {
     "ctw_lane_lattice": (I32, [P, P, I32, P, I32, I32, P, I32, F64, P]),
     "ctw_lattice_free": (None, [C.POINTER(CtwLattice)]),
     "ctw_lattice_nbest": (I32, [C.POINTER(CtwLattice), I32, I64, P, I64, P, P, C.POINTER(I32), C.POINTER(I64)]),
+    "ctw_lattice_nbest_phrases": (I32, [C.POINTER(CtwLattice), I32, P, P, P, P, P, I32, I64, P, I64, P, P,
+                                        C.POINTER(I32), C.POINTER(I64)]),
     "ctw_advance_chunk_compat": (I32, [P] * 6 + [I64, I64] + [P] * 5 + [I64, P, I64, I64, F64, F64,
                                       I64, F64, I64, P, I64, I64, I32, C.POINTER(I64),
                                       C.POINTER(CtwExport)]),

@@ -24,6 +24,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <unordered_map>
 #include <unordered_set>
 #include <string>
 #include <vector>
@@ -1591,15 +1592,54 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
   return 0;
 }
 
-int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32_t* words, int64_t words_cap,
-                      int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops) {
+namespace {
+
+// Deterministic phrase automaton (Aho-Corasick over word ids): per state a
+// sorted goto list, a failure link and the cost of the phrases completed on
+// entering the state (negative = boost).
+struct PhraseFsa {
+  int32_t n;
+  const int32_t* goto_off;
+  const int32_t* goto_word;
+  const int32_t* goto_next;
+  const int32_t* fail;
+  const double* out_cost;
+};
+
+inline int32_t fsa_step(const PhraseFsa* F, int32_t b, int32_t w, double* cost) {
+  if (!F) return 0;
+  for (;;) {
+    const int32_t* lo = F->goto_word + F->goto_off[b];
+    const int32_t* hi = F->goto_word + F->goto_off[b + 1];
+    const int32_t* it = std::lower_bound(lo, hi, w);
+    if (it != hi && *it == w) {
+      const int32_t nb = F->goto_next[it - F->goto_word];
+      *cost += F->out_cost[nb];
+      return nb;
+    }
+    if (b == 0) {
+      *cost += F->out_cost[0];
+      return 0;
+    }
+    b = F->fail[b];
+  }
+}
+
+// n best distinct word sequences of the lattice composed with an optional
+// phrase automaton. Search states are (lattice node, automaton state); the
+// remaining cost h is exact (backward DP over the reachable product), so A*
+// pops complete paths in cost order; a partial path is dominated once
+// another reached the same search state with the same word prefix.
+int lattice_nbest(const ctw_lattice* lat, const PhraseFsa* F, int32_t n, int64_t max_pops, int32_t* words,
+                  int64_t words_cap, int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops) {
   *n_found = 0;
   if (pops) *pops = 0;
   word_off[0] = 0;
   if (n <= 0 || lat->status == 4) return 0;
   const double INF = HUGE_VAL;
   const int64_t na = lat->n_arcs, ns = lat->n_seeds;
-  // node ids -> dense indices
+  const int64_t NB = F ? F->n : 1;
+  // lattice nodes -> dense indices; final weight per node
   std::vector<int32_t> ids;
   ids.reserve((size_t)(2 * na + ns));
   for (int64_t k = 0; k < ns; ++k) ids.push_back((int32_t)k);
@@ -1611,9 +1651,8 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
   ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
   auto idx = [&](int32_t node) { return (int)(std::lower_bound(ids.begin(), ids.end(), node) - ids.begin()); };
   const int nn = (int)ids.size();
-  std::vector<double> fin((size_t)nn, INF), beta((size_t)nn, INF);
-  std::vector<int> out_off((size_t)nn + 1, 0);
-  std::vector<int> asrc((size_t)na), adst((size_t)na);
+  std::vector<double> fin((size_t)nn, INF);
+  std::vector<int> out_off((size_t)nn + 1, 0), asrc((size_t)na), adst((size_t)na);
   for (int64_t k = 0; k < na; ++k) {
     asrc[k] = idx(lat->arc_src[k]);
     adst[k] = idx(lat->arc_dst[k]);
@@ -1626,26 +1665,81 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
     std::vector<int> fill(out_off.begin(), out_off.end() - 1);
     for (int64_t k = 0; k < na; ++k) adj[fill[asrc[k]]++] = (int)k;
   }
-  // exact remaining cost over the kept arcs (layers backwards: arcs are
-  // sorted by frame)
-  for (int v = 0; v < nn; ++v) beta[v] = fin[v];
-  for (int64_t k = na - 1; k >= 0; --k) {
-    const double c = lat->arc_w[k] + beta[adst[k]];
-    if (c < beta[asrc[k]]) beta[asrc[k]] = c;
+  // ---- reachable product states, forward (arcs are sorted by frame)
+  std::unordered_map<int64_t, int> pid;  // node * NB + b -> product index
+  std::vector<int> pnode, pb;
+  std::vector<double> pstart;  // start cost (seeds only), else INF
+  auto get = [&](int v, int b) {
+    const int64_t key = (int64_t)v * NB + b;
+    auto it = pid.find(key);
+    if (it != pid.end()) return it->second;
+    const int p = (int)pnode.size();
+    pid.emplace(key, p);
+    pnode.push_back(v);
+    pb.push_back(b);
+    pstart.push_back(INF);
+    return p;
+  };
+  struct PA {
+    int from, to, arc;
+    double c;
+  };
+  std::vector<PA> parcs;
+  std::vector<uint64_t> seed_h((size_t)ns);
+  std::vector<int> seed_p((size_t)ns, -1);
+  for (int64_t k = 0; k < ns; ++k) {
+    double c = lat->seed_cost[k];
+    int32_t b = 0;
+    for (int64_t j = lat->seed_lab_off[k]; j < lat->seed_lab_off[k + 1]; ++j) b = fsa_step(F, b, lat->seed_lab[j], &c);
+    const int p = get(idx((int32_t)k), b);
+    seed_p[k] = p;
+    if (c < pstart[p]) pstart[p] = c;
   }
-  // A*: partial paths in a persistent tree; priority = g + beta (exact
-  // remaining cost), deeper first among ties. A partial path is dominated
-  // when an earlier-popped one reached the same node with the same word
-  // prefix (same continuations, no higher cost): (node, prefix hash) is
-  // expanded once -- exact for distinct word sequences and it keeps
-  // equal-cost alignment variants from exploding.
+  {
+    // frontier expansion layer by layer: product states of a node are known
+    // before its out-arcs are processed because arcs are frame-sorted
+    std::vector<std::vector<int>> states_of((size_t)nn);
+    for (int p = 0; p < (int)pnode.size(); ++p) states_of[pnode[p]].push_back(p);
+    for (int64_t k = 0; k < na; ++k) {
+      const int v = asrc[k];
+      for (size_t q = 0; q < states_of[v].size(); ++q) {
+        const int p = states_of[v][q];
+        double c = lat->arc_w[k];
+        int32_t b = pb[p];
+        for (int64_t j = lat->arc_lab_off[k]; j < lat->arc_lab_off[k + 1]; ++j) b = fsa_step(F, b, lat->arc_lab[j], &c);
+        const size_t before = pnode.size();
+        const int t = get(adst[k], b);
+        if (pnode.size() > before) states_of[adst[k]].push_back(t);
+        parcs.push_back(PA{p, t, (int)k, c});
+      }
+    }
+  }
+  const int np = (int)pnode.size();
+  // ---- exact remaining cost (backward over product arcs: frame-sorted)
+  std::vector<double> h((size_t)np, INF);
+  for (int p = 0; p < np; ++p)
+    if (out_off[pnode[p]] == out_off[pnode[p] + 1]) h[p] = fin[pnode[p]];
+  for (int64_t q = (int64_t)parcs.size() - 1; q >= 0; --q) {
+    const PA& a = parcs[q];
+    const double c = a.c + h[a.to];
+    if (c < h[a.from]) h[a.from] = c;
+  }
+  std::vector<int> pout_off((size_t)np + 1, 0);
+  for (const PA& a : parcs) pout_off[a.from + 1]++;
+  for (int p = 0; p < np; ++p) pout_off[p + 1] += pout_off[p];
+  std::vector<int> padj(parcs.size());
+  {
+    std::vector<int> fill(pout_off.begin(), pout_off.end() - 1);
+    for (size_t q = 0; q < parcs.size(); ++q) padj[fill[parcs[q].from]++] = (int)q;
+  }
+  // ---- A*
   struct P {
     int parent;
-    int node;
-    int arc;
+    int p;
+    int parc;
     int depth;
     double g;
-    uint64_t h;  // hash of the word prefix
+    uint64_t hh;
   };
   struct QE {
     double f;
@@ -1657,22 +1751,27 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
       return idx > o.idx;
     }
   };
-  auto mix = [](uint64_t h, int32_t w) {
-    h ^= (uint64_t)(uint32_t)w + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
-    return h * 0xBF58476D1CE4E5B9ull;
+  auto mix = [](uint64_t x, int32_t w) {
+    x ^= (uint64_t)(uint32_t)w + 0x9E3779B97F4A7C15ull + (x << 6) + (x >> 2);
+    return x * 0xBF58476D1CE4E5B9ull;
   };
   std::vector<P> tree;
   std::vector<QE> heap;
-  auto push = [&](const P& p) {
-    tree.push_back(p);
-    heap.push_back(QE{p.g + beta[p.node], p.depth, (int)tree.size() - 1});
+  auto push = [&](const P& e) {
+    tree.push_back(e);
+    heap.push_back(QE{e.g + h[e.p], e.depth, (int)tree.size() - 1});
     std::push_heap(heap.begin(), heap.end(), std::greater<QE>());
   };
+  std::vector<int> seed_of_p((size_t)np, -1);
   for (int64_t k = 0; k < ns; ++k) {
-    const int v = idx((int32_t)k);
-    uint64_t h = 0x12345678ull;
-    for (int64_t j = lat->seed_lab_off[k]; j < lat->seed_lab_off[k + 1]; ++j) h = mix(h, lat->seed_lab[j]);
-    if (beta[v] < INF) push(P{-1, v, -1, 0, lat->seed_cost[k], h});
+    const int p = seed_p[k];
+    uint64_t x = 0x12345678ull;
+    for (int64_t j = lat->seed_lab_off[k]; j < lat->seed_lab_off[k + 1]; ++j) x = mix(x, lat->seed_lab[j]);
+    double c = lat->seed_cost[k];
+    int32_t b = 0;
+    for (int64_t j = lat->seed_lab_off[k]; j < lat->seed_lab_off[k + 1]; ++j) b = fsa_step(F, b, lat->seed_lab[j], &c);
+    seed_of_p[p] = (int)k;
+    if (h[p] < INF) push(P{-1, p, -1, 0, c, x});
   }
   std::vector<std::vector<int32_t>> seen;
   std::vector<double> found_cost;
@@ -1684,34 +1783,35 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
     heap.pop_back();
     ++npop;
     const P cur = tree[top.idx];
-    const uint64_t key = mix(cur.h, cur.node) ^ ((uint64_t)cur.node << 1);
-    if (!expanded.insert(key).second) continue;  // dominated (same node, same words so far)
-    if (fin[cur.node] < INF && out_off[cur.node] == out_off[cur.node + 1] && cur.arc >= 0) {
+    const uint64_t key = mix(cur.hh, cur.p) ^ ((uint64_t)cur.p << 1);
+    if (!expanded.insert(key).second) continue;  // dominated (same search state, same words so far)
+    const int v = pnode[cur.p];
+    if (out_off[v] == out_off[v + 1]) {
+      if (!(fin[v] < INF) || cur.parc < 0) continue;
       // complete path: words = seed labels + arc labels, oldest first
       std::vector<int> arcs_rev;
-      int t = top.idx, seed_node = -1;
+      int t = top.idx, seed = -1;
       while (t >= 0) {
-        if (tree[t].arc >= 0) arcs_rev.push_back(tree[t].arc);
-        else seed_node = ids[tree[t].node];
+        if (tree[t].parc >= 0) arcs_rev.push_back(parcs[tree[t].parc].arc);
+        else seed = seed_of_p[tree[t].p];
         t = tree[t].parent;
       }
       std::vector<int32_t> w;
-      for (int64_t j = lat->seed_lab_off[seed_node]; j < lat->seed_lab_off[seed_node + 1]; ++j)
-        w.push_back(lat->seed_lab[j]);
+      for (int64_t j = lat->seed_lab_off[seed]; j < lat->seed_lab_off[seed + 1]; ++j) w.push_back(lat->seed_lab[j]);
       for (auto it = arcs_rev.rbegin(); it != arcs_rev.rend(); ++it)
         for (int64_t j = lat->arc_lab_off[*it]; j < lat->arc_lab_off[*it + 1]; ++j) w.push_back(lat->arc_lab[j]);
       if (std::find(seen.begin(), seen.end(), w) == seen.end()) {
         seen.push_back(w);
-        found_cost.push_back(cur.g + fin[cur.node]);
+        found_cost.push_back(cur.g + fin[v]);
       }
       continue;
     }
-    for (int q = out_off[cur.node]; q < out_off[cur.node + 1]; ++q) {
-      const int k = adj[q];
-      if (!(beta[adst[k]] < INF)) continue;
-      uint64_t h = cur.h;
-      for (int64_t j = lat->arc_lab_off[k]; j < lat->arc_lab_off[k + 1]; ++j) h = mix(h, lat->arc_lab[j]);
-      push(P{top.idx, adst[k], k, cur.depth + 1, cur.g + lat->arc_w[k], h});
+    for (int q = pout_off[cur.p]; q < pout_off[cur.p + 1]; ++q) {
+      const PA& a = parcs[padj[q]];
+      if (!(h[a.to] < INF)) continue;
+      uint64_t x = cur.hh;
+      for (int64_t j = lat->arc_lab_off[a.arc]; j < lat->arc_lab_off[a.arc + 1]; ++j) x = mix(x, lat->arc_lab[j]);
+      push(P{top.idx, a.to, padj[q], cur.depth + 1, cur.g + a.c, x});
     }
   }
   if (pops) *pops = npop;
@@ -1722,12 +1822,27 @@ int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32
   for (size_t k = 0; k < seen.size(); ++k) {
     costs[k] = found_cost[k];
     word_off[k] = pos;
-    if (pos + (int64_t)seen[k].size() <= words_cap)
-      std::copy(seen[k].begin(), seen[k].end(), words + pos);
+    if (pos + (int64_t)seen[k].size() <= words_cap) std::copy(seen[k].begin(), seen[k].end(), words + pos);
     pos += (int64_t)seen[k].size();
   }
   word_off[seen.size()] = pos;
   return need > words_cap ? -2 : 0;
+}
+
+}  // namespace
+
+int ctw_lattice_nbest(const ctw_lattice* lat, int32_t n, int64_t max_pops, int32_t* words, int64_t words_cap,
+                      int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops) {
+  return lattice_nbest(lat, nullptr, n, max_pops, words, words_cap, word_off, costs, n_found, pops);
+}
+
+int ctw_lattice_nbest_phrases(const ctw_lattice* lat, int32_t fsa_states, const int32_t* goto_off,
+                              const int32_t* goto_word, const int32_t* goto_next, const int32_t* fail_link,
+                              const double* out_cost, int32_t n, int64_t max_pops, int32_t* words,
+                              int64_t words_cap, int64_t* word_off, double* costs, int32_t* n_found, int64_t* pops) {
+  if (fsa_states <= 0) return fail(-1, "phrase automaton needs at least the root state");
+  PhraseFsa F{fsa_states, goto_off, goto_word, goto_next, fail_link, out_cost};
+  return lattice_nbest(lat, &F, n, max_pops, words, words_cap, word_off, costs, n_found, pops);
 }
 
 }  // extern "C"

@@ -71,8 +71,10 @@ class Lattice:
     def num_arcs(self) -> int:
         return len(self.src)
 
-    def nbest(self, n: int, max_pops: int = 2_000_000) -> list[Hypothesis]:
-        """The n lowest-cost distinct word sequences, best first."""
+    def nbest(self, n: int, max_pops: int = 2_000_000, phrases: "PhraseBoost | None" = None) -> list[Hypothesis]:
+        """The n lowest-cost distinct word sequences, best first; with
+        ``phrases``, costs include the phrase automaton's (multi-word
+        boosting by lattice rescoring)."""
         if n <= 0:
             return []
         L = _lib.load()
@@ -83,8 +85,15 @@ class Lattice:
             costs = np.zeros(n, np.float64)
             found = C.c_int32()
             pops = C.c_int64()
-            rc = L.ctw_lattice_nbest(C.byref(self._c), n, max_pops, _lib.ptr(words), cap, _lib.ptr(off),
-                                     _lib.ptr(costs), C.byref(found), C.byref(pops))
+            if phrases is None:
+                rc = L.ctw_lattice_nbest(C.byref(self._c), n, max_pops, _lib.ptr(words), cap, _lib.ptr(off),
+                                         _lib.ptr(costs), C.byref(found), C.byref(pops))
+            else:
+                f = phrases
+                rc = L.ctw_lattice_nbest_phrases(C.byref(self._c), f.num_states, _lib.ptr(f.goto_off),
+                                                 _lib.ptr(f.goto_word), _lib.ptr(f.goto_next), _lib.ptr(f.fail),
+                                                 _lib.ptr(f.out_cost), n, max_pops, _lib.ptr(words), cap,
+                                                 _lib.ptr(off), _lib.ptr(costs), C.byref(found), C.byref(pops))
             if rc == -2:
                 cap = int(off[int(found.value)]) + 16
                 continue
@@ -92,6 +101,75 @@ class Lattice:
             self.last_pops = int(pops.value)
             return [Hypothesis(tuple(int(x) for x in words[off[k]:off[k + 1]]), float(costs[k]), self.frame_count)
                     for k in range(int(found.value))]
+
+
+class PhraseBoost:
+    """Multi-word (phrase) boosting as a deterministic Aho-Corasick automaton
+    over word ids. ``phrases`` maps a word-id tuple to a magnitude; like the
+    reference's word tables (boosting.py:33-55) a boost of m is the cost -m,
+    paid once per occurrence of the phrase in a hypothesis (overlapping and
+    nested occurrences all count). A one-word phrase is the reference's word
+    boost; longer phrases are beyond the reference.
+    Applied by ``Lattice.nbest(n, phrases=...)`` (lattice rescoring)."""
+
+    def __init__(self, phrases: dict):
+        children = [{}]
+        own = [0.0]
+        for ph, mag in phrases.items():
+            ph = tuple(int(w) for w in ph)
+            if not ph or any(w <= 0 for w in ph):
+                raise ValueError("phrases are non-empty tuples of word ids > 0")
+            s = 0
+            for w in ph:
+                nxt = children[s].get(w)
+                if nxt is None:
+                    nxt = len(children)
+                    children[s][w] = nxt
+                    children.append({})
+                    own.append(0.0)
+                s = nxt
+            own[s] += -float(mag)
+        n = len(children)
+        fail = [0] * n
+        out = list(own)
+        order = []
+        queue = list(children[0].values())
+        order.extend(queue)
+        while queue:  # breadth first: failure links and accumulated outputs
+            nq = []
+            for s in queue:
+                for w, t in children[s].items():
+                    f = fail[s]
+                    while f and w not in children[f]:
+                        f = fail[f]
+                    fail[t] = children[f][w] if (w in children[f] and children[f][w] != t) else 0
+                    nq.append(t)
+            for t in nq:
+                out[t] = own[t] + out[fail[t]]
+            queue = nq
+        self.num_states = n
+        offs, ws, ns = [0], [], []
+        for s in range(n):
+            for w in sorted(children[s]):
+                ws.append(w)
+                ns.append(children[s][w])
+            offs.append(len(ws))
+        self.goto_off = np.asarray(offs, np.int32)
+        self.goto_word = np.asarray(ws or [0], np.int32)
+        self.goto_next = np.asarray(ns or [0], np.int32)
+        self.fail = np.asarray(fail, np.int32)
+        self.out_cost = np.asarray(out, np.float64)
+        self._children = children
+
+    def cost(self, words) -> float:
+        """Boost cost of a word sequence under the automaton."""
+        s, c = 0, 0.0
+        for w in words:
+            while s and w not in self._children[s]:
+                s = int(self.fail[s])
+            s = self._children[s].get(w, 0)
+            c += float(self.out_cost[s])
+        return c
 
 
 def decode_lattices(graph, config, utterances: Sequence, lattice_beam: float = 6.0, boost=None, *,
@@ -128,4 +206,4 @@ def build_lattices(pool, states, mats, on_dev, packed, hyps, lattice_beam: float
     return res
 
 
-__all__ = ["Lattice", "decode_lattices", "DecodeFailure"]
+__all__ = ["Lattice", "PhraseBoost", "decode_lattices", "DecodeFailure"]

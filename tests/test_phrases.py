@@ -1,0 +1,90 @@
+"""Phrase (multi-word) boosting: the Aho-Corasick automaton against brute
+force on the CPU; lattice rescoring with it against path enumeration on the
+GPU. One-word phrases are the reference's word boost (boosting.py:58-67:
+every arc with that output label pays the table cost); longer phrases are
+beyond the reference."""
+
+import random
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+
+
+def test_automaton_matches_brute_force():
+    import lattice_oracle as lo
+
+    from paper_2311_04996_b200 import PhraseBoost
+
+    rng = random.Random(0)
+    for _ in range(400):
+        phr = {}
+        for _ in range(rng.randint(1, 6)):
+            ph = tuple(rng.randint(1, 4) for _ in range(rng.randint(1, 3)))
+            phr[ph] = phr.get(ph, 0.0) + rng.uniform(0.5, 3.0)
+        pb = PhraseBoost(phr)
+        w = [rng.randint(1, 5) for _ in range(rng.randint(0, 12))]
+        assert abs(pb.cost(w) - lo.phrase_cost(w, phr)) <= 1e-9
+
+
+def test_bad_phrases():
+    from paper_2311_04996_b200 import PhraseBoost
+
+    with pytest.raises(ValueError):
+        PhraseBoost({(): 1.0})
+    with pytest.raises(ValueError):
+        PhraseBoost({(0, 3): 1.0})
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(3))
+def test_lattice_rescoring_matches_enumeration(seed):
+    import lattice_oracle as lo
+
+    from paper_2311_04996_b200 import DecoderConfig, PhraseBoost, decode_lattices, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=10, num_words=30, order=2, seed=7 + seed, min_pron=1,
+                                            max_pron=3))
+    frames = synth.planted_utterances(s, 1, 10, seed=30 + seed, gap=3.0, noise=1.0)[0]
+    cfg = DecoderConfig(beam=12.0, max_active=200)
+    beam = 3.0
+    lat = decode_lattices(s.graph, cfg, [frames], lattice_beam=beam)[0]
+    plain = lat.nbest(20)
+    rng = np.random.default_rng(seed)
+    # phrases built from the lattice's own alternatives so they matter
+    words = sorted({w for h in plain for w in h.words})
+    phr = {}
+    for h in plain[1:6]:
+        if len(h.words) >= 2:
+            i = int(rng.integers(0, len(h.words) - 1))
+            phr[tuple(h.words[i:i + 2])] = float(rng.uniform(1.0, 4.0))
+    for w in words[:3]:
+        phr[(w,)] = float(rng.uniform(0.5, 2.0))
+    pb = PhraseBoost(phr)
+    got = lat.nbest(8, phrases=pb)
+    # oracle: every complete path of the kept lattice, plus brute-force phrase costs
+    import oracle as orc
+
+    ch = orc.OracleChannel.from_config(s.graph, cfg)
+    seeds = [(int(st), float(c), tuple(int(x) for x in ch.act_chain_pool[ch.act_chain_off[k]:ch.act_chain_off[k + 1]]))
+             for k, (st, c) in enumerate(zip(ch.act_state, ch.act_cost))]
+    ch.advance_frames(frames)
+    recs = [[(r[2], r[3]) for r in fr] for fr in ch.history_records()]
+    ora = lo.lattice(s.graph, cfg.acoustic_scale, np.asarray(frames, np.float64), seeds, recs, beam)
+    want = lo.nbest(ora, lo.kept(ora, beam), seeds, 8, np.asarray(s.graph.final, np.float64),
+                    bound=float("inf"), phrases=phr)
+    assert got and want
+    for (w, c), h in zip(want, got):
+        assert abs(c - h.total_cost) <= 1e-3  # north_star n-best tolerance
+    wmap = dict(want)
+    for h in got:
+        if h.words in wmap:
+            assert abs(wmap[h.words] - h.total_cost) <= 1e-3
+    # consistency with the plain n-best: rescoring = plain cost + phrase cost
+    pmap = {h.words: h.total_cost for h in lat.nbest(200)}
+    for h in got:
+        if h.words in pmap:
+            assert abs(pmap[h.words] + pb.cost(h.words) - h.total_cost) <= 1e-9
