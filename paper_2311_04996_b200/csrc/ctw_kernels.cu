@@ -266,6 +266,7 @@ struct FrameCtr {
   int nbb;      // boundary-bin members collected
   int rec_ctr;  // survivors written (records of the frame)
   int nslot;    // slots allocated (the slot list's fill)
+  int nib;      // in-beam slots compacted by the count pass
   uint32_t bhist[CTW_NB];      // cost histogram over [min, min + beam]
 };
 
@@ -734,8 +735,8 @@ __device__ __forceinline__ int cmp_prefix(unsigned long long key, uint32_t state
 // prefix bucket is taken whole. Every rank histograms its own slots into rank
 // 0's digit histogram; rank 0 fixes the digit. Leaves (l_ph, l_pl, l_depth)
 // in every rank.
-__device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, int n_all, unsigned long long cut_key,
-                             long long k) {
+__device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, const uint2* ib, int n_all,
+                             unsigned long long cut_key, long long k) {
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
   Smem* G = L.G;
@@ -762,7 +763,7 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, i
     for (int i = L.sw0 + tid; i < n_all; i += L.swstride) {
       const unsigned long long key = sv[i].x;
       if (key > cut_key) continue;
-      const uint32_t st = L.slots[i].y;
+      const uint32_t st = ib[i].y;
       if (cmp_prefix(key, st, d, ph, pl) != 0) continue;
       atomicAdd(&sm.hist[digit_of(key, st, d)], 1u);
     }
@@ -874,8 +875,13 @@ __device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost,
 // CTW_ERR_EPS_ITERS), the in-beam count and (hist) the cost histogram over
 // [min, min + beam] for the max-active select; merges them into the frame
 // counters and meets the other ranks at a barrier.
-__device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* sv, int n_all, long long max_ne_iters,
-                          unsigned long long cut_key, double min_cost, double bin_scale, bool hist) {
+// With `hist` (decoding) the in-beam slots are compacted: sv[j] = value and
+// ib[j] = (table index, state) for j < in-beam count (cluster-wide list, warp-
+// aggregated appends); the select and record stages then sweep only those.
+// Without it (seeding) sv[i] holds slot i's value for every slot.
+__device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* sv, uint2* ib, int n_all,
+                          long long max_ne_iters, unsigned long long cut_key, double min_cost, double bin_scale,
+                          bool hist) {
   const int tid = threadIdx.x;
   if (hist)
     for (int i = tid; i < CTW_NB; i += CTW_BS) sm.lbhist[i] = 0;
@@ -886,26 +892,31 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
   __syncthreads();
   int c = 0, mpd = 0;
   for (int i0 = L.sw0 + tid; i0 < n_all; i0 += CTW_UNR * L.swstride) {
-    uint32_t h[CTW_UNR];
+    uint2 h[CTW_UNR];
     ulonglong2 v[CTW_UNR];
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * L.swstride;
-      h[u] = i < n_all ? L.slots[i].x : 0u;
+      h[u] = i < n_all ? L.slots[i] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * L.swstride;
-      if (i < n_all) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u]]));
+      if (i < n_all) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u].x]));
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * L.swstride;
       if (i >= n_all) break;
-      sv[i] = v[u];
+      if (!hist) sv[i] = v[u];
       if (v[u].x <= cut_key) {
         ++c;
-        if (hist) atomicAdd(&sm.lbhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
+        if (hist) {
+          atomicAdd(&sm.lbhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
+          const int j = agg_alloc(&fc->nib, nullptr);
+          sv[j] = v[u];
+          ib[j] = h[u];
+        }
       }
       if ((uint32_t)v[u].y & CTW_EPS_BIT) mpd = max(mpd, (int)((uint32_t)(v[u].y >> 32) >> CTW_PRED_BITS));
     }
@@ -959,7 +970,8 @@ __device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_all) {
 // them exactly in shared memory (bitonic). Falls back to the cluster-wide
 // digit-wise radix select when the boundary bin overflows CTW_BBUF. Leaves
 // the threshold in every rank's l_* fields.
-__device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const ulonglong2* sv, int n_all,
+__device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const ulonglong2* sv, const uint2* ib,
+                                 int n_all,
                                  unsigned long long cut_key, double min_cost, double bin_scale, long long k) {
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
@@ -1012,14 +1024,14 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
   if (bcount == need) return;  // the whole boundary bin survives
   if (bcount > CTW_BBUF) {
     if (tid == 0) sm.l_radix = 1;
-    radix_select(sm, L, sv, n_all, cut_key, k);
+    radix_select(sm, L, sv, ib, n_all, cut_key, k);
     return;
   }
   for (int i = L.sw0 + tid; i < n_all; i += L.swstride) {
     const unsigned long long key = sv[i].x;
     if (key <= cut_key && cost_bin(key, min_cost, bin_scale) == bsel) {
       const int p = atomicAdd(&fc->nbb, 1);
-      G->bbuf[p] = make_ulonglong2(key, L.slots[i].y);
+      G->bbuf[p] = make_ulonglong2(key, ib[i].y);
     }
   }
   cl.sync();
@@ -1343,9 +1355,13 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     const double cutoff = __dadd_rn(min_cost, a.cfg.beam);
     const unsigned long long cut_key = d2key(cutoff);
     const double bin_scale = (double)CTW_NB / a.cfg.beam;
-    ulonglong2* sv = reinterpret_cast<ulonglong2*>(L.front);  // gathered values; the frontier sets are free now
+    // in-beam values and (table index, state) pairs, compacted by the count
+    // pass into the (now free) frontier sets
+    ulonglong2* sv = reinterpret_cast<ulonglong2*>(L.front);
+    uint2* ib = L.front + 2 * (size_t)L.seg;
     if (status == CTW_OK)
-      status = count_pass(sm, L, fc, sv, n_all, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
+      status = count_pass(sm, L, fc, sv, ib, n_all, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
+    const int n_ib = sm.cnt_all;
 #ifdef CTW_DEBUG
     if (status == CTW_OK && tid == 0) {
       const unsigned long long gm = *((volatile unsigned long long*)&G->min_key);
@@ -1364,7 +1380,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       if (rank == 0) prof[11] += in_beam;
       const bool select = (long long)in_beam > a.cfg.max_active;
       const int n_surv = select ? (int)a.cfg.max_active : in_beam;
-      if (select) select_threshold(sm, L, fc, sv, n_all, cut_key, min_cost, bin_scale, a.cfg.max_active);
+      if (select) select_threshold(sm, L, fc, sv, ib, n_ib, cut_key, min_cost, bin_scale, a.cfg.max_active);
       if (rank == 0 && tid == 0) {
         const long long t = clock64();
         prof[3] += t - tclk;
@@ -1397,17 +1413,17 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           return bb < bsel || (bb == bsel && (key < tk || (key == tk && state <= ts)));
         };
         int mine = 0;
-        for (int i = L.sw0 + tid; i < n_all; i += L.swstride) mine += keep(sv[i].x, L.slots[i].y);
+        for (int i = L.sw0 + tid; i < n_ib; i += L.swstride) mine += keep(sv[i].x, ib[i].y);
         int pos, tot;
         Smem::Scan(sm.scan).ExclusiveSum(mine, pos, tot);
         if (tid == 0) sm.rbase = atomicAdd(&fc->rec_ctr, tot);
         __syncthreads();
         pos += sm.rbase;
         const int hop_cap = n_all + 2;
-        for (int i = L.sw0 + tid; i < n_all; i += L.swstride) {
+        for (int i = L.sw0 + tid; i < n_ib; i += L.swstride) {
           const ulonglong2 v0 = sv[i];
           const unsigned long long key = v0.x;
-          const uint2 it = L.slots[i];
+          const uint2 it = ib[i];
           const uint32_t h = it.x, st2 = it.y;
           if (!keep(key, st2)) continue;
           const CtwStateRange rg = g.ranges[st2];  // independent of the walk: overlaps it
@@ -1554,7 +1570,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
   if (status == CTW_OK && (uint32_t)sm.n_slots > L.seg) status = CTW_GROW_TABLE;
   if (status == CTW_OK && n_own > lane.scap) status = CTW_GROW_SRC;
   ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);
-  if (status == CTW_OK) status = count_pass(sm, L, fc, sv, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
+  if (status == CTW_OK) status = count_pass(sm, L, fc, sv, nullptr, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
   if (status == CTW_OK) {
     CtwSrc* dst = lane.src[0];
     for (int i = tid; i < n_own; i += CTW_BS) {
