@@ -143,6 +143,15 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
 /* Replace a lane's boost vector without re-seeding (the reference reads
  * DecodeState.boost at every advance, decoder.py:287-305, so assigning
  * ch.boost between chunks takes effect from the next frame). */
+/* Phrase boosting inside the search (on-the-fly composition with a
+ * multi-state boost FST; beyond the reference's one-state word boost,
+ * boosting.py:75-86). A deterministic automaton over word labels:
+ * next[b * (max_olabel + 1) + w] is the state after word w from state b,
+ * cost[b] the cost paid on entering b (negative = boost). Token keys become
+ * (graph state | automaton state << ceil(log2 num_states)); recorded and
+ * exported states are those keys. Takes effect at the next ctw_lane_reset;
+ * n_states = 0 removes it. */
+int ctw_lane_set_fsa(ctw_lanes* l, int32_t lane, int32_t n_states, const uint16_t* next, const double* cost);
 int ctw_lane_set_boost(ctw_lanes* l, int32_t lane, const double* boost, int64_t boost_len);
 
 /* Advance n lanes by one chunk each. loglik rows are `width` wide, dtype 0 =

@@ -34,7 +34,7 @@
 
 extern "C" int ctw_launch_decode(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                  const double*, const void*, int, int, const long long*, const int*,
-                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, cudaStream_t);
+                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, int, cudaStream_t);
 extern "C" int ctw_launch_seed(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                const double*, const int*, int, int, const CtwDecodeCfg*, CtwLaneOut*,
                                cudaStream_t);
@@ -137,6 +137,11 @@ struct ctw_lanes {
   std::vector<CtwSrc*> seed_src;
   std::vector<int32_t*> seed_pend;
   std::vector<int32_t> seed_n, seed_cap;
+  // phrase automata (ctw_lane_set_fsa), device copies per lane
+  std::vector<uint16_t*> fsa_next;
+  std::vector<double*> fsa_cost;
+  std::vector<int64_t> fsa_cap;
+  std::vector<double> fsa_min;  // most negative entry cost (early-pruning exactness)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   // scratch
@@ -324,6 +329,7 @@ int init_lane(ctw_lanes* l, int i) {
   const uint32_t tlog2 = std::max(std::min<uint32_t>(std::max<uint32_t>(6, ceil_log2(2 * S + 2)), 16),
                                   std::min<uint32_t>(l->tlog2_hint, ceil_log2(2 * S + 2)));
   if (int r = alloc_table(l, i, tlog2)) return r;
+  L.smask = 0xFFFFFFFFu;
   L.rcap = 0;
   L.fcap = 256;
   L.pcap = 1 << 10;
@@ -385,6 +391,10 @@ int reserve_lanes(ctw_lanes* l, int n) {
   l->seed_pend.resize(n, nullptr);
   l->seed_n.resize(n, 0);
   l->seed_cap.resize(n, 0);
+  l->fsa_next.resize(n, nullptr);
+  l->fsa_cost.resize(n, nullptr);
+  l->fsa_cap.resize(n, 0);
+  l->fsa_min.resize(n, 0.0);
   for (int i = l->n; i < n; ++i) {
     if (int r = init_lane(l, i)) return r;
   }
@@ -718,6 +728,8 @@ void ctw_lanes_destroy(ctw_lanes* l) {
     dfree(l->boost_buf[i]);
     sfree(l->seed_src[i], l->stream);
     sfree(l->seed_pend[i], l->stream);
+    dfree(l->fsa_next[i]);
+    dfree(l->fsa_cost[i]);
   }
   for (CtwRecPage* p : l->slabs) sfree(p, l->stream);
   cudaStreamSynchronize(l->stream);
@@ -778,7 +790,7 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
       L.boost = nullptr;
       L.boost_len = 0;
     }
-    L.prune_ok = prune_flag(l, b, b ? boost_lens[i] : 0);
+    L.prune_ok = prune_flag(l, b, b ? boost_lens[i] : 0) && !(L.fsa_next && l->g->eps_olabel && l->fsa_min[lane] < 0);
     L.n_src = 0;
     L.src_buf = 0;
     L.frame_count = 0;
@@ -837,9 +849,54 @@ int ctw_lane_set_boost(ctw_lanes* l, int32_t lane, const double* boost, int64_t 
     L.boost = nullptr;
     L.boost_len = 0;
   }
-  L.prune_ok = prune_flag(l, boost, boost_len);
+  L.prune_ok = prune_flag(l, boost, boost_len) && !(L.fsa_next && l->g->eps_olabel && l->fsa_min[lane] < 0);
   if (int r = sync_lane(l, lane)) return r;
   CUDA_TRY(cudaStreamSynchronize(l->stream));
+  return 0;
+}
+
+int ctw_lane_set_fsa(ctw_lanes* l, int32_t lane, int32_t n_states, const uint16_t* next, const double* cost) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (lane < 0 || lane >= l->n) return fail(-1, "lane id out of range");
+  CtwLane& L = l->h[lane];
+  if (n_states <= 0) {
+    L.fsa_next = nullptr;
+    L.fsa_cost = nullptr;
+    L.fsa_states = L.fsa_width = 0;
+    L.sbits = 0;
+    L.smask = 0xFFFFFFFFu;
+    l->fsa_min[lane] = 0.0;
+    return sync_lane(l, lane);
+  }
+  const uint32_t sbits = std::max<uint32_t>(1, ceil_log2((uint64_t)l->g->S));
+  if (sbits >= 32 || (uint64_t)n_states > ((1ull << (32 - sbits)) - 1))
+    return fail(-1, "phrase automaton has too many states for this graph's token keys");
+  const int64_t width = l->g->max_ol + 1;
+  const int64_t cells = (int64_t)n_states * width;
+  for (int64_t k = 0; k < cells; ++k)
+    if (next[k] >= n_states) return fail(-1, "phrase automaton transition out of range");
+  if (l->fsa_cap[lane] < cells) {
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    dfree(l->fsa_next[lane]);
+    dfree(l->fsa_cost[lane]);
+    CUDA_TRY(dalloc(&l->fsa_next[lane], (size_t)cells));
+    CUDA_TRY(dalloc(&l->fsa_cost[lane], (size_t)std::max<int64_t>(cells / width, n_states)));
+    l->fsa_cap[lane] = cells;
+  }
+  CUDA_TRY(cudaMemcpyAsync(l->fsa_next[lane], next, (size_t)cells * 2, cudaMemcpyHostToDevice, l->stream));
+  CUDA_TRY(cudaMemcpyAsync(l->fsa_cost[lane], cost, (size_t)n_states * 8, cudaMemcpyHostToDevice, l->stream));
+  double mn = 0.0;
+  for (int32_t b = 0; b < n_states; ++b) mn = std::min(mn, cost[b]);
+  l->fsa_min[lane] = mn;
+  L.fsa_next = l->fsa_next[lane];
+  L.fsa_cost = l->fsa_cost[lane];
+  L.fsa_states = n_states;
+  L.fsa_width = (int32_t)width;
+  L.sbits = sbits;
+  L.smask = (1u << sbits) - 1u;
+  if (int r = sync_lane(l, lane)) return r;
+  CUDA_TRY(cudaStreamSynchronize(l->stream));  // host arrays may go away
   return 0;
 }
 
@@ -901,8 +958,10 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     CUDA_TRY(cudaMemcpyAsync(l->d_nframes, l->h_nframes, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
     CUDA_TRY(cudaMemcpyAsync(l->d_lloff, l->h_lloff, m * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
     CUDA_TRY(cudaEventRecord(l->ev0, l->stream));
+    int any_fsa = 0;
+    for (int k = 0; k < m; ++k) any_fsa |= l->h[todo[k]].fsa_next != nullptr;
     if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
-                          l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, l->stream))
+                          l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, l->stream))
       return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
     CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
     l->launches++;
@@ -1475,6 +1534,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
         CUDA_TRY(cudaMemcpy(hb.data(), L.boost, hb.size() * 8, cudaMemcpyDeviceToHost));
         for (double x : hb) bmin = std::min(bmin, x);
       }
+      if (L.fsa_next) bmin = std::min(bmin, l->fsa_min[lane]);
       e.emit_lb = g->w_min_emit + bmin;
       ent[k] = e;
     }
@@ -1574,7 +1634,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
         o.arc_src_state[k2] = a.src_state;
         o.arc_w[k2] = a.w;
         double fw = INF;
-        if (a.frame == T - 1) fw = e.final_mode ? g->h_final[a.dst_state] : 0.0;
+        if (a.frame == T - 1) fw = e.final_mode ? g->h_final[(uint32_t)a.dst_state & L.smask] : 0.0;
         o.arc_dst_final[k2] = fw;
         if (a.code > 0) al.push_back(a.code);
         else if (a.code < 0) {

@@ -127,6 +127,12 @@ struct CtwLane {
   // epsilon increments are >= 0 (graph weights and, when epsilon arcs carry
   // olabels, the boost) and max_ne_iters is not a tight cap. Set by the host.
   int32_t prune_ok;
+  // phrase automaton (ctw_lane_set_fsa): token keys = graph state | automaton
+  // state << sbits; smask recovers the graph state (all ones without one)
+  const uint16_t* fsa_next;  // [fsa_states x fsa_width] next automaton state per word label
+  const double* fsa_cost;    // [fsa_states] cost of entering the state (negative = boost)
+  int32_t fsa_states, fsa_width;
+  uint32_t sbits, smask;
 };
 
 // Per-launch result of one lane.

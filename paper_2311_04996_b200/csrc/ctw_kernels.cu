@@ -60,7 +60,7 @@
 #define CTW_ETILE (CTW_BS * CTW_EIPT)
 #define CTW_DISC 0xFFFFFFFFu             // epsilon tile item: discovery only (no value)
 #define CTW_NB 1024      // cost-histogram bins over [min, min + beam] for the max-active select
-#define CTW_BBUF 1024    // boundary-bin capacity of the exact (cost, state) sort
+#define CTW_BBUF 512     // boundary-bin capacity of the exact (cost, state) sort
 
 namespace cg = cooperative_groups;
 
@@ -126,7 +126,32 @@ struct LaneCtx {
   int32_t* pool;
   bool prune;    // CtwLane::prune_ok
   int* tie_ctr;  // diagnostics: epsilon/epsilon ties between distinct predecessors
+  // phrase automaton (on-the-fly composition with a multi-state boost FST):
+  // token key = graph state | automaton state << sbits; null fnext = none
+  const uint16_t* fnext;
+  const double* fcost;
+  int32_t fwidth;
+  uint32_t sbits, smask;
 };
+
+// Destination key and boost of an arc with output label ol leaving the token
+// with key `key` (reference order: the boost is added after the arc weight,
+// _kernel.pyx:251-252): the dense word table, or the phrase automaton's
+// transition (the key carries the automaton state; only word arcs move it).
+template <bool FSA>
+__device__ __forceinline__ uint32_t arc_dest(const LaneCtx& L, const double* boost, uint32_t key, int32_t ol,
+                                             uint32_t nextstate, double& nc) {
+  if (FSA && L.fnext) {
+    uint32_t b = key >> L.sbits;
+    if (ol != 0) {
+      b = L.fnext[(size_t)b * L.fwidth + ol];
+      nc = __dadd_rn(nc, L.fcost[b]);
+    }
+    return nextstate | (b << L.sbits);
+  }
+  if (boost && ol != 0) nc = __dadd_rn(nc, boost[ol]);
+  return nextstate;
+}
 
 // Find-or-insert `d` (linear probing). Returns the table index or CTW_EMPTY
 // when the table is full.
@@ -248,7 +273,7 @@ __device__ __forceinline__ void tok_clear(CtwTok* e) {
 
 // --------------------------------------------------------- shared memory --
 
-#define CTW_NBIG 1024  // high out-degree sources expanded arc-parallel per frame (list capacity)
+#define CTW_NBIG 512   // high out-degree sources expanded arc-parallel per frame (list capacity)
 #ifndef CTW_BIG
 #define CTW_BIG 64  // emitting out-degree above which a source is expanded arc-parallel
 #endif
@@ -275,7 +300,7 @@ struct BigSrc {
   int32_t idx;  // source index (emitting winners' aux)
   uint32_t beg;
   int32_t deg;
-  int32_t pad;
+  uint32_t key;  // source token key
   double cost;
 };
 
@@ -290,7 +315,6 @@ struct __align__(16) Smem {
     } em;
     struct {  // epsilon closure: each warp's current chunk of 32 frontier items
       double cost[CTW_WARPS][32];
-      unsigned long long gb[CTW_WARPS][32];  // slot-position prefix handed to discovered successors
       unsigned long long gu[CTW_WARPS][32];  // the item's own slot position (tie-break)
       int off[CTW_WARPS][32];
       uint32_t beg[CTW_WARPS][32];
@@ -303,6 +327,11 @@ struct __align__(16) Smem {
       double cost[CTW_NBIG];
     } bg;
     ulonglong2 bbuf[CTW_BBUF];  // rank 0: max-active boundary bin (cost key, state)
+    struct {  // count / select stages (the expansion buffers are free then)
+      uint32_t lbhist[CTW_NB];  // local cost histogram
+      uint32_t hist[256];       // local digit histogram (radix select)
+      uint32_t rhist[2][256];   // rank 0: merged radix digit histogram (digit parity)
+    } cs;
   };
   // ---- cluster fields: meaningful in rank 0 only, reached through DSMEM ----
   FrameCtr fc[2];
@@ -317,7 +346,6 @@ struct __align__(16) Smem {
   int sel_depth;              // digits fixed; survivor iff top digits <= prefix
   int rneed;
   int sel_done;
-  uint32_t rhist[2][256];     // radix digit histogram (digit parity)
   // ---- per-rank fields ----
   int status_l;         // sticky local status (grow requests, walk failures)
   int st_pub[2];        // status published at a barrier (barrier parity)
@@ -333,8 +361,6 @@ struct __align__(16) Smem {
   uint2* in1;
   int work;             // this rank's chunk counter (rank-local sweeps)
   unsigned long long min_key;  // running minimum seen by this rank (>= the cluster's)
-  uint32_t hist[256];          // local digit histogram (radix select)
-  uint32_t lbhist[CTW_NB];     // local cost histogram
   int n_all;            // slots of all ranks (after the closure)
   int cnt_l, mpd_l, cnt_all, mpd_all;
   int nbig;
@@ -418,32 +444,39 @@ __device__ __forceinline__ int csync(Smem& sm) {
 // (c + w) (+ boost), find-or-insert the destination, update its slot
 // position, install the candidate if it wins the Gauss-Seidel order, and
 // queue the destination for the next pass when it changed.
+template <bool FSA>
 __device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const double* boost,
                                         double relax_eps, uint32_t epoch, int q, int* ctr_out, uint2* nxt,
-                                        uint2* tiny, int w, int lo, uint32_t o, uint32_t a, const CtwArc& arc) {
+                                        uint2* tiny, int w, int lo, uint32_t o, uint32_t a, const CtwArc& arc,
+                                        uint32_t ikey) {
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
   const uint32_t aux = sm.ep.aux[w][lo];
   const bool valued = aux != CTW_DISC;
-  double nc = arc.weight;
-  if (valued) {
-    nc = __dadd_rn(sm.ep.cost[w][lo], arc.weight);
-    if (boost) {
-      const int32_t ol = g.olabel[a];
-      if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
-    }
+  double nc = valued ? __dadd_rn(sm.ep.cost[w][lo], arc.weight) : arc.weight;
+  uint32_t dkey = (uint32_t)arc.nextstate;
+  if (FSA) {
+    double nb = nc;
+    dkey = arc_dest<FSA>(L, boost, ikey, g.olabel[a], (uint32_t)arc.nextstate, nb);
+    if (valued) nc = nb;
+  } else if (boost && valued) {
+    const int32_t ol = g.olabel[a];
+    if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
   }
   if (!(nc < INF)) return;
   bool is_new = false;
   ulonglong2 seen;
-  const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
+  const uint32_t d = tok_locate(L, dkey, &seen, is_new);
   if (d == CTW_EMPTY) {
     atomicMax(&sm.status_l, CTW_GROW_TABLE);
     return;
   }
-  if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
+  if (is_new) slot_append(sm, L, d, dkey);
   CtwTok* ed = &L.T[d];
-  gpos_min(ed, sm.ep.gb[w][lo] | min(o, 15u));
-  const uint2 item = make_uint2(d, (uint32_t)arc.nextstate);
+  // slot-position chain key handed to a discovered successor:
+  // level + 1, discoverer's key << 4 | arc offset
+  const unsigned long long gu = sm.ep.gu[w][lo];
+  gpos_min(ed, ((((gu >> 56) + 1) << 56) | ((gu << 4) & CTW_KEY56)) | min(o, 15u));
+  const uint2 item = make_uint2(d, dkey);
   bool push = false, big = false;
   if (valued) {
     unsigned long long oldk;
@@ -497,6 +530,7 @@ __device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphD
 // 32-item chunks over the virtual concatenation of the ranks' input segments;
 // every rank pushes to its own output segments. Returns CTW_OK or
 // CTW_ERR_EPS_ITERS (divergence: more passes than a convergent closure needs).
+template <bool FSA>
 __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, FrameCtr* fc, const double* boost,
                             double relax_eps, double beam, long long pass_cap) {
   cg::cluster_group cl = cg::this_cluster();
@@ -566,7 +600,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
         const uint2 it = i < n_first ? in0[i] : in1[i - n_first];
         // the range and the entry are independent loads: issue them together
         const CtwTok* eu = &L.T[it.x];
-        const CtwStateRange r = g.ranges[it.y];
+        const CtwStateRange r = g.ranges[FSA ? (it.y & L.smask) : it.y];
         const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
         const unsigned long long gu = __ldcg(&eu->gpos);
         deg = (int)(r.emit_beg - r.eps_beg);
@@ -586,7 +620,6 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
           }
           sm.ep.cost[w][lane] = c;
           sm.ep.gu[w][lane] = gu;
-          sm.ep.gb[w][lane] = (((gu >> 56) + 1) << 56) | ((gu << 4) & CTW_KEY56);
           sm.ep.beg[w][lane] = r.eps_beg;
           sm.ep.aux[w][lane] = aux;
         }
@@ -616,7 +649,12 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
         const uint32_t o = (uint32_t)(k - sm.ep.off[w][lo]);
         const uint32_t a = sm.ep.beg[w][lo] + o;
         const CtwArc arc = g.arcs[a];
-        eps_arc(sm, L, g, boost, relax_eps, epoch, q, ctr_out, nxt, tiny, w, lo, o, a, arc);
+        uint32_t ikey = 0;  // the item's token key (phrase automaton state)
+        if (FSA) {
+          const int ii = base + lo;
+          ikey = (ii < n_first ? in0[ii] : in1[ii - n_first]).y;
+        }
+        eps_arc<FSA>(sm, L, g, boost, relax_eps, epoch, q, ctr_out, nxt, tiny, w, lo, o, a, arc, ikey);
       }
       __syncwarp();
     }
@@ -748,7 +786,7 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, c
       sm.rneed = (int)k;
       sm.sel_done = 0;
     }
-    for (int i = tid; i < 256; i += CTW_BS) sm.rhist[0][i] = 0;
+    for (int i = tid; i < 256; i += CTW_BS) sm.cs.rhist[0][i] = 0;
   }
   cl.sync();
   for (int d = 0; d < 12; ++d) {
@@ -756,7 +794,7 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, c
       sm.l_ph = *((volatile unsigned long long*)&G->sel_hi);
       sm.l_pl = *((volatile uint32_t*)&G->sel_lo);
     }
-    for (int i = tid; i < 256; i += CTW_BS) sm.hist[i] = 0;
+    for (int i = tid; i < 256; i += CTW_BS) sm.cs.hist[i] = 0;
     __syncthreads();
     const unsigned long long ph = sm.l_ph;
     const uint32_t pl = sm.l_pl;
@@ -765,20 +803,20 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, c
       if (key > cut_key) continue;
       const uint32_t st = ib[i].y;
       if (cmp_prefix(key, st, d, ph, pl) != 0) continue;
-      atomicAdd(&sm.hist[digit_of(key, st, d)], 1u);
+      atomicAdd(&sm.cs.hist[digit_of(key, st, d)], 1u);
     }
     __syncthreads();
     for (int i = tid; i < 256; i += CTW_BS)
-      if (sm.hist[i]) atomicAdd(&G->rhist[d & 1][i], sm.hist[i]);
+      if (sm.cs.hist[i]) atomicAdd(&G->cs.rhist[d & 1][i], sm.cs.hist[i]);
     if (L.rank == 0)
-      for (int i = tid; i < 256; i += CTW_BS) sm.rhist[(d + 1) & 1][i] = 0;
+      for (int i = tid; i < 256; i += CTW_BS) sm.cs.rhist[(d + 1) & 1][i] = 0;
     cl.sync();
     if (L.rank == 0 && tid < 32) {
       // warp 0 of rank 0: locate the bucket holding the need-th smallest
       uint32_t c[8];
       uint32_t sum = 0;
       for (int j = 0; j < 8; ++j) {
-        c[j] = sm.rhist[d & 1][tid * 8 + j];
+        c[j] = sm.cs.rhist[d & 1][tid * 8 + j];
         sum += c[j];
       }
       uint32_t incl = sum;
@@ -803,7 +841,7 @@ __device__ void radix_select(Smem& sm, const LaneCtx& L, const ulonglong2* sv, c
         else sm.sel_lo = (sm.sel_lo << 8) | (uint32_t)b;
         sm.sel_depth = d + 1;
         sm.rneed = (int)rem;
-        if (sm.rhist[d & 1][b] == rem) sm.sel_done = 1;
+        if (sm.cs.rhist[d & 1][b] == rem) sm.sel_done = 1;
       }
     }
     cl.sync();
@@ -850,6 +888,11 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int n
   L.pool_cap = lane.pcap;
   L.prune = lane.prune_ok != 0;
   L.tie_ctr = nullptr;
+  L.fnext = lane.fsa_next;
+  L.fcost = lane.fsa_cost;
+  L.fwidth = lane.fsa_width;
+  L.sbits = lane.sbits;
+  L.smask = lane.smask;
   return L;
 }
 
@@ -884,7 +927,7 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
                           bool hist) {
   const int tid = threadIdx.x;
   if (hist)
-    for (int i = tid; i < CTW_NB; i += CTW_BS) sm.lbhist[i] = 0;
+    for (int i = tid; i < CTW_NB; i += CTW_BS) sm.cs.lbhist[i] = 0;
   if (tid == 0) {
     sm.cnt_l = 0;
     sm.mpd_l = 0;
@@ -912,7 +955,7 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
       if (v[u].x <= cut_key) {
         ++c;
         if (hist) {
-          atomicAdd(&sm.lbhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
+          atomicAdd(&sm.cs.lbhist[cost_bin(v[u].x, min_cost, bin_scale)], 1u);
           const int j = agg_alloc(&fc->nib, nullptr);
           sv[j] = v[u];
           ib[j] = h[u];
@@ -932,7 +975,7 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
   __syncthreads();
   if (hist)
     for (int i = tid; i < CTW_NB; i += CTW_BS) {
-      const uint32_t n = sm.lbhist[i];
+      const uint32_t n = sm.cs.lbhist[i];
       if (n) atomicAdd(&fc->bhist[i], n);
     }
   if (tid == 0) {
@@ -1072,10 +1115,11 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
 // Relax one emitting arc: ((c + (-scale * ll)) + w) (+ boost), then
 // find-or-insert the destination and install the candidate if it wins
 // (_kernel.pyx:243-287).
+template <bool FSA>
 __device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
                                                 const double* nll_s, bool smem_ll, long long row0, double neg_scale,
                                                 const double* boost, uint32_t arc_i, double cost, uint32_t src_idx,
-                                                const CtwArc& arc) {
+                                                uint32_t src_key, const CtwArc& arc) {
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
   double ac;
   if (smem_ll) ac = nll_s[arc.ilabel - 1];
@@ -1085,19 +1129,21 @@ __device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, cons
     ac = __dmul_rn(neg_scale, x);
   }
   double nc = __dadd_rn(__dadd_rn(cost, ac), arc.weight);
-  if (boost) {
+  uint32_t dkey = (uint32_t)arc.nextstate;
+  if (FSA) dkey = arc_dest<FSA>(L, boost, src_key, g.olabel[arc_i], (uint32_t)arc.nextstate, nc);
+  else if (boost) {
     const int32_t ol = g.olabel[arc_i];
     if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
   }
   if (!(nc < INF)) return;
   bool is_new = false;
   ulonglong2 seen;
-  const uint32_t d = tok_locate(L, (uint32_t)arc.nextstate, &seen, is_new);
+  const uint32_t d = tok_locate(L, dkey, &seen, is_new);
   if (d == CTW_EMPTY) {
     atomicMax(&sm.status_l, CTW_GROW_TABLE);
     return;
   }
-  if (is_new) slot_append(sm, L, d, (uint32_t)arc.nextstate);
+  if (is_new) slot_append(sm, L, d, dkey);
   CtwTok* ed = &L.T[d];
   // Gauss-Seidel slot position of an emitting-reached state = its
   // first-arrival arc (_kernel.pyx:256-272)
@@ -1108,13 +1154,18 @@ __device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, cons
   if (tok_relax_from(L, ed, nk, arc_i, src_idx, 0ULL, seen, &oldk)) track_min(sm, nk);
 }
 
+template <bool FSA>
 __device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
                                          const double* nll_s, bool smem_ll, long long row0, double neg_scale,
-                                         const double* boost, uint32_t arc_i, double cost, uint32_t src_idx) {
+                                         const double* boost, uint32_t arc_i, double cost, uint32_t src_idx,
+                                         uint32_t src_key) {
   const CtwArc arc = g.arcs[arc_i];
-  emit_arc_loaded(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, arc_i, cost, src_idx, arc);
+  emit_arc_loaded<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, arc_i, cost, src_idx, src_key, arc);
 }
 
+// FSA: some lane of the launch has a phrase automaton (token keys carry its
+// state); the plain instantiation keeps the hot path free of it.
+template <bool FSA>
 __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
   extern __shared__ double nll_s[];
   __shared__ Smem sm;
@@ -1229,7 +1280,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
             bs.idx = base + lane_;
             bs.beg = r.emit_beg;
             bs.deg = deg;
-            bs.pad = 0;
+            bs.key = 0;
             bs.cost = t.cost;
             bigl[j] = bs;
             deg = 0;
@@ -1255,8 +1306,9 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           if (sm.em.off[w][mid] <= k) lo = mid;
           else hi = mid - 1;
         }
-        emit_arc(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
-                 sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]), sm.em.cost[w][lo], (uint32_t)(base + lo));
+        emit_arc<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
+                 sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]), sm.em.cost[w][lo], (uint32_t)(base + lo),
+                 FSA ? (uint32_t)src[base + lo].state : 0u);
       }
       __syncwarp();
     }
@@ -1302,8 +1354,9 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
             if (sm.bg.pref[mid] <= k) lo = mid;
             else hi = mid - 1;
           }
-          emit_arc(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
-                   sm.bg.beg[lo] + (uint32_t)(k - sm.bg.pref[lo]), sm.bg.cost[lo], (uint32_t)sm.bg.idx[lo]);
+          emit_arc<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
+                   sm.bg.beg[lo] + (uint32_t)(k - sm.bg.pref[lo]), sm.bg.cost[lo], (uint32_t)sm.bg.idx[lo],
+                   FSA ? (uint32_t)src[sm.bg.idx[lo]].state : 0u);
         }
       }
       __syncthreads();
@@ -1319,7 +1372,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     // ---- epsilon closure ----
     int st = CTW_OK;
     if (sm.st_all < CTW_GROW_TABLE)
-      st = eps_fixpoint(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
+      st = eps_fixpoint<FSA>(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
     const int vote = sm.st_all;
     if (tid == 0) {
       int tot = 0;  // slots allocated by all ranks (stable: the closure is over)
@@ -1426,7 +1479,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           const uint2 it = ib[i];
           const uint32_t h = it.x, st2 = it.y;
           if (!keep(key, st2)) continue;
-          const CtwStateRange rg = g.ranges[st2];  // independent of the walk: overlaps it
+          const CtwStateRange rg = g.ranges[FSA ? (st2 & L.smask) : st2];  // independent of the walk: overlaps it
           const WalkEnd wk = walk(L, g, v0, src, pend, hop_cap);
           if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
           const int32_t code = record_code(sm, L, g, h, wk);
@@ -1563,7 +1616,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
     sm.snap_slots = sm.n_slots;
   }
   __syncthreads();
-  int status = eps_fixpoint(sm, L, g, fc, lane.boost, cfg.relax_eps, cfg.beam,
+  int status = eps_fixpoint<true>(sm, L, g, fc, lane.boost, cfg.relax_eps, cfg.beam,
                             divergence_cap(cfg.max_ne_iters, L.tcap));
   const int n_own = min(sm.n_slots, (int)L.seg);
   if (status == CTW_OK && sm.st_all >= CTW_GROW_TABLE) status = sm.st_all;
@@ -1582,7 +1635,7 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
       s.state = (int32_t)L.slots[i].y;
       s.bp = -1;
       s.cost = key2d(v0.x);
-      const CtwStateRange rg = g.ranges[s.state];
+      const CtwStateRange rg = g.ranges[(uint32_t)s.state & L.smask];
       s.emit_beg = rg.emit_beg;
       s.emit_end = rg.emit_end;
       dst[i] = s;
@@ -1638,7 +1691,7 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
       const CtwSrc t = src[i];
       double tot;
       if (pass == 0) {
-        const double fw = g.final_w[t.state];
+        const double fw = g.final_w[(uint32_t)t.state & lane.smask];
         if (fw == INF) continue;
         tot = t.cost + fw;
       } else {
@@ -1730,15 +1783,16 @@ static int cluster_size(int n) {
 extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                  const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
                                  int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
-                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, cudaStream_t stream) {
+                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
+  void (*KFN)(CtwLane*, GraphDev, ChunkArgs, CtwLaneOut*) = any_fsa ? k_decode_chunk<true> : k_decode_chunk<false>;
   ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, *cfg};
   const size_t dyn = (width <= CTW_MAX_SMEM_WIDTH ? (size_t)width : 0) * sizeof(double);
   if (dyn + sizeof(Smem) > 48 * 1024)
-    cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaFuncSetAttribute(KFN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   (void)cudaGetLastError();  // drop stale errors of unchecked calls
   const int R = cluster_size(n);
-  if (R > 8) cudaFuncSetAttribute(k_decode_chunk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (R > 8) cudaFuncSetAttribute(KFN, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(n * R));
   lc.blockDim = dim3(CTW_BS);
@@ -1751,7 +1805,7 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_decode_chunk, d_lanes, g, a, out);
+  cudaError_t e = cudaLaunchKernelEx(&lc, KFN, d_lanes, g, a, out);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }

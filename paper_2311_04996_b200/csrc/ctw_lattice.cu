@@ -56,6 +56,23 @@ __device__ __forceinline__ double lat_key2d(unsigned long long k) {
 
 __device__ __forceinline__ uint32_t lat_hash(uint32_t s, uint32_t shift) { return (s * 0x9E3779B1u) >> shift; }
 
+// Destination token key of an arc (phrase automaton: the key carries the
+// automaton state) and its boost, added after the arc weight like the
+// decoder (ctw_kernels.cu arc_dest).
+__device__ __forceinline__ uint32_t lat_dest(const CtwLane& lane, uint32_t key, int32_t ol, uint32_t nextstate,
+                                             double& c) {
+  if (lane.fsa_next) {
+    uint32_t b = key >> lane.sbits;
+    if (ol != 0) {
+      b = lane.fsa_next[(size_t)b * lane.fsa_width + ol];
+      c = __dadd_rn(c, lane.fsa_cost[b]);
+    }
+    return nextstate | (b << lane.sbits);
+  }
+  if (lane.boost && ol != 0) c = __dadd_rn(c, lane.boost[ol]);
+  return nextstate;
+}
+
 }  // namespace
 
 namespace {
@@ -136,7 +153,6 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
   const long long R = lane.n_rec;
   const int S0 = E.n_seeds;
   const double neg_scale = -a.acoustic_scale;
-  const double* boost = lane.boost;
   if (tid == 0) {
     sm.n_arcs = 0;
     sm.lpool_used = 0;
@@ -158,7 +174,7 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
     int32_t st;
     double c;
     lat_rec(lane, r, &st, &c);
-    if (a.g.final_w[st] != INF) sm.final_mode = 1;  // benign race: all writers store 1
+    if (a.g.final_w[(uint32_t)st & lane.smask] != INF) sm.final_mode = 1;  // benign race: all writers store 1
   }
   __syncthreads();
   const bool fm = sm.final_mode != 0;
@@ -166,7 +182,7 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
     int32_t st;
     double c;
     lat_rec(lane, r, &st, &c);
-    const double fw = fm ? a.g.final_w[st] : 0.0;
+    const double fw = fm ? a.g.final_w[(uint32_t)st & lane.smask] : 0.0;
     if (fm && fw == INF) continue;
     E.beta[S0 + r] = lat_d2key(fw);
     atomicMin(&sm.best, lat_d2key(c + fw));
@@ -230,7 +246,7 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
             c0s = E.seeds[si].cost;
             nd = (int)si;
           }
-          const CtwStateRange rg = a.g.ranges[st0];
+          const CtwStateRange rg = a.g.ranges[(uint32_t)st0 & lane.smask];
           deg = (int)(rg.emit_end - rg.emit_beg);
           // no arc of this source can be kept (epsilon continuations only add)
           if (cut_ok && c0s + step_lb + min_beta > cutoff + 1e-9 * fabs(cutoff)) deg = 0;
@@ -262,8 +278,8 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
             x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
           }
           double c0 = __dadd_rn(__dmul_rn(neg_scale, x), arc.weight);
-          int32_t ol0 = a.g.olabel[ai];
-          if (boost && ol0 != 0) c0 = __dadd_rn(c0, boost[ol0]);
+          const int32_t ol0 = a.g.olabel[ai];
+          const uint32_t x0 = lat_dest(lane, (uint32_t)sst, ol0, (uint32_t)arc.nextstate, c0);
           if (!(c0 < INF)) continue;
           if (cut_ok && sc + c0 + min_beta > cutoff) {
             atomicAdd(&sm.pruned, 1ULL);
@@ -276,7 +292,7 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
           int8_t cpred[LAT_CL];
           int32_t colab[LAT_CL];
           int n = 1;
-          cst[0] = arc.nextstate;
+          cst[0] = (int32_t)x0;
           ccost[0] = c0;
           cpred[0] = -1;
           colab[0] = ol0;
@@ -286,16 +302,16 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
           bool overflow = false;
           while (qh < qt) {
             const int u = queue[qh++];
-            const CtwStateRange ru = a.g.ranges[cst[u]];
+            const CtwStateRange ru = a.g.ranges[(uint32_t)cst[u] & lane.smask];
             for (uint32_t b = ru.eps_beg; b < ru.emit_beg; ++b) {
               const CtwArc ea = a.g.arcs[b];
               double cy = __dadd_rn(ccost[u], ea.weight);
               const int32_t oly = a.g.olabel[b];
-              if (boost && oly != 0) cy = __dadd_rn(cy, boost[oly]);
+              const int32_t ykey = (int32_t)lat_dest(lane, (uint32_t)cst[u], oly, (uint32_t)ea.nextstate, cy);
               if (!(cy < INF)) continue;
               if (cut_ok && sc + cy + min_beta > cutoff) continue;
               int j = 0;
-              while (j < n && cst[j] != ea.nextstate) ++j;
+              while (j < n && cst[j] != ykey) ++j;
               if (j < n) {
                 if (!(cy < ccost[j])) continue;
               } else {
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
                   continue;
                 }
                 ++n;
-                cst[j] = ea.nextstate;
+                cst[j] = ykey;
               }
               ccost[j] = cy;
               cpred[j] = (int8_t)u;

@@ -276,9 +276,28 @@ class LanePool:
             self.free.extend(ids)
 
     def reset(self, ids, boosts) -> np.ndarray:
+        """Fresh channels on lanes `ids`. A boost is a dense per-word cost
+        vector (the reference's tables) or a PhraseBoost (phrase automaton
+        composed inside the search)."""
         n = len(ids)
         idarr = np.asarray(ids, np.int32)
         st = np.zeros(n, np.int32)
+        L = _lib.load()
+        width = self.dg.fg_ref().max_olabel + 1 if self.dg.fg_ref() is not None else None
+        dense = []
+        for lane, b in zip(ids, boosts):
+            if b is not None and hasattr(b, "dense_next") and b.single_words and width is not None:
+                b = b.word_costs(width)  # one-word phrases: the reference's one-state boost
+            if b is not None and hasattr(b, "dense_next"):
+                nxt = b.dense_next(width)
+                cost = np.ascontiguousarray(b.out_cost, np.float64)
+                _lib.check(L.ctw_lane_set_fsa(self.handle, int(lane), int(b.num_states), _lib.ptr(nxt),
+                                              _lib.ptr(cost)), "phrase automaton")
+                dense.append(None)
+            else:
+                _lib.check(L.ctw_lane_set_fsa(self.handle, int(lane), 0, None, None), "phrase automaton")
+                dense.append(b)
+        boosts = dense
         keep = [None if b is None else np.ascontiguousarray(b, np.float64) for b in boosts]
         ptrs = (C.c_void_p * n)(*[None if b is None else b.ctypes.data for b in keep])
         lens = np.asarray([0 if b is None else len(b) for b in keep], np.int64)
@@ -452,12 +471,17 @@ class DecodeState:
             _lib.check(_lib.load().ctw_lane_set_boost(self._pool.handle, self._lane, _lib.ptr(b),
                                                       0 if b is None else len(b)), "set boost")
 
-    def set_boost(self, boost: np.ndarray | None):
-        """Bind a dense per-word boost cost vector before the first frame and
-        re-run the initial closure (decoder.py:231-238)."""
+    def set_boost(self, boost):
+        """Bind a dense per-word boost cost vector (or a PhraseBoost) before
+        the first frame and re-run the initial closure (decoder.py:231-238)."""
         if self.frame_count != 0:
             raise DecodeError("boost table must be attached before any frame is decoded")
-        self._boost = None if boost is None else np.ascontiguousarray(boost, np.float64)
+        if boost is not None and hasattr(boost, "dense_next"):  # PhraseBoost: composed inside the search
+            if self._pool is None:
+                raise DecodeError("phrase boosting needs the native lane path (no kernel= plug-in)")
+            self._boost = boost
+        else:
+            self._boost = None if boost is None else np.ascontiguousarray(boost, np.float64)
         self._seed_initial_tokens()
 
     # -- introspection -------------------------------------------------------------

@@ -160,6 +160,60 @@ class PhraseBoost:
         self.fail = np.asarray(fail, np.int32)
         self.out_cost = np.asarray(out, np.float64)
         self._children = children
+        self.phrases = {tuple(int(w) for w in p): float(m) for p, m in phrases.items()}
+
+    @property
+    def single_words(self) -> bool:
+        """Only one-word phrases: equivalent to the reference's one-state
+        word boost, so the decoder uses the dense word table for it."""
+        return all(len(p) == 1 for p in self.phrases)
+
+    def word_costs(self, width: int) -> np.ndarray:
+        """Dense per-word cost vector (boosting.py:58-67 layout)."""
+        v = np.zeros(width, np.float64)
+        for ph, mag in self.phrases.items():
+            if ph[0] < width:
+                v[ph[0]] += -float(mag)
+        return v
+
+    def to_fst(self, max_olabel: int):
+        """The explicit acceptor (every word label from every state), for
+        composition-based checks: arcs w:w with the entry cost of delta(b, w);
+        every state final with weight 0."""
+        from .synth import Fst
+
+        nxt = self.dense_next(max_olabel + 1)
+        src, lab, w, ns = [], [], [], []
+        for b in range(self.num_states):
+            for x in range(1, max_olabel + 1):
+                t = int(nxt[b, x])
+                src.append(b)
+                lab.append(x)
+                w.append(float(self.out_cost[t]))
+                ns.append(t)
+        return Fst(self.num_states, 0, src, lab, lab, w, ns, np.zeros(self.num_states))
+
+    def dense_next(self, width: int) -> np.ndarray:
+        """Transition table next[b, w] for word labels 0..width-1 (label 0
+        keeps the state): the full automaton delta, breadth first (a state
+        copies its failure state's row, then overrides its own gotos)."""
+        n = self.num_states
+        if n > 65535:
+            raise ValueError("phrase automaton too large (> 65535 states)")
+        nxt = np.zeros((n, width), np.uint16)
+        order = [0]
+        head = 0
+        while head < len(order):
+            s = order[head]
+            head += 1
+            if s:
+                nxt[s] = nxt[int(self.fail[s])]
+            for w, t in self._children[s].items():
+                if w < width:
+                    nxt[s, w] = t
+                order.append(t)
+        nxt[:, 0] = np.arange(n, dtype=np.uint16)
+        return nxt
 
     def cost(self, words) -> float:
         """Boost cost of a word sequence under the automaton."""

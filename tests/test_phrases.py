@@ -88,3 +88,55 @@ def test_lattice_rescoring_matches_enumeration(seed):
     for h in got:
         if h.words in pmap:
             assert abs(pmap[h.words] + pb.cost(h.words) - h.total_cost) <= 1e-9
+
+
+def _compose_oracle(s, pb):
+    from paper_2311_04996_b200 import synth
+
+    b = pb.to_fst(s.graph.max_olabel)
+    tlgb = synth.arc_sort(synth.connect(synth.compose(s.tlg, b)))
+    return tlgb.to_flat()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4))
+def test_in_search_phrase_boost_matches_explicit_composition(seed):
+    """Phrase automaton composed inside the search == decoding the explicit
+    composition TLG o B (reference compose semantics, wfst.py:307-366):
+    identical words, cost within 1e-9 relative (B's weight is added after the
+    arc weight instead of folded into it)."""
+    from paper_2311_04996_b200 import DecoderConfig, PhraseBoost, decode_batch, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=10, num_words=25, order=2, seed=11 + seed, min_pron=1,
+                                            max_pron=3))
+    utts = synth.planted_utterances(s, 6, 40, seed=40 + seed, gap=4.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=10_000)
+    rng = np.random.default_rng(seed)
+    plain = decode_batch(s.graph, cfg, utts)
+    phr = {}
+    for h in plain[:4]:
+        if len(h.words) >= 2:
+            i = int(rng.integers(0, len(h.words) - 1))
+            phr[tuple(h.words[i:i + 2])] = float(rng.uniform(1.0, 5.0))
+    phr[(int(rng.integers(1, 26)), int(rng.integers(1, 26)))] = 3.0
+    phr[(int(rng.integers(1, 26)),)] = 1.5
+    pb = PhraseBoost(phr)
+    assert not pb.single_words
+    got = decode_batch(s.graph, cfg, utts, boost=[pb] * len(utts))
+    want = decode_batch(_compose_oracle(s, pb), cfg, utts)
+    for g, w in zip(got, want):
+        assert g.words == w.words
+        assert abs(g.total_cost - w.total_cost) <= 1e-9 * max(1.0, abs(w.total_cost))
+
+
+@pytest.mark.gpu
+def test_single_word_phrases_are_the_word_boost():
+    from paper_2311_04996_b200 import DecoderConfig, PhraseBoost, decode_batch, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=10, num_words=25, order=2, seed=3, min_pron=1, max_pron=3))
+    utts = synth.planted_utterances(s, 4, 40, seed=9, gap=4.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=300)
+    pb = PhraseBoost({(3,): 2.0, (7,): 1.0, (11,): 4.0})
+    assert pb.single_words
+    dense = pb.word_costs(s.graph.max_olabel + 1)
+    assert decode_batch(s.graph, cfg, utts, boost=[pb] * 4) == decode_batch(s.graph, cfg, utts, boost=dense)
