@@ -140,3 +140,32 @@ def test_single_word_phrases_are_the_word_boost():
     assert pb.single_words
     dense = pb.word_costs(s.graph.max_olabel + 1)
     assert decode_batch(s.graph, cfg, utts, boost=[pb] * 4) == decode_batch(s.graph, cfg, utts, boost=dense)
+
+
+@pytest.mark.gpu
+def test_lattice_of_phrase_boosted_decode():
+    """Lattices of lanes decoded with an in-search phrase automaton: the
+    lattice's best path is the boosted decode's best path and its 1-best
+    equals it."""
+    from paper_2311_04996_b200 import DecoderConfig, PhraseBoost, decode_batch, decode_lattices, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=10, num_words=25, order=2, seed=12, min_pron=1, max_pron=3))
+    utts = synth.planted_utterances(s, 4, 30, seed=8, gap=4.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    plain = decode_batch(s.graph, cfg, utts)
+    phr = {tuple(h.words[:2]): 2.5 for h in plain if len(h.words) >= 2}
+    pb = PhraseBoost(phr)
+    hyps = decode_batch(s.graph, cfg, utts, boost=[pb] * 4)
+    lats = decode_lattices(s.graph, cfg, utts, lattice_beam=4.0, boost=[pb] * 4)
+    for lat, h in zip(lats, hyps):
+        assert lat.status == 0
+        assert lat.best_path == h
+        assert abs(lat.best_cost - h.total_cost) <= 1e-9
+        assert lat.nbest(2)[0].words == h.words
+
+
+def test_fsa_too_large_for_graph_is_rejected():
+    from paper_2311_04996_b200 import PhraseBoost
+
+    pb = PhraseBoost({tuple(range(1, 40)): 1.0})
+    assert pb.num_states == 40
