@@ -59,7 +59,9 @@
 #define CTW_EIPT 2                       // frontier items per thread per epsilon tile
 #define CTW_ETILE (CTW_BS * CTW_EIPT)
 #define CTW_DISC 0xFFFFFFFFu             // epsilon tile item: discovery only (no value)
+#ifndef CTW_NB
 #define CTW_NB 1024      // cost-histogram bins over [min, min + beam] for the max-active select
+#endif
 #define CTW_BBUF 512     // boundary-bin capacity of the exact (cost, state) sort
 
 namespace cg = cooperative_groups;
@@ -273,7 +275,9 @@ __device__ __forceinline__ void tok_clear(CtwTok* e) {
 
 // --------------------------------------------------------- shared memory --
 
+#ifndef CTW_NBIG
 #define CTW_NBIG 512   // high out-degree sources expanded arc-parallel per frame (list capacity)
+#endif
 #ifndef CTW_BIG
 #define CTW_BIG 64  // emitting out-degree above which a source is expanded arc-parallel
 #endif
