@@ -413,7 +413,7 @@ int reserve_lanes(ctw_lanes* l, int n) {
 int32_t prune_flag(const ctw_lanes* l, const double* boost, int64_t len) {
   const ctw_graph* g = l->g;
   if (!g->eps_nonneg || l->cfg.max_ne_iters < (1 << 16)) return 0;
-  if (getenv("CTW_NOPRUNE")) return 0;  // diagnostics: exact full closure
+  if (getenv("CTW_NOPRUNE")) return 0;  // diagnostics: every candidate valued (full closure)
   if (boost && g->eps_olabel)
     for (int64_t i = 0; i < len; ++i)
       if (!(boost[i] >= 0.0)) return 0;

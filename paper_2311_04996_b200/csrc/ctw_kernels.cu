@@ -304,7 +304,7 @@ struct BigSrc {
   int32_t idx;  // source index (emitting winners' aux)
   uint32_t beg;
   int32_t deg;
-  uint32_t key;  // source token key
+  int32_t pad;
   double cost;
 };
 
@@ -363,7 +363,6 @@ struct __align__(16) Smem {
   int n_cur, n_first, any_big;
   uint2* in0;           // input of the current epsilon pass: in0[0, n_first) ++ in1[0, n_cur - n_first)
   uint2* in1;
-  int work;             // this rank's chunk counter (rank-local sweeps)
   unsigned long long min_key;  // running minimum seen by this rank (>= the cluster's)
   int n_all;            // slots of all ranks (after the closure)
   int cnt_l, mpd_l, cnt_all, mpd_all;
@@ -1284,7 +1283,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
             bs.idx = base + lane_;
             bs.beg = r.emit_beg;
             bs.deg = deg;
-            bs.key = 0;
+            bs.pad = 0;
             bs.cost = t.cost;
             bigl[j] = bs;
             deg = 0;
@@ -1419,14 +1418,6 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     if (status == CTW_OK)
       status = count_pass(sm, L, fc, sv, ib, n_all, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
     const int n_ib = sm.cnt_all;
-#ifdef CTW_DEBUG
-    if (status == CTW_OK && tid == 0) {
-      const unsigned long long gm = *((volatile unsigned long long*)&G->min_key);
-      if (gm != sm.min_key)
-        printf("min mismatch lane %d rank %d frame %d local %.17g rank0 %.17g passes %d\n", b, rank, f,
-               key2d(sm.min_key), key2d(gm), sm.passes);
-    }
-#endif
     if (rank == 0 && tid == 0) {
       const long long t = clock64();
       prof[2] += t - tclk;

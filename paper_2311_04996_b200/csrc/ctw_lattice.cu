@@ -137,7 +137,6 @@ struct __align__(16) LatSmem {
   unsigned long long min_beta;
   unsigned long long best;
   int final_mode;
-  int deg_tot;
   unsigned long long items, pruned;
 };
 
