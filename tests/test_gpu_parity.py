@@ -275,3 +275,29 @@ def test_lane_reuse_and_decode_failure_per_index():
         assert isinstance(got[0], Hypothesis) and isinstance(got[4], Hypothesis)
         assert isinstance(got[2], DecodeFailure) and "frame 4" in str(got[2].error)
         assert isinstance(got[3], DecodeFailure)
+
+
+def test_bench_scale_history_matches_oracle(oracle_mod):
+    """The benchmark's own graph (C2: 3-gram TLG, 4.5 M arcs) at the bench
+    configuration (beam 17, max_active 10k): every record's cost, state and
+    transcript equal the CPU oracle's for two Conformer-shaped utterances."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    from conftest import assert_history_equivalent
+
+    from paper_2311_04996_b200 import DecoderConfig, DecodeState, best_path
+
+    s = bench.system(False, "c2")
+    utts = bench.workload(s, 2, 60, 0)
+    cfg = DecoderConfig(beam=bench.BEAM, max_active=bench.MAX_ACTIVE)
+    for u in utts:
+        ch = DecodeState(s.graph, cfg)
+        ch.advance_frames(u)
+        oc = oracle_mod.OracleChannel.from_config(s.graph, cfg)
+        oc.advance_frames(u.astype(np.float64))
+        assert_history_equivalent(ch.history_records(), oc.history_records(), exact_prev=False)
+        h = best_path(ch)
+        assert (h.words, h.total_cost, h.frame_count) == oc.best_path()

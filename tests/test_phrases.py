@@ -169,3 +169,24 @@ def test_fsa_too_large_for_graph_is_rejected():
 
     pb = PhraseBoost({tuple(range(1, 40)): 1.0})
     assert pb.num_states == 40
+
+
+@pytest.mark.gpu
+def test_streaming_with_phrase_boost_equals_offline():
+    from paper_2311_04996_b200 import (BatcherConfig, Chunk, DecoderConfig, PhraseBoost, StreamPool, decode_batch,
+                                       synth)
+
+    s = synth.build_system(synth.SystemSpec(num_units=10, num_words=25, order=2, seed=12, min_pron=1, max_pron=3))
+    utts = synth.planted_utterances(s, 4, 45, seed=5, gap=4.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    plain = decode_batch(s.graph, cfg, utts)
+    pb = PhraseBoost({tuple(h.words[:2]): 2.0 for h in plain if len(h.words) >= 2})
+    offline = decode_batch(s.graph, cfg, utts, boost=[pb] * len(utts))
+    pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=2))
+    sids = [pool.create_stream(pb) for _ in utts]
+    for sid, u in zip(sids, utts):
+        for i in range(0, len(u), 7):
+            pool.push_chunk(Chunk(sid, u[i:i + 7], is_last=i + 7 >= len(u)))
+    finals = pool.drain()
+    for sid, want in zip(sids, offline):
+        assert finals[sid] == want
