@@ -487,6 +487,13 @@ def main():
             traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
         except ValueError:
             traffic = None
+    ncu = None
+    nfile = ROOT / "profiles" / "ncu_metrics.json"
+    if nfile.exists():
+        try:
+            ncu = json.loads(nfile.read_text())
+        except ValueError:
+            ncu = None
 
     if rank != 0:
         return
@@ -505,12 +512,19 @@ def main():
                      "traffic": traffic, "kernel": "k_decode_chunk",
                      "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms_per_launch": kernel_ms,
                      "bytes_model": "28*E_emit + 24*N_src (SURVEY 8(d))",
+                     # the north star's evidence metric: DRAM bytes ncu measured for this kernel
+                     # (profiles/traffic.json, C2 512x250 launches) over this run's launch time
+                     "measured_dram_gbs": (traffic / (kernel_ms / 1e3) / 1e9
+                                           if traffic and args.config == "c2" and n == 512 and F == 250 else None),
+                     "measured_dram_frac": (traffic / (kernel_ms / 1e3) / 1e9 / peak
+                                            if traffic and args.config == "c2" and n == 512 and F == 250 else None),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
         "workload_stats": {"emitting_arcs_per_lane_frame": st["arcs"] / max(1, st["frames"]),
                            "tokens_per_lane_frame": st["src_tokens"] / max(1, st["frames"]),
                            "max_slots": st["max_slots"], "wall_s_timed": t_wall},
         "clocks": clk.summary(),
         "stage_profile": _stage_profile(prof, st),
+        "ncu": ncu,
         "graph_load": graph_load,
     }
     if args.lattice > 0 and world == 1:

@@ -30,7 +30,9 @@
 
 #include "ctw_common.h"
 
+#ifndef LAT_BS
 #define LAT_BS 512
+#endif
 #define LAT_CL 48       // local epsilon-closure capacity per work item
 #define LAT_QL 128      // local relaxation budget per work item
 
