@@ -172,6 +172,13 @@ int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wor
                   int64_t* word_off, double* total_cost, int64_t* frame_count, int32_t* status);
 
 /* Channel introspection: committed frame count, active tokens, records. */
+/* Partial-history garbage collection (long-running streams; SURVEY 8(f)
+ * item 2): keep only the records reachable from each lane's active tokens
+ * (everything best_path or a later partial hypothesis can reach), renumber
+ * them in frame order and release the rest. kept[i] = records kept. After
+ * it, history export returns the kept records only and lattices are not
+ * available for the lane. */
+int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* kept);
 int ctw_lane_info(ctw_lanes* l, int32_t lane, int64_t* frame_count, int64_t* n_tokens,
                   int64_t* n_records);
 /* Reference-layout export of frames [frame_from, frame_count) of one lane.

@@ -42,6 +42,9 @@ extern "C" int ctw_launch_best(const CtwLane*, const CtwStateRange*, const CtwAr
                                const double*, const int*, int, int32_t*, const long long*, const int*,
                                int*, double*, int*, cudaStream_t);
 extern "C" int ctw_launch_clear(CtwTok*, uint32_t, cudaStream_t);
+extern "C" int ctw_launch_hist_mark(const CtwLane*, const int*, uint32_t* const*, int, cudaStream_t);
+extern "C" int ctw_launch_hist_compact(CtwLane*, const int*, uint32_t* const*, int32_t* const*,
+                                       CtwRecPage* const* const*, long long*, int, cudaStream_t);
 extern "C" int ctw_launch_lattice(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
                                   CtwLatEntry*, int, const void*, int, int, double, double, cudaStream_t);
 
@@ -142,6 +145,7 @@ struct ctw_lanes {
   std::vector<double*> fsa_cost;
   std::vector<int64_t> fsa_cap;
   std::vector<double> fsa_min;  // most negative entry cost (early-pruning exactness)
+  std::vector<char> compacted;  // history garbage-collected since the last reset (no lattice)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   // scratch
@@ -395,6 +399,7 @@ int reserve_lanes(ctw_lanes* l, int n) {
   l->fsa_cost.resize(n, nullptr);
   l->fsa_cap.resize(n, 0);
   l->fsa_min.resize(n, 0.0);
+  l->compacted.resize(n, 0);
   for (int i = l->n; i < n; ++i) {
     if (int r = init_lane(l, i)) return r;
   }
@@ -797,6 +802,7 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
     L.pool_used = 0;
     L.n_rec = 0;
     L.pend_valid = 0;
+    l->compacted[lane] = 0;
     trim_hist(l, lane);
     if (int r = sync_lane(l, lane)) return r;
   }
@@ -1119,6 +1125,96 @@ int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wor
                              cudaMemcpyDeviceToHost, l->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(l->stream));
+  return 0;
+}
+
+int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* kept) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (n <= 0) return 0;
+  if (int r = check_ids(l, lane_ids, n)) return r;
+  cudaStream_t st = l->stream;
+  std::vector<uint32_t*> marks(n, nullptr);
+  std::vector<int32_t*> newidx(n, nullptr);
+  std::vector<CtwRecPage**> nptab(n, nullptr);
+  std::vector<std::vector<CtwRecPage*>> npages(n);
+  auto take_page = [&]() -> CtwRecPage* {
+    if (l->free_pages.empty()) {
+      CtwRecPage* slab = nullptr;
+      if (salloc(&slab, CTW_SLAB, st) != cudaSuccess) return nullptr;
+      l->slabs.push_back(slab);
+      for (int k = CTW_SLAB - 1; k >= 0; --k) l->free_pages.push_back(slab + k);
+    }
+    CtwRecPage* p = l->free_pages.back();
+    l->free_pages.pop_back();
+    return p;
+  };
+  for (int i = 0; i < n; ++i) {
+    const CtwLane& L = l->h[lane_ids[i]];
+    const int64_t R = L.n_rec;
+    const int64_t W = (R + 31) / 32 + 1;
+    CUDA_TRY(salloc(&marks[i], (size_t)W, st));
+    CUDA_TRY(cudaMemsetAsync(marks[i], 0, (size_t)W * 4, st));
+    CUDA_TRY(salloc(&newidx[i], (size_t)R + 1, st));
+    const int64_t np = std::max<int64_t>(1, (R + CTW_PAGE - 1) / CTW_PAGE);  // worst case: all kept
+    for (int64_t k = 0; k < np; ++k) {
+      CtwRecPage* p = take_page();
+      if (!p) return fail(-3, "out of memory for history pages");
+      npages[i].push_back(p);
+    }
+    CUDA_TRY(salloc(&nptab[i], (size_t)np, st));
+    CUDA_TRY(cudaMemcpyAsync(nptab[i], npages[i].data(), np * sizeof(CtwRecPage*), cudaMemcpyHostToDevice, st));
+  }
+  if (int r = ensure_scratch(l, n)) return r;
+  for (int i = 0; i < n; ++i) l->h_ids[i] = lane_ids[i];
+  uint32_t** d_marks = nullptr;
+  int32_t** d_newidx = nullptr;
+  CtwRecPage*** d_nptab = nullptr;
+  long long* d_kept = nullptr;
+  CUDA_TRY(salloc(&d_marks, (size_t)n, st));
+  CUDA_TRY(salloc(&d_newidx, (size_t)n, st));
+  CUDA_TRY(salloc(&d_nptab, (size_t)n, st));
+  CUDA_TRY(salloc(&d_kept, (size_t)n, st));
+  CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, n * sizeof(int), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_marks, marks.data(), n * sizeof(uint32_t*), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_newidx, newidx.data(), n * sizeof(int32_t*), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_nptab, nptab.data(), n * sizeof(CtwRecPage**), cudaMemcpyHostToDevice, st));
+  if (ctw_launch_hist_mark(l->d, l->d_ids, d_marks, n, st) ||
+      ctw_launch_hist_compact(l->d, l->d_ids, d_marks, d_newidx, d_nptab, d_kept, n, st))
+    return fail(-1, std::string("history compaction launch: ") + cudaGetErrorString(cudaGetLastError()));
+  std::vector<long long> kv(n);
+  CUDA_TRY(cudaMemcpyAsync(kv.data(), d_kept, n * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; ++i) {
+    const int lane = lane_ids[i];
+    CtwLane& L = l->h[lane];
+    // the lane adopts the first pages of the new set; the rest and the old
+    // pages go back to the free list
+    const int64_t keep_pages = std::max<int64_t>(1, (kv[i] + CTW_PAGE - 1) / CTW_PAGE);
+    for (CtwRecPage* p : l->hpages[lane]) l->free_pages.push_back(p);
+    l->hpages[lane].assign(npages[i].begin(), npages[i].begin() + keep_pages);
+    for (size_t k = (size_t)keep_pages; k < npages[i].size(); ++k) l->free_pages.push_back(npages[i][k]);
+    if ((int64_t)l->hpages[lane].size() > l->ptab_cap[lane]) {
+      sfree(L.pages, st);
+      CUDA_TRY(salloc(&L.pages, l->hpages[lane].size(), st));
+      l->ptab_cap[lane] = (int64_t)l->hpages[lane].size();
+    }
+    CUDA_TRY(cudaMemcpyAsync(L.pages, l->hpages[lane].data(), l->hpages[lane].size() * sizeof(CtwRecPage*),
+                             cudaMemcpyHostToDevice, st));
+    L.rcap = (int64_t)l->hpages[lane].size() * CTW_PAGE;
+    L.n_rec = kv[i];
+    l->compacted[lane] = 1;
+    if (kept) kept[i] = kv[i];
+    if (int r = sync_lane(l, lane)) return r;
+    sfree(marks[i], st);
+    sfree(newidx[i], st);
+    sfree(nptab[i], st);
+  }
+  sfree(d_marks, st);
+  sfree(d_newidx, st);
+  sfree(d_nptab, st);
+  sfree(d_kept, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
   return 0;
 }
 
@@ -1473,6 +1569,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
   for (int i = 0; i < n; ++i) {
     std::memset(&out[i], 0, sizeof(out[i]));
     if (!l->seeded[lane_ids[i]]) return fail(-1, "lane not seeded (call ctw_lane_reset first)");
+    if (l->compacted[lane_ids[i]]) return fail(-1, "lane history was garbage-collected: no lattice");
   }
   const size_t esz = dtype ? 8 : 4;
   std::vector<int32_t> frames(n);

@@ -484,6 +484,20 @@ class DecodeState:
             self._boost = None if boost is None else np.ascontiguousarray(boost, np.float64)
         self._seed_initial_tokens()
 
+    def compact_history(self) -> int:
+        """Partial-history garbage collection (ctw_lane_compact): drop the
+        records no active token can reach; best_path and later partial
+        hypotheses are unchanged, history_records() then lists the kept
+        records only. Returns the records kept."""
+        if self._pool is None:
+            raise DecodeError("history compaction needs the native lane path")
+        kept = np.zeros(1, np.int64)
+        ids = np.asarray([self._lane], np.int32)
+        _lib.check(_lib.load().ctw_lane_compact(self._pool.handle, _lib.ptr(ids), 1, _lib.ptr(kept)),
+                   "history compaction")
+        self._cache = None
+        return int(kept[0])
+
     # -- introspection -------------------------------------------------------------
 
     def _export(self) -> dict:

@@ -301,3 +301,38 @@ def test_bench_scale_history_matches_oracle(oracle_mod):
         assert_history_equivalent(ch.history_records(), oc.history_records(), exact_prev=False)
         h = best_path(ch)
         assert (h.words, h.total_cost, h.frame_count) == oc.best_path()
+
+
+def test_history_compaction_keeps_best_paths():
+    """Partial-history garbage collection (ctw_lane_compact): offline and
+    streamed best paths, partial hypotheses and final hypotheses unchanged;
+    history shrinks."""
+    from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, DecodeState, StreamPool, best_path, synth
+
+    s = _system(num_units=30, num_words=50, order=2, seed=2)
+    utts = synth.planted_utterances(s, 4, 80, seed=8, gap=4.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    for u in utts:
+        a, b = DecodeState(s.graph, cfg), DecodeState(s.graph, cfg)
+        for i in range(0, len(u), 10):
+            a.advance_frames(u[i:i + 10])
+            b.advance_frames(u[i:i + 10])
+            before = len([r for fr in b.history_records() for r in fr])
+            kept = b.compact_history()
+            assert kept <= before
+            assert best_path(a) == best_path(b)
+        assert sum(len(fr) for fr in b.history_records()) < sum(len(fr) for fr in a.history_records())
+    # streams with collection every 2 chunks == streams without
+    finals = []
+    for gc in (None, 2):
+        pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=3), gc_every=gc)
+        sids = [pool.create_stream() for _ in utts]
+        partial = []
+        for sid, u in zip(sids, utts):
+            for i in range(0, len(u), 9):
+                pool.push_chunk(Chunk(sid, u[i:i + 9], is_last=i + 9 >= len(u)))
+        while pool.ready_streams():
+            partial.extend(pool.step())
+        finals.append((pool.drain(), partial))
+    (f0, p0), (f1, p1) = finals
+    assert f0 == f1 and p0 == p1
