@@ -426,18 +426,27 @@ __device__ __forceinline__ int csync(Smem& sm) {
     sm.min_pub[e & 1] = *((volatile unsigned long long*)&sm.min_key);
   }
   cl.sync();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp 0: lane k reads rank k's published values (one DSMEM round trip
+    // for all ranks), then a warp reduction
+    const int k = threadIdx.x;
     int s = 0;
-    unsigned long long m = sm.min_key;
-    for (int k = 0; k < (int)cl.num_blocks(); ++k) {
+    unsigned long long m = ~0ULL;
+    if (k < (int)cl.num_blocks()) {
       const Smem* o = cl.map_shared_rank(&sm, k);
-      s = max(s, o->st_pub[e & 1]);
-      const unsigned long long mk = o->min_pub[e & 1];
-      if (mk < m) m = mk;
+      s = o->st_pub[e & 1];
+      m = o->min_pub[e & 1];
     }
-    sm.st_all = s;
-    sm.min_key = m;
-    sm.epoch = e + 1;
+    for (int d = 16; d; d >>= 1) {
+      s = max(s, __shfl_xor_sync(0xFFFFFFFFu, s, d));
+      const unsigned long long mo = __shfl_xor_sync(0xFFFFFFFFu, m, d);
+      if (mo < m) m = mo;
+    }
+    if (k == 0) {
+      sm.st_all = s;
+      if (m < sm.min_key) sm.min_key = m;
+      sm.epoch = e + 1;
+    }
   }
   __syncthreads();
   return sm.st_all;
@@ -551,7 +560,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
       if (pass == 1) {
         // every slot created before the stage (the ranks' published counts)
         int tot = 0;
-        for (int k = 0; k < R; ++k) tot += cl.map_shared_rank(&sm, k)->snap_slots;
+        for (int k = 0; k < R; ++k) tot += cl.map_shared_rank(&sm, k)->snap_slots;  // once per frame
         sm.in0 = L.slots;
         sm.n_first = min(tot, (int)L.seg);
         sm.in1 = L.slots;
@@ -663,10 +672,9 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
     }
     // the barrier ending the pass (also merges the ranks' running minima)
     if (csync(sm) >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
-    if (tid == 0) {
-      int any = 0;
-      for (int k = 0; k < R; ++k) any |= cl.map_shared_rank(&sm, k)->pc_big[q];
-      sm.any_big = any;
+    if (tid < 32) {
+      const int any = __any_sync(0xFFFFFFFFu, tid < R && cl.map_shared_rank(&sm, tid)->pc_big[q]);
+      if (tid == 0) sm.any_big = any;
     }
     __syncthreads();
     // a quiet pass (only <= relax_eps changes) ends the closure; otherwise the
@@ -1377,10 +1385,10 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     if (sm.st_all < CTW_GROW_TABLE)
       st = eps_fixpoint<FSA>(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
     const int vote = sm.st_all;
-    if (tid == 0) {
-      int tot = 0;  // slots allocated by all ranks (stable: the closure is over)
-      for (int k = 0; k < R; ++k) tot += cl.map_shared_rank(&sm, k)->n_slots;
-      sm.n_all = tot;
+    if (tid < 32) {
+      int tot = tid < R ? cl.map_shared_rank(&sm, tid)->n_slots : 0;  // stable: the closure is over
+      for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, d);
+      if (tid == 0) sm.n_all = tot;
     }
     __syncthreads();
     const int n_alloc = sm.n_all;
