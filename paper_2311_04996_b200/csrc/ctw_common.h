@@ -99,7 +99,10 @@ struct __align__(16) CtwSrc {
 // (3/4 load), so lists of CTW_LOAD(tcap) entries never overflow in a frame
 // that commits.
 #define CTW_RMAX 16  // 8 portable; 16 with the non-portable cluster attribute
-#define CTW_LOAD(tcap) ((tcap) - (tcap) / 4)
+#ifndef CTW_LOAD_DIV
+#define CTW_LOAD_DIV 4
+#endif
+#define CTW_LOAD(tcap) ((tcap) - (tcap) / CTW_LOAD_DIV)
 #define CTW_SLOTS_LEN(tcap) ((uint64_t)CTW_LOAD(tcap))
 #define CTW_FRONT_LEN(tcap) (4 * (uint64_t)CTW_LOAD(tcap))
 
