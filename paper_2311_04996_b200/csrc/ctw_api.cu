@@ -1645,6 +1645,40 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
     CUDA_TRY(cudaMemcpyAsync(ent.data(), d_ent, m * sizeof(CtwLatEntry), cudaMemcpyDeviceToHost, l->stream));
     CUDA_TRY(cudaStreamSynchronize(l->stream));
     std::vector<int> again;
+    // stage every finished lane's device results first (one synchronisation)
+    struct Host {
+      std::vector<CtwLatArc> arcs;
+      std::vector<int32_t> lab, spend, pool;
+      std::vector<CtwSrc> seeds;
+    };
+    std::vector<Host> hb((size_t)m);
+    for (int k = 0; k < m; ++k) {
+      const int i = todo[k];
+      const CtwLatEntry& e = ent[k];
+      if (e.status == 1 || e.status == 2) continue;
+      const int lane = lane_ids[i];
+      const CtwLane& L = l->h[lane];
+      Host& h = hb[k];
+      h.arcs.resize((size_t)e.n_arcs);
+      h.lab.resize((size_t)e.lpool_used);
+      const int ns = l->seed_n[lane];
+      h.seeds.resize((size_t)ns);
+      h.spend.resize((size_t)ns);
+      h.pool.resize((size_t)L.pool_used);
+      if (e.n_arcs)
+        CUDA_TRY(cudaMemcpyAsync(h.arcs.data(), d_arcs[i], h.arcs.size() * sizeof(CtwLatArc),
+                                 cudaMemcpyDeviceToHost, l->stream));
+      if (e.lpool_used)
+        CUDA_TRY(cudaMemcpyAsync(h.lab.data(), d_lab[i], h.lab.size() * 4, cudaMemcpyDeviceToHost, l->stream));
+      if (ns) {
+        CUDA_TRY(cudaMemcpyAsync(h.seeds.data(), l->seed_src[lane], ns * sizeof(CtwSrc), cudaMemcpyDeviceToHost,
+                                 l->stream));
+        CUDA_TRY(cudaMemcpyAsync(h.spend.data(), l->seed_pend[lane], ns * 4, cudaMemcpyDeviceToHost, l->stream));
+      }
+      if (L.pool_used)
+        CUDA_TRY(cudaMemcpyAsync(h.pool.data(), L.pool, h.pool.size() * 4, cudaMemcpyDeviceToHost, l->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
     for (int k = 0; k < m; ++k) {
       const int i = todo[k];
       const CtwLatEntry& e = ent[k];
@@ -1665,24 +1699,13 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       o.lattice_beam = lattice_beam;
       o.closure_items = e.closure_items;
       o.closure_pruned = e.closure_pruned;
-      std::vector<CtwLatArc> arcs((size_t)e.n_arcs);
-      std::vector<int32_t> lab((size_t)e.lpool_used);
+      Host& hh = hb[k];
+      const std::vector<CtwLatArc>& arcs = hh.arcs;
+      const std::vector<int32_t>& lab = hh.lab;
+      const std::vector<CtwSrc>& seeds = hh.seeds;
+      const std::vector<int32_t>& spend = hh.spend;
+      const std::vector<int32_t>& pool = hh.pool;
       const int ns = l->seed_n[lane];
-      std::vector<CtwSrc> seeds((size_t)ns);
-      std::vector<int32_t> spend((size_t)ns), pool((size_t)L.pool_used);
-      if (e.n_arcs)
-        CUDA_TRY(cudaMemcpyAsync(arcs.data(), d_arcs[i], arcs.size() * sizeof(CtwLatArc), cudaMemcpyDeviceToHost,
-                                 l->stream));
-      if (e.lpool_used)
-        CUDA_TRY(cudaMemcpyAsync(lab.data(), d_lab[i], lab.size() * 4, cudaMemcpyDeviceToHost, l->stream));
-      if (ns) {
-        CUDA_TRY(cudaMemcpyAsync(seeds.data(), l->seed_src[lane], ns * sizeof(CtwSrc), cudaMemcpyDeviceToHost,
-                                 l->stream));
-        CUDA_TRY(cudaMemcpyAsync(spend.data(), l->seed_pend[lane], ns * 4, cudaMemcpyDeviceToHost, l->stream));
-      }
-      if (L.pool_used)
-        CUDA_TRY(cudaMemcpyAsync(pool.data(), L.pool, pool.size() * 4, cudaMemcpyDeviceToHost, l->stream));
-      CUDA_TRY(cudaStreamSynchronize(l->stream));
       o.n_seeds = ns;
       o.seed_state = cmalloc<int32_t>(ns);
       o.seed_cost = cmalloc<double>(ns);

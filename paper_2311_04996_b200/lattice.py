@@ -63,9 +63,17 @@ class Lattice:
         self.src_state = arr(c.arc_src_state, na, np.int32)
         self.weight = arr(c.arc_w, na, np.float64)
         self.dst_final = arr(c.arc_dst_final, na, np.float64)
-        aoff = arr(c.arc_lab_off, na + 1, np.int64)
-        alab = arr(c.arc_lab, int(aoff[-1]) if na else 0, np.int32)
-        self.labels = [tuple(int(x) for x in alab[aoff[k]:aoff[k + 1]]) for k in range(na)]
+        self.label_off = arr(c.arc_lab_off, na + 1, np.int64) if na else np.zeros(1, np.int64)
+        self.label_pool = arr(c.arc_lab, int(self.label_off[-1]), np.int32)
+        self._labels = None
+
+    @property
+    def labels(self) -> list:
+        """Output labels of every arc (tuples; built on first use)."""
+        if self._labels is None:
+            off, pool = self.label_off.tolist(), self.label_pool.tolist()
+            self._labels = [tuple(pool[off[k]:off[k + 1]]) for k in range(len(off) - 1)]
+        return self._labels
 
     @property
     def num_arcs(self) -> int:
