@@ -336,3 +336,33 @@ def test_history_compaction_keeps_best_paths():
         finals.append((pool.drain(), partial))
     (f0, p0), (f1, p1) = finals
     assert f0 == f1 and p0 == p1
+
+
+def test_ragged_wide_nan_and_extreme_configs_match_oracle(oracle_mod):
+    """Edge cases in one launch each: ragged utterance lengths, frames wider
+    than the shared-memory row (log-likelihoods read from global memory),
+    NaN log-likelihoods (dropped like the reference's `nc < inf` test,
+    _kernel.pyx:253), f64 input, and extreme beam / max_active."""
+    from paper_2311_04996_b200 import DecodeFailure, DecoderConfig, decode_batch, synth
+
+    s = _system(num_units=12, num_words=30, order=2, seed=6, min_pron=1, max_pron=4)
+    rng = np.random.default_rng(1)
+    base = synth.planted_utterances(s, 6, 50, seed=4, gap=4.0, noise=1.0)
+    ragged = [u[: int(rng.integers(1, 50))] for u in base]
+    wide = [np.concatenate([u, rng.normal(-9.0, 1.0, size=(len(u), 5000 - u.shape[1]))], axis=1) for u in base[:3]]
+    nanu = base[3].copy()
+    nanu[5, :4] = np.nan
+    cases = [(ragged, DecoderConfig(beam=12.0, max_active=200)),
+             (wide, DecoderConfig(beam=12.0, max_active=200)),
+             ([nanu], DecoderConfig(beam=12.0, max_active=200)),
+             (base[:3], DecoderConfig(beam=1e-6, max_active=1)),
+             (base[:3], DecoderConfig(beam=1e9, max_active=1_000_000))]
+    for utts, cfg in cases:
+        got = decode_batch(s.graph, cfg, utts)
+        for u, h in zip(utts, got):
+            try:
+                want = oracle_mod.decode_utterance(s.graph, cfg, np.asarray(u, np.float64))
+            except oracle_mod.OracleError:
+                assert isinstance(h, DecodeFailure)
+                continue
+            assert (h.words, h.total_cost, h.frame_count) == want
