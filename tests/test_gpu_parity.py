@@ -366,3 +366,21 @@ def test_ragged_wide_nan_and_extreme_configs_match_oracle(oracle_mod):
                 assert isinstance(h, DecodeFailure)
                 continue
             assert (h.words, h.total_cost, h.frame_count) == want
+
+
+def test_long_utterance_history_pages(oracle_mod):
+    """3000 frames in 7 chunks of one channel: history spans several 64K-record
+    pages and the frame-start array regrows; best path == oracle."""
+    from paper_2311_04996_b200 import DecoderConfig, DecodeState, best_path, synth
+
+    s = _system(num_units=12, num_words=30, order=2, seed=6, min_pron=1, max_pron=4)
+    u = synth.planted_utterances(s, 1, 3000, seed=5, gap=3.0, noise=1.0)[0]
+    cfg = DecoderConfig(beam=14.0, max_active=2000)
+    ch = DecodeState(s.graph, cfg)
+    for i in range(0, len(u), 450):
+        ch.advance_frames(u[i:i + 450])
+    oc = oracle_mod.OracleChannel.from_config(s.graph, cfg)
+    oc.advance_frames(u)
+    h = best_path(ch)
+    assert (h.words, h.total_cost, h.frame_count) == oc.best_path()
+    assert sum(len(f) for f in ch.history_records()) > 65536
