@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small", action="store_true", help="tiny graph smoke run (not a bench number)")
     ap.add_argument("--streams", type=int, default=2000, help="C4 streaming channels (0 = skip)")
-    ap.add_argument("--stream-seconds", type=float, default=5.0, help="audio per stream in the C4 run")
+    ap.add_argument("--stream-seconds", type=float, default=10.0, help="audio per stream in the C4 run")
     ap.add_argument("--cpu-streams", type=int, default=32, help="streams in the CPU reference C4 run")
     ap.add_argument("--lattice", type=int, default=64,
                     help="utterances in the lattice leg (decode + lattice + 10-best; 0 = skip)")
