@@ -496,6 +496,7 @@ def main():
     words_bytes = sum(len(h.words) for h in out_e2e) * 4 + n * (8 + 8 + 4)
 
     # ---- roofline of the frame kernel (k_decode_chunk) ----
+    emit_share = _stage_profile(prof, st)["emit"]
     launches = max(1, st["decode_launches"])
     algo_bytes = (28 * st["arcs"] + 24 * st["src_tokens"]) / launches
     kernel_ms = st["decode_ms"] / launches
@@ -540,6 +541,12 @@ def main():
                                            if traffic and args.config == "c2" and n == 512 and F == 250 else None),
                      "measured_dram_frac": (traffic / (kernel_ms / 1e3) / 1e9 / peak
                                             if traffic and args.config == "c2" and n == 512 and F == 250 else None),
+                     # the emitting-expansion stage alone (its share of the launch from the
+                     # kernel's clock64 stage counters): the same bytes over its time
+                     "emit_stage_ms": kernel_ms * emit_share,
+                     "emit_stage_gbs": algo_bytes / (kernel_ms * emit_share / 1e3) / 1e9 if emit_share > 0 else None,
+                     "emit_stage_frac": algo_bytes / (kernel_ms * emit_share / 1e3) / 1e9 / peak
+                     if emit_share > 0 else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
         "workload_stats": {"emitting_arcs_per_lane_frame": st["arcs"] / max(1, st["frames"]),
                            "tokens_per_lane_frame": st["src_tokens"] / max(1, st["frames"]),
