@@ -179,6 +179,11 @@ int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wor
  * it, history export returns the kept records only and lattices are not
  * available for the lane. */
 int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* kept);
+/* Grow the lanes' token tables now to the largest size any lane of the set
+ * has needed (a streaming server does this when it opens a stream, so no
+ * chunk has to be re-run mid-stream for a bigger table). Call between
+ * ctw_lane_reset and the first ctw_advance. */
+int ctw_lanes_presize(ctw_lanes* l, const int32_t* lane_ids, int32_t n);
 int ctw_lane_info(ctw_lanes* l, int32_t lane, int64_t* frame_count, int64_t* n_tokens,
                   int64_t* n_records);
 /* Reference-layout export of frames [frame_from, frame_count) of one lane.

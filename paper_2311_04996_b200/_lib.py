@@ -70,6 +70,7 @@ _SIGS = {
     "ctw_advance": (I32, [P, P, I32, P, I32, I32, P, P, I32, P, P]),
     "ctw_best_path": (I32, [P, P, I32, P, I64, P, P, P, P]),
     "ctw_lane_compact": (I32, [P, P, I32, P]),
+    "ctw_lanes_presize": (I32, [P, P, I32]),
     "ctw_lane_info": (I32, [P, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     "ctw_lane_export": (I32, [P, I32, I64, I64, P, I64, C.POINTER(CtwExport)]),
     "ctw_export_free": (None, [C.POINTER(CtwExport)]),

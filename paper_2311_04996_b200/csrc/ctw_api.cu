@@ -163,6 +163,8 @@ struct ctw_lanes {
   // best-path scratch
   int32_t* d_words = nullptr;
   size_t words_cap = 0;
+  int32_t* h_words = nullptr;  // pinned staging of the whole word window (one D2H)
+  size_t h_words_cap = 0;
   long long* d_woff = nullptr;
   int* d_wcap = nullptr;
   int* d_nwords = nullptr;
@@ -752,7 +754,7 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   dfree(l->d_tcost);
   dfree(l->d_bstatus);
   for (void* p : {(void*)l->h_ids, (void*)l->h_nframes, (void*)l->h_lloff, (void*)l->h_out, (void*)l->h_woff,
-                  (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus})
+                  (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus, (void*)l->h_words})
     if (p) cudaFreeHost(p);
   if (l->ev0) cudaEventDestroy(l->ev0);
   if (l->ev1) cudaEventDestroy(l->ev1);
@@ -1094,6 +1096,14 @@ int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wor
     CUDA_TRY(cudaMemcpyAsync(l->h_nwords, l->d_nwords, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
     CUDA_TRY(cudaMemcpyAsync(l->h_tcost, l->d_tcost, n * sizeof(double), cudaMemcpyDeviceToHost, l->stream));
     CUDA_TRY(cudaMemcpyAsync(l->h_bstatus, l->d_bstatus, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
+    // the whole word window in one copy (pinned), sliced per lane below
+    if ((size_t)tot > l->h_words_cap) {
+      if (l->h_words) cudaFreeHost(l->h_words);
+      CUDA_TRY(cudaMallocHost((void**)&l->h_words, ((size_t)tot + tot / 2) * sizeof(int32_t)));
+      l->h_words_cap = (size_t)tot + tot / 2;
+    }
+    if (tot) CUDA_TRY(cudaMemcpyAsync(l->h_words, l->d_words, (size_t)tot * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                      l->stream));
     CUDA_TRY(cudaStreamSynchronize(l->stream));
     bool redo = false;
     for (int i = 0; i < n; ++i)
@@ -1121,10 +1131,8 @@ int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wor
   if (need > words_cap) return -2;
   for (int i = 0; i < n; ++i) {
     if (status[i] != 0 || l->h_nwords[i] == 0) continue;
-    CUDA_TRY(cudaMemcpyAsync(words + word_off[i], l->d_words + l->h_woff[i], l->h_nwords[i] * sizeof(int32_t),
-                             cudaMemcpyDeviceToHost, l->stream));
+    std::memcpy(words + word_off[i], l->h_words + l->h_woff[i], l->h_nwords[i] * sizeof(int32_t));
   }
-  CUDA_TRY(cudaStreamSynchronize(l->stream));
   return 0;
 }
 
@@ -1215,6 +1223,18 @@ int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* 
   sfree(d_nptab, st);
   sfree(d_kept, st);
   CUDA_TRY(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ctw_lanes_presize(ctw_lanes* l, const int32_t* lane_ids, int32_t n) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  CUDA_TRY(cudaSetDevice(l->g->device));
+  if (int r = check_ids(l, lane_ids, n)) return r;
+  for (int i = 0; i < n; ++i) {
+    CtwLane& L = l->h[lane_ids[i]];
+    if (L.tlog2 < l->tlog2_hint)
+      if (int r = alloc_table(l, lane_ids[i], l->tlog2_hint)) return r;
+  }
   return 0;
 }
 

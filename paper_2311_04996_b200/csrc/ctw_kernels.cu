@@ -1718,36 +1718,51 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
       }
     }
   }
-  if (ln != 0) return;
   if (best_i < 0) {
-    status[warp] = 1;
-    nwords[warp] = 0;
-    total_cost[warp] = INF;
+    if (ln == 0) {
+      status[warp] = 1;
+      nwords[warp] = 0;
+      total_cost[warp] = INF;
+    }
     return;
   }
-  status[warp] = 0;
-  total_cost[warp] = best;
-  int count = 0;
-  for (int r = src[best_i].bp; r >= 0;) {
-    const int2 lk = lane.pages[r >> CTW_PAGE_LOG2]->link[r & (CTW_PAGE - 1)];
-    count += code_len(lane.pool, lk.y);
-    r = lk.x;
-  }
-  nwords[warp] = count;
-  if (count > wcap[warp]) return;
+  // one walk of the prev chain (lane 0): words are written newest-first from
+  // the end of the lane's window, then the warp moves them to its start
+  const int cap = wcap[warp];
   int32_t* w = words + woff[warp];
-  int pos = count;
-  for (int r = src[best_i].bp; r >= 0;) {
-    const int2 lk = lane.pages[r >> CTW_PAGE_LOG2]->link[r & (CTW_PAGE - 1)];
-    const int c = lk.y;
-    if (c > 0) w[--pos] = c;
-    else if (c < 0) {
-      const int32_t* seg = lane.pool + (-c - 1);
-      const int m = seg[0];
-      pos -= m;
-      for (int j = 0; j < m; ++j) w[pos + j] = seg[1 + j];
+  int pos = cap, count = 0;
+  if (ln == 0) {
+    status[warp] = 0;
+    total_cost[warp] = best;
+    for (int r = src[best_i].bp; r >= 0;) {
+      const int2 lk = lane.pages[r >> CTW_PAGE_LOG2]->link[r & (CTW_PAGE - 1)];
+      const int c = lk.y;
+      if (c > 0) {
+        if (pos > 0) w[pos - 1] = c;
+        --pos;
+        ++count;
+      } else if (c < 0) {
+        const int32_t* seg = lane.pool + (-c - 1);
+        const int m = seg[0];
+        for (int j = m - 1; j >= 0; --j) {
+          if (pos > 0) w[pos - 1] = seg[1 + j];
+          --pos;
+        }
+        count += m;
+      }
+      r = lk.x;
     }
-    r = lk.x;
+    nwords[warp] = count;  // > cap: the host retries with a bigger window
+  }
+  count = __shfl_sync(0xFFFFFFFFu, count, 0);
+  pos = __shfl_sync(0xFFFFFFFFu, pos, 0);
+  if (count > cap || pos == 0) return;
+  __syncwarp();
+  for (int k = 0; k < count; k += 32) {
+    const int32_t v = (k + ln < count) ? w[pos + k + ln] : 0;
+    __syncwarp();
+    if (k + ln < count) w[k + ln] = v;
+    __syncwarp();
   }
 }
 
