@@ -409,6 +409,16 @@ def reference_arm(args):
     print(json.dumps(line))
 
 
+def lane_memory(pool):
+    """Token-table sizes and device bytes of the pool's lanes (ctw_lane_capacity)."""
+    caps = [pool.capacity(i) for i in range(pool.size)]
+    hist = {}
+    for c in caps:
+        hist[c["table_log2"]] = hist.get(c["table_log2"], 0) + 1
+    return {"n": len(caps), "table_log2_hist": {str(k): v for k, v in sorted(hist.items())},
+            "bytes_total": sum(c["bytes"] for c in caps)}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -550,7 +560,8 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"},
         "workload_stats": {"emitting_arcs_per_lane_frame": st["arcs"] / max(1, st["frames"]),
                            "tokens_per_lane_frame": st["src_tokens"] / max(1, st["frames"]),
-                           "max_slots": st["max_slots"], "wall_s_timed": t_wall},
+                           "max_slots": st["max_slots"], "wall_s_timed": t_wall,
+                           "lanes": lane_memory(pool)},
         "clocks": clk.summary(),
         "stage_profile": _stage_profile(prof, st),
         "ncu": ncu,

@@ -186,6 +186,10 @@ int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* 
 int ctw_lanes_presize(ctw_lanes* l, const int32_t* lane_ids, int32_t n);
 int ctw_lane_info(ctw_lanes* l, int32_t lane, int64_t* frame_count, int64_t* n_tokens,
                   int64_t* n_records);
+/* Capacities of one lane's device buffers: out6 = {token-table log2 size,
+ * source capacity, history record capacity, frame capacity, olabel pool
+ * capacity, device bytes held by the lane}. */
+int ctw_lane_capacity(ctw_lanes* l, int32_t lane, int64_t* out6);
 /* Reference-layout export of frames [frame_from, frame_count) of one lane.
  * Records get global indices base, base+1, ... in (frame, state) order;
  * predecessors inside the exported range are renumbered, external

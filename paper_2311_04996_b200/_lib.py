@@ -72,6 +72,7 @@ _SIGS = {
     "ctw_lane_compact": (I32, [P, P, I32, P]),
     "ctw_lanes_presize": (I32, [P, P, I32]),
     "ctw_lane_info": (I32, [P, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
+    "ctw_lane_capacity": (I32, [P, I32, P]),
     "ctw_lane_export": (I32, [P, I32, I64, I64, P, I64, C.POINTER(CtwExport)]),
     "ctw_export_free": (None, [C.POINTER(CtwExport)]),
     "ctw_lanes_stats": (I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(F64), C.POINTER(I64),

@@ -1248,6 +1248,27 @@ int ctw_lane_info(ctw_lanes* l, int32_t lane, int64_t* frame_count, int64_t* n_t
   return 0;
 }
 
+int ctw_lane_capacity(ctw_lanes* l, int32_t lane, int64_t* out6) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  if (lane < 0 || lane >= l->n) return fail(-1, "lane id out of range");
+  if (!out6) return fail(-1, "null output");
+  const CtwLane& L = l->h[lane];
+  const uint64_t tcap = 1ull << L.tlog2;
+  const int64_t scap = (int64_t)L.scap + 1;
+  const int64_t bytes = (int64_t)(tcap * sizeof(CtwTok) + CTW_SLOTS_LEN(tcap) * sizeof(uint2) +
+                                  CTW_FRONT_LEN(tcap) * sizeof(uint2)) +
+                        scap * (int64_t)(3 * sizeof(CtwSrc) + sizeof(int32_t)) +
+                        (int64_t)l->hpages[lane].size() * (int64_t)sizeof(CtwRecPage) +
+                        (int64_t)L.fcap * (int64_t)sizeof(int64_t) + (int64_t)L.pcap * (int64_t)sizeof(int32_t);
+  out6[0] = L.tlog2;
+  out6[1] = L.scap;
+  out6[2] = L.rcap;
+  out6[3] = L.fcap;
+  out6[4] = L.pcap;
+  out6[5] = bytes;
+  return 0;
+}
+
 void ctw_export_free(ctw_export* e) {
   if (!e) return;
   free(e->counts);

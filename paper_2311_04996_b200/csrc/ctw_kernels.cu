@@ -50,6 +50,9 @@
 #define CTW_DEFAULT_CLUSTER 8
 #endif
 #define CTW_WARPS (CTW_BS / 32)
+#ifndef CTW_EPS_INLINE
+#define CTW_EPS_INLINE
+#endif
 #define CTW_IPT 4                        // sources per thread per expansion tile
 #define CTW_TILE (CTW_BS * CTW_IPT)
 #define CTW_MAX_SMEM_WIDTH 4096
@@ -113,6 +116,11 @@ __device__ __forceinline__ void snap128(void* addr, unsigned long long& lo, unsi
 __device__ __forceinline__ uint32_t tok_hash(uint32_t s, uint32_t shift) {
   return (s * 0x9E3779B1u) >> shift;
 }
+
+// Graph reads (16 B vector loads through the read-only path).
+__device__ __forceinline__ CtwArc ld_arc(const CtwArc* arcs, uint32_t i) { return arcs[i]; }
+
+__device__ __forceinline__ CtwStateRange ld_range(const CtwStateRange* ranges, uint32_t s) { return ranges[s]; }
 
 struct LaneCtx {
   CtwTok* T;
@@ -543,7 +551,7 @@ __device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphD
 // every rank pushes to its own output segments. Returns CTW_OK or
 // CTW_ERR_EPS_ITERS (divergence: more passes than a convergent closure needs).
 template <bool FSA>
-__device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, FrameCtr* fc, const double* boost,
+__device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, FrameCtr* fc, const double* boost,
                             double relax_eps, double beam, long long pass_cap) {
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x;
@@ -593,26 +601,32 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
     // warps grab 32 frontier items at a time and spread the items' epsilon
     // arcs over their lanes
     const int lane = tid & 31, w = tid >> 5;
-    for (;;) {
-      // guided chunks: 32 items, 8 near the end of the pass (shorter tail
-      // before the barrier)
-      int base = 0, gsz = 32;
+    // guided chunks: 32 items, 8 near the end of the pass (shorter tail
+    // before the barrier); a claim is (base << 1) | (size == 8)
+    auto claim = [&]() -> int {
+      int c = 0;
       if (lane == 0) {
-        if (n_cur - *((volatile int*)&G->pw[q]) < tail) gsz = 8;
-        base = atomicAdd(&G->pw[q], gsz);
+        const bool small = n_cur - *((volatile int*)&G->pw[q]) < tail;
+        c = (atomicAdd(&G->pw[q], small ? 8 : 32) << 1) | (small ? 1 : 0);
       }
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      gsz = __shfl_sync(0xFFFFFFFFu, gsz, 0);
+      return __shfl_sync(0xFFFFFFFFu, c, 0);
+    };
+    for (;;) {
+      const int cur_claim = claim();
+      const int base = cur_claim >> 1, gsz = (cur_claim & 1) ? 8 : 32;
       if (base >= n_cur) break;
       const int nv = min(gsz, n_cur - base);
       if (lane == 0) atomicAdd(&sm.eps_items, nv);
       int deg = 0;
+      uint2 it = make_uint2(0u, 0u);
       if (lane < nv) {
         const int i = base + lane;
-        const uint2 it = i < n_first ? in0[i] : in1[i - n_first];
+        it = i < n_first ? in0[i] : in1[i - n_first];
+      }
+      if (lane < nv) {
         // the range and the entry are independent loads: issue them together
         const CtwTok* eu = &L.T[it.x];
-        const CtwStateRange r = g.ranges[FSA ? (it.y & L.smask) : it.y];
+        const CtwStateRange r = ld_range(g.ranges, FSA ? (it.y & L.smask) : it.y);
         const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
         const unsigned long long gu = __ldcg(&eu->gpos);
         deg = (int)(r.emit_beg - r.eps_beg);
@@ -660,7 +674,7 @@ __device__ int eps_fixpoint(Smem& sm, const LaneCtx& L, const GraphDev& g, Frame
         }
         const uint32_t o = (uint32_t)(k - sm.ep.off[w][lo]);
         const uint32_t a = sm.ep.beg[w][lo] + o;
-        const CtwArc arc = g.arcs[a];
+        const CtwArc arc = ld_arc(g.arcs, a);
         uint32_t ikey = 0;  // the item's token key (phrase automaton state)
         if (FSA) {
           const int ii = base + lo;
@@ -919,7 +933,9 @@ __device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost,
   return min(max(b, 0), CTW_NB - 1);
 }
 
-#define CTW_UNR 4  // independent table loads in flight per thread in slot sweeps
+#ifndef CTW_UNR
+#define CTW_UNR 2  // independent table loads in flight per thread in slot sweeps (4 spills: -2%)
+#endif
 
 // One sweep over this rank's slots: gathers every slot's final (key, tb|aux)
 // into sv (this rank's part of the compact value array; coalesced for the
@@ -1170,14 +1186,15 @@ __device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const Graph
                                          const double* nll_s, bool smem_ll, long long row0, double neg_scale,
                                          const double* boost, uint32_t arc_i, double cost, uint32_t src_idx,
                                          uint32_t src_key) {
-  const CtwArc arc = g.arcs[arc_i];
+  const CtwArc arc = ld_arc(g.arcs, arc_i);
   emit_arc_loaded<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, arc_i, cost, src_idx, src_key, arc);
 }
 
 // FSA: some lane of the launch has a phrase automaton (token keys carry its
 // state); the plain instantiation keeps the hot path free of it.
 template <bool FSA>
-__global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lanes, GraphDev g, ChunkArgs a, CtwLaneOut* out) {
+__global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lanes, const __grid_constant__ GraphDev g,
+                                                                const __grid_constant__ ChunkArgs a, CtwLaneOut* out) {
   extern __shared__ double nll_s[];
   __shared__ Smem sm;
   cg::cluster_group cl = cg::this_cluster();
@@ -1206,8 +1223,11 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   int err_frame = -1;
   int n_slots_max = 0;
   long long src_total = 0, rec_need = 0;
-  long long prof[CTW_NPROF] = {0};
+  // stage counters: rank-local, tid 0 only, kept in shared memory (a
+  // register array here would be live in every thread of the frame loop)
+  long long* prof = reinterpret_cast<long long*>(sm.mydiag);
   if (tid == 0) {
+    for (int k = 0; k < CTW_NPROF; ++k) prof[k] = 0;
     sm.status_l = CTW_OK;
     sm.epoch = 0;
     sm.st_pub[0] = sm.st_pub[1] = 0;
@@ -1266,22 +1286,27 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
 
     // ---- emitting expansion, load-balanced over out-degree ----
     const int lane_ = tid & 31, w = tid >> 5;
+    // a claim is (base << 1) | (size == 8): 32 sources, 8 in the guided tail
+    auto claim_e = [&]() -> int {
+      int c = 0;
+      if (lane_ == 0) {
+        const bool small = n_src - *((volatile int*)&fc->work_e) < 32 * CTW_WARPS * R;
+        c = (atomicAdd(&fc->work_e, small ? 8 : 32) << 1) | (small ? 1 : 0);
+      }
+      return __shfl_sync(0xFFFFFFFFu, c, 0);
+    };
     for (;;) {
       // warps grab 32 sources at a time and spread their emitting arcs over
       // the lanes (warp scan of out-degrees); sources with more than
       // CTW_BIG arcs go to the arc-parallel list instead
-      int base = 0, gsz = 32;
-      if (lane_ == 0) {
-        if (n_src - *((volatile int*)&fc->work_e) < 32 * CTW_WARPS * R) gsz = 8;  // guided tail
-        base = atomicAdd(&fc->work_e, gsz);
-      }
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
-      gsz = __shfl_sync(0xFFFFFFFFu, gsz, 0);
+      const int cur_claim = claim_e();
+      const int base = cur_claim >> 1, gsz = (cur_claim & 1) ? 8 : 32;
       if (base >= n_src) break;
       const int nv = min(gsz, n_src - base);
       int deg = 0;
+      CtwSrc t;
+      if (lane_ < nv) t = src[base + lane_];
       if (lane_ < nv) {
-        const CtwSrc t = src[base + lane_];
         const CtwStateRange r{0u, t.emit_beg, t.emit_end, 0u};  // cached with the token
         deg = (int)(r.emit_end - r.emit_beg);
         if (deg > CTW_BIG) {
@@ -1482,7 +1507,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           const uint2 it = ib[i];
           const uint32_t h = it.x, st2 = it.y;
           if (!keep(key, st2)) continue;
-          const CtwStateRange rg = g.ranges[FSA ? (st2 & L.smask) : st2];  // independent of the walk: overlaps it
+          const CtwStateRange rg = ld_range(g.ranges, FSA ? (st2 & L.smask) : st2);  // independent of the walk: overlaps it
           const WalkEnd wk = walk(L, g, v0, src, pend, hop_cap);
           if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
           const int32_t code = record_code(sm, L, g, h, wk);
@@ -1532,8 +1557,6 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   // per-rank diagnostics -> rank 0 (plain stores + remote loads between two
   // barriers; the second keeps every rank's shared memory alive until rank 0
   // has read it)
-  if (tid == 0)
-    for (int k = 0; k < CTW_NPROF; ++k) sm.mydiag[k] = (unsigned long long)prof[k];
   cl.sync();
   long long dsum[6] = {0, 0, 0, 0, 0, 0};
   if (rank == 0 && tid == 0)

@@ -327,6 +327,13 @@ class LanePool:
                 "reruns": int(v[4]), "calls": int(v[5]),
                 "grow_lanes": {"table": int(v[6]), "history": int(v[7]), "pool": int(v[8]), "sources": int(v[9])}}
 
+    def capacity(self, lane: int) -> dict:
+        """Device buffer capacities of one lane (ctw_lane_capacity)."""
+        v = np.zeros(6, np.int64)
+        _lib.check(_lib.load().ctw_lane_capacity(self.handle, int(lane), _lib.ptr(v)), "lane capacity")
+        return {"table_log2": int(v[0]), "sources": int(v[1]), "records": int(v[2]), "frames": int(v[3]),
+                "olabel_pool": int(v[4]), "bytes": int(v[5])}
+
     def reset_stats(self) -> None:
         _lib.load().ctw_lanes_reset_stats(self.handle)
 
