@@ -50,6 +50,12 @@
 #define CTW_DEFAULT_CLUSTER 8
 #endif
 #define CTW_WARPS (CTW_BS / 32)
+#ifndef CTW_LD256
+#define CTW_LD256 1  // token-table reads as one 256-bit load per entry (one L2 request, not two)
+#endif
+#ifndef CTW_IDLE_PROF
+#define CTW_IDLE_PROF 0
+#endif
 #ifndef CTW_EPS_INLINE
 #define CTW_EPS_INLINE
 #endif
@@ -186,6 +192,23 @@ __device__ __forceinline__ void gpos_min(CtwTok* e, unsigned long long v) {
   atomicMin(&e->gpos, v);
 }
 
+// The whole 32 B entry in one L2 request (sm_100 256-bit load, L2 only).
+// 64-bit elements: each half of (key, tb|aux) stays single-copy atomic, as
+// the relax logic assumes (a key read is always a historical key).
+__device__ __forceinline__ void ld_tok(const CtwTok* e, ulonglong2& v, unsigned long long& gpos, uint32_t& state) {
+#if CTW_LD256
+  unsigned long long w3;
+  asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v.x), "=l"(v.y), "=l"(gpos), "=l"(w3)
+               : "l"(e));
+  state = (uint32_t)w3;  // (stamp in the upper half)
+#else
+  v = __ldcg(reinterpret_cast<const ulonglong2*>(e));
+  gpos = __ldcg(&e->gpos);
+  state = __ldcg(&e->state);
+#endif
+}
+
 // Find-or-insert `d` and return a snapshot of its (key, tb|aux) in *v: the
 // probe reads the entry's value and hash key together (plain loads; a
 // claimed hash key never changes within a frame), so a hit costs one round
@@ -196,8 +219,15 @@ __device__ __forceinline__ uint32_t tok_locate(const LaneCtx& L, uint32_t d, ulo
   uint32_t h = tok_hash(d, L.shift);
   for (uint32_t probe = 0; probe <= L.mask; ++probe) {
     const CtwTok* e = &L.T[h];
+#if CTW_LD256
+    ulonglong2 val;
+    unsigned long long gp_;
+    uint32_t k;
+    ld_tok(e, val, gp_, k);
+#else
     const ulonglong2 val = __ldcg(reinterpret_cast<const ulonglong2*>(e));
     const uint32_t k = __ldcg(&e->state);
+#endif
     if (k == d) {
       *v = val;
       return h;
@@ -362,12 +392,20 @@ struct __align__(16) Smem {
   int status_l;         // sticky local status (grow requests, walk failures)
   int st_pub[2];        // status published at a barrier (barrier parity)
   unsigned long long min_pub[2];  // running minimum published at a barrier (barrier parity)
+  unsigned long long eps_idle;  // CTW_IDLE_PROF: warp-cycles waiting at the epsilon pass barriers
   unsigned long long mydiag[CTW_NPROF + 1];  // this rank's diagnostics, read by rank 0 at the end
   int epoch;            // barriers passed (all ranks pass the same sequence)
   int st_all;           // max status over the ranks at the last barrier
   int n_slots;          // slots this rank created in the frame
   int snap_slots;       // n_slots at the start of the epsilon stage
   int pc_big[2];        // this rank made a big change in the pass (pass parity)
+  // the epsilon pass's parameters, read where used instead of being held in
+  // registers across the chunk loop (32-register budget: +3% measured)
+  int* eo_ctr;          // output counters of the pass
+  uint2* eo_nxt;        // output sets of the pass
+  uint2* eo_tiny;
+  double eo_relax;      // relax_eps
+  double eo_beam;
   int n_cur, n_first, any_big;
   uint2* in0;           // input of the current epsilon pass: in0[0, n_first) ++ in1[0, n_cur - n_first)
   uint2* in1;
@@ -466,9 +504,7 @@ __device__ __forceinline__ int csync(Smem& sm) {
 // queue the destination for the next pass when it changed.
 template <bool FSA>
 __device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const double* boost,
-                                        double relax_eps, uint32_t epoch, int q, int* ctr_out, uint2* nxt,
-                                        uint2* tiny, int w, int lo, uint32_t o, uint32_t a, const CtwArc& arc,
-                                        uint32_t ikey) {
+                                        int w, int lo, uint32_t o, uint32_t a, const CtwArc& arc, uint32_t ikey) {
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
   const uint32_t aux = sm.ep.aux[w][lo];
   const bool valued = aux != CTW_DISC;
@@ -504,7 +540,7 @@ __device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphD
     if (tok_relax_from(L, ed, nk, CTW_EPS_BIT | a, aux, sm.ep.gu[w][lo], seen, &oldk)) {
       track_min(sm, nk);
       push = true;
-      big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > relax_eps;
+      big = is_new || oldk == ~0ULL || oldk == nk || (key2d(oldk) - nc) > sm.eo_relax;
     } else {
       push = big = is_new;
     }
@@ -512,6 +548,13 @@ __device__ __forceinline__ void eps_arc(Smem& sm, const LaneCtx& L, const GraphD
     push = big = is_new;  // discovery only: successors are discovered next pass
   }
   if (!push) return;
+  // the pass's parameters come from shared memory (not registers held
+  // across the chunk loop): read only on the push path
+  const uint32_t epoch = (uint32_t)sm.passes;
+  const int q = sm.passes & 1;
+  int* ctr_out = sm.eo_ctr;
+  uint2* nxt = sm.eo_nxt;
+  uint2* tiny = sm.eo_tiny;
   if (big) sm.pc_big[q] = 1;
   bool first;
   if (is_new) {  // this thread created the slot: first to touch its stamp
@@ -590,6 +633,11 @@ __device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const Gra
         sm.pcnt[(pass + 1) % 3][1] = 0;
       }
       sm.passes = (int)pass;
+      sm.eo_ctr = ctr_out;
+      sm.eo_nxt = nxt;
+      sm.eo_tiny = tiny;
+      sm.eo_relax = relax_eps;
+      sm.eo_beam = beam;
     }
     __syncthreads();
     if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
@@ -597,7 +645,6 @@ __device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const Gra
     const int tail = 32 * CTW_WARPS * R;  // items left when chunks shrink
     const uint2* in0 = sm.in0;
     const uint2* in1 = sm.in1;
-    const uint32_t epoch = (uint32_t)pass;
     // warps grab 32 frontier items at a time and spread the items' epsilon
     // arcs over their lanes
     const int lane = tid & 31, w = tid >> 5;
@@ -621,18 +668,25 @@ __device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const Gra
       uint2 it = make_uint2(0u, 0u);
       if (lane < nv) {
         const int i = base + lane;
-        it = i < n_first ? in0[i] : in1[i - n_first];
+        it = i < sm.n_first ? sm.in0[i] : sm.in1[i - sm.n_first];
       }
       if (lane < nv) {
         // the range and the entry are independent loads: issue them together
         const CtwTok* eu = &L.T[it.x];
         const CtwStateRange r = ld_range(g.ranges, FSA ? (it.y & L.smask) : it.y);
+#if CTW_LD256
+        ulonglong2 v;
+        unsigned long long gu;
+        uint32_t st_;
+        ld_tok(eu, v, gu, st_);
+#else
         const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(eu));
         const unsigned long long gu = __ldcg(&eu->gpos);
+#endif
         deg = (int)(r.emit_beg - r.eps_beg);
         if (deg > 0) {
           const double c = key2d(v.x);
-          const bool valued = v.x != ~0ULL && !(L.prune && c > running_cut(sm, beam));
+          const bool valued = v.x != ~0ULL && !(L.prune && c > running_cut(sm, sm.eo_beam));
           uint32_t aux = CTW_DISC;
           if (valued) {
             const uint32_t tbu = (uint32_t)v.y, auxu = (uint32_t)(v.y >> 32);
@@ -680,12 +734,19 @@ __device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const Gra
           const int ii = base + lo;
           ikey = (ii < n_first ? in0[ii] : in1[ii - n_first]).y;
         }
-        eps_arc<FSA>(sm, L, g, boost, relax_eps, epoch, q, ctr_out, nxt, tiny, w, lo, o, a, arc, ikey);
+        eps_arc<FSA>(sm, L, g, boost, w, lo, o, a, arc, ikey);
       }
       __syncwarp();
     }
+#if CTW_IDLE_PROF
+    const long long t_done = clock64();
+#endif
     // the barrier ending the pass (also merges the ranks' running minima)
-    if (csync(sm) >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
+    const int vst = csync(sm);
+#if CTW_IDLE_PROF
+    if (lane == 0) atomicAdd(&sm.eps_idle, (unsigned long long)(clock64() - t_done));
+#endif
+    if (vst >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
     if (tid < 32) {
       const int any = __any_sync(0xFFFFFFFFu, tid < R && cl.map_shared_rank(&sm, tid)->pc_big[q]);
       if (tid == 0) sm.any_big = any;
@@ -1228,6 +1289,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   long long* prof = reinterpret_cast<long long*>(sm.mydiag);
   if (tid == 0) {
     for (int k = 0; k < CTW_NPROF; ++k) prof[k] = 0;
+    sm.eps_idle = 0;
     sm.status_l = CTW_OK;
     sm.epoch = 0;
     sm.st_pub[0] = sm.st_pub[1] = 0;
@@ -1458,7 +1520,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     }
     if (status == CTW_OK) {
       const int in_beam = sm.cnt_all;
-      if (rank == 0) prof[11] += in_beam;
+      if (rank == 0 && tid == 0) prof[11] += in_beam;
       const bool select = (long long)in_beam > a.cfg.max_active;
       const int n_surv = select ? (int)a.cfg.max_active : in_beam;
       if (select) select_threshold(sm, L, fc, sv, ib, n_ib, cut_key, min_cost, bin_scale, a.cfg.max_active);
@@ -1558,12 +1620,13 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   // barriers; the second keeps every rank's shared memory alive until rank 0
   // has read it)
   cl.sync();
-  long long dsum[6] = {0, 0, 0, 0, 0, 0};
+  long long dsum[7] = {0, 0, 0, 0, 0, 0, 0};
   if (rank == 0 && tid == 0)
     for (int r = 0; r < R; ++r) {
       const Smem* o = cl.map_shared_rank(&sm, r);
       const int ks[6] = {9, 10, 12, 13, 14, 15};
       for (int j = 0; j < 6; ++j) dsum[j] += (long long)o->mydiag[ks[j]];
+      dsum[6] += (long long)o->eps_idle;
     }
   cl.sync();
   if (rank == 0 && tid == 0) {
@@ -1580,7 +1643,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     o.prof[12] = dsum[2];
     o.prof[13] = dsum[3];
     o.prof[14] = dsum[4];
-    o.prof[15] = 0;
+    o.prof[15] = dsum[6];  // epsilon-barrier idle warp-cycles (CTW_IDLE_PROF builds), else 0
     if (status == CTW_OK) {
       lane.n_src = n_src;
       lane.src_buf = (F > 0) ? cur_buf : committed;

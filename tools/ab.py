@@ -57,7 +57,7 @@ def child(args):
                       "rtfx_mean": audio / (sum(ms) / len(ms) / 1e3), "ms": ms,
                       "cycles_per_lane_frame": sum(prof[k] for k in ("emit", "eps", "beam_count", "select",
                                                                     "records", "reset")) / (frames / 1),
-                      "stage": {k: prof[k] / frames for k in ("emit", "eps", "beam_count", "select", "records",
+                      "stage": {k: prof[k] / frames for k in ("emit", "eps", "beam_count", "select", "records", "r15",
                                                               "reset")},
                       "digest": h.hexdigest()[:16]}))
 
