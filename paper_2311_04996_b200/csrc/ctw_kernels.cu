@@ -392,6 +392,9 @@ struct __align__(16) Smem {
   int status_l;         // sticky local status (grow requests, walk failures)
   int st_pub[2];        // status published at a barrier (barrier parity)
   unsigned long long min_pub[2];  // running minimum published at a barrier (barrier parity)
+  // kernel-level bookkeeping kept by tid 0 (not live registers in every thread)
+  long long tclk, src_total, rec_need, n_rec;
+  int n_slots_max, err_frame;
   unsigned long long eps_idle;  // CTW_IDLE_PROF: warp-cycles waiting at the epsilon pass barriers
   unsigned long long mydiag[CTW_NPROF + 1];  // this rank's diagnostics, read by rank 0 at the end
   int epoch;            // barriers passed (all ranks pass the same sequence)
@@ -1278,17 +1281,18 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   int cur_buf = lane.src_buf;
   const int w0 = (cur_buf + 1) % 3, w1 = (cur_buf + 2) % 3;
   const int committed = cur_buf;
-  long long n_rec = lane.n_rec;
   int pend_valid = lane.pend_valid;
   int status = CTW_OK;
-  int err_frame = -1;
-  int n_slots_max = 0;
-  long long src_total = 0, rec_need = 0;
   // stage counters: rank-local, tid 0 only, kept in shared memory (a
   // register array here would be live in every thread of the frame loop)
   long long* prof = reinterpret_cast<long long*>(sm.mydiag);
   if (tid == 0) {
     for (int k = 0; k < CTW_NPROF; ++k) prof[k] = 0;
+    sm.src_total = 0;
+    sm.rec_need = 0;
+    sm.n_slots_max = 0;
+    sm.err_frame = -1;
+    sm.n_rec = lane.n_rec;
     sm.eps_idle = 0;
     sm.status_l = CTW_OK;
     sm.epoch = 0;
@@ -1308,7 +1312,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   cl.sync();
 
   for (int f = 0; f < F; ++f) {
-    long long tclk = clock64();
+    if (tid == 0) sm.tclk = clock64();
     FrameCtr* fc = &G->fc[f & 1];
     L.slot_ctr = &fc->nslot;
     const CtwSrc* src = lane.src[cur_buf];
@@ -1344,7 +1348,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
         for (int j = 0; j < 3; ++j) sm.pcnt[j][0] = sm.pcnt[j][1] = 0;
       }
     }
-    src_total += n_src;
+    if (tid == 0) sm.src_total += n_src;
 
     // ---- emitting expansion, load-balanced over out-degree ----
     const int lane_ = tid & 31, w = tid >> 5;
@@ -1464,8 +1468,8 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
 
     if (rank == 0 && tid == 0) {
       const long long t = clock64();
-      prof[0] += t - tclk;
-      tclk = t;
+      prof[0] += t - sm.tclk;
+      sm.tclk = t;
     }
     // ---- epsilon closure ----
     int st = CTW_OK;
@@ -1483,8 +1487,8 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     if (tid == 0) {
       if (rank == 0) {
         const long long t = clock64();
-        prof[1] += t - tclk;
-        tclk = t;
+        prof[1] += t - sm.tclk;
+        sm.tclk = t;
         prof[6] += sm.passes;
         prof[8] += n_all;
       }
@@ -1495,7 +1499,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       prof[14] += sm.eps_disc;
       prof[15] += sm.arcs_f;  // (moved to arcs_expanded at the end)
     }
-    n_slots_max = max(n_slots_max, n_all);
+    if (tid == 0) sm.n_slots_max = max(sm.n_slots_max, n_all);
     if (st != CTW_OK) status = st;
     else if (vote >= CTW_GROW_TABLE) status = vote;
     else if (n_alloc == 0) status = CTW_ERR_NO_SURVIVORS;
@@ -1515,8 +1519,8 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     const int n_ib = sm.cnt_all;
     if (rank == 0 && tid == 0) {
       const long long t = clock64();
-      prof[2] += t - tclk;
-      tclk = t;
+      prof[2] += t - sm.tclk;
+      sm.tclk = t;
     }
     if (status == CTW_OK) {
       const int in_beam = sm.cnt_all;
@@ -1526,16 +1530,16 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       if (select) select_threshold(sm, L, fc, sv, ib, n_ib, cut_key, min_cost, bin_scale, a.cfg.max_active);
       if (rank == 0 && tid == 0) {
         const long long t = clock64();
-        prof[3] += t - tclk;
+        prof[3] += t - sm.tclk;
         prof[7] += select;
-        tclk = t;
+        sm.tclk = t;
       }
-      if (n_rec + n_surv > lane.rcap) {
+      if (sm.n_rec + n_surv > lane.rcap) {
         status = CTW_GROW_HIST;
-        rec_need = n_rec + n_surv;
+        if (tid == 0) sm.rec_need = sm.n_rec + n_surv;
       } else if (n_surv > lane.scap) {
         status = CTW_GROW_SRC;
-        rec_need = n_surv;
+        if (tid == 0) sm.rec_need = n_surv;
       } else {
         // ---- records + next sources: per-thread counts, one block scan,
         // one cluster counter for the rank's base, then independent
@@ -1573,7 +1577,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           const WalkEnd wk = walk(L, g, v0, src, pend, hop_cap);
           if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
           const int32_t code = record_code(sm, L, g, h, wk);
-          const long long r = n_rec + pos;
+          const long long r = sm.n_rec + pos;
           CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
           const int ro = (int)(r & (CTW_PAGE - 1));
           pg->link[ro] = make_int2(wk.bp, code);
@@ -1589,27 +1593,29 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           nsrc[pos] = ns;
           ++pos;
         }
-        if (rank == 0 && tid == 0) lane.frame_base[lane.frame_count + f] = n_rec;
+        if (rank == 0 && tid == 0) lane.frame_base[lane.frame_count + f] = sm.n_rec;
         const int v2 = csync(sm);  // (H)
-        if (tid == 0) sm.tot_surv = *((volatile int*)&fc->rec_ctr);
+        if (tid == 0) {
+          sm.tot_surv = *((volatile int*)&fc->rec_ctr);
+          sm.n_rec += sm.tot_surv;
+        }
         __syncthreads();
-        n_rec += sm.tot_surv;
         n_src = sm.tot_surv;
         if (v2 != CTW_OK) status = v2;  // grow request (>= 16) or a failed walk (ERR_EPS_ITERS)
       }
     }
     if (rank == 0 && tid == 0) {
       const long long t = clock64();
-      prof[4] += t - tclk;
-      tclk = t;
+      prof[4] += t - sm.tclk;
+      sm.tclk = t;
     }
 
     // ---- reset every table entry this rank created (also on failure) ----
     reset_slots(L, n_all);
     __syncthreads();
-    if (rank == 0 && tid == 0) prof[5] += clock64() - tclk;
+    if (rank == 0 && tid == 0) prof[5] += clock64() - sm.tclk;
     if (status != CTW_OK) {
-      err_frame = f;
+      if (tid == 0) sm.err_frame = f;
       break;
     }
     cur_buf = nxt_buf;
@@ -1632,11 +1638,11 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   if (rank == 0 && tid == 0) {
     CtwLaneOut o;
     o.status = status;
-    o.err_frame = err_frame;
-    o.n_slots_max = n_slots_max;
+    o.err_frame = sm.err_frame;
+    o.n_slots_max = sm.n_slots_max;
     o.arcs_expanded = dsum[5];
-    o.src_total = src_total;
-    o.rec_need = rec_need;
+    o.src_total = sm.src_total;
+    o.rec_need = sm.rec_need;
     for (int k = 0; k < CTW_NPROF; ++k) o.prof[k] = prof[k];
     o.prof[9] = dsum[0];
     o.prof[10] = dsum[1];
@@ -1649,7 +1655,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       lane.src_buf = (F > 0) ? cur_buf : committed;
       lane.frame_count += F;
       lane.pool_used = sm.pool_used;
-      lane.n_rec = n_rec;
+      lane.n_rec = sm.n_rec;
       lane.pend_valid = pend_valid;
     }
     o.n_src = lane.n_src;
