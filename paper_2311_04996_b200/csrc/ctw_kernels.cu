@@ -1111,13 +1111,13 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
   const int tid = threadIdx.x;
   Smem* G = L.G;
   if (L.rank == 0 && tid < 32) {
-    uint32_t cnt[CTW_NB / 32];
+    // warp 0 of rank 0: lane t owns bins [32t, 32t + 32); one warp scan of
+    // the lane sums finds the lane holding the k-th smallest cost, which
+    // re-reads its bins (no per-thread array: it would spill)
+    const uint32_t* bh = fc->bhist + tid * (CTW_NB / 32);
     uint32_t sum = 0;
-#pragma unroll
-    for (int j = 0; j < CTW_NB / 32; ++j) {
-      cnt[j] = fc->bhist[tid * (CTW_NB / 32) + j];
-      sum += cnt[j];
-    }
+#pragma unroll 8
+    for (int j = 0; j < CTW_NB / 32; ++j) sum += bh[(j + tid) & (CTW_NB / 32 - 1)];  // rotated: fewer bank conflicts
     uint32_t incl = sum;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
@@ -1128,13 +1128,14 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
     if (excl < need && need <= incl) {
       uint32_t run = excl;
       for (int j = 0; j < CTW_NB / 32; ++j) {
-        if (run + cnt[j] >= need) {
+        const uint32_t c = bh[j];
+        if (run + c >= need) {
           sm.sel_bin = tid * (CTW_NB / 32) + j;
           sm.sel_need = (int)(need - run);
-          sm.sel_bcount = (int)cnt[j];
+          sm.sel_bcount = (int)c;
           break;
         }
-        run += cnt[j];
+        run += c;
       }
     }
     if (tid == 0) {
