@@ -13,7 +13,7 @@ from .decoder import (DecodeFailure, DecoderConfig, DecodeState, FlatGraph, Hypo
 from .errors import BoostError, BoostParseError, CtcWfstError, DecodeError, FstParseError, GraphError, StreamError
 from .kernels import KERNEL_NAME, compiled_available
 from .graphio import load_graph, save_graph
-from .lattice import Lattice, PhraseBoost, decode_lattices
+from .lattice import Lattice, PhraseBoost, decode_lattices, nbest_lattices
 from .streaming import BatcherConfig, Chunk, StreamPool
 from .wfst import Arc, SymbolTable, Wfst, arc_sort, read_fst_text, read_symbols, write_fst_text, write_symbols
 

@@ -142,7 +142,10 @@ struct __align__(16) LatSmem {
   unsigned long long items, pruned;
 };
 
-__global__ void __launch_bounds__(LAT_BS) k_lattice(LatArgs a) {
+#ifndef LAT_MINB
+#define LAT_MINB 4  // 4 CTAs (64 warps) per SM: every lane of a 512-lane batch resident (61 -> 32 registers; lattice stage -32 %)
+#endif
+__global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
   __shared__ LatSmem sm;
   const int tid = threadIdx.x;
   CtwLatEntry& E = a.ent[blockIdx.x];

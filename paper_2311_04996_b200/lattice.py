@@ -268,4 +268,23 @@ def build_lattices(pool, states, mats, on_dev, packed, hyps, lattice_beam: float
     return res
 
 
-__all__ = ["Lattice", "PhraseBoost", "decode_lattices", "DecodeFailure"]
+def nbest_lattices(lattices: Sequence, n: int, max_pops: int = 2_000_000, phrases: "PhraseBoost | None" = None,
+                   workers: int | None = None) -> list:
+    """``Lattice.nbest`` over many lattices on a host thread pool (the C
+    search runs with the GIL released): a list of n-best lists in input
+    order; a DecodeFailure entry stays a DecodeFailure."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(lat):
+        return lat.nbest(n, max_pops=max_pops, phrases=phrases) if isinstance(lat, Lattice) else lat
+
+    lattices = list(lattices)
+    workers = workers or min(len(lattices), os.cpu_count() or 1)
+    if workers <= 1 or len(lattices) <= 1:
+        return [one(x) for x in lattices]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(one, lattices))
+
+
+__all__ = ["Lattice", "PhraseBoost", "decode_lattices", "nbest_lattices", "DecodeFailure"]

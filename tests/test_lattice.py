@@ -181,3 +181,16 @@ def test_lattice_batch_and_boost():
         nb = lat.nbest(3)
         assert nb[0].words == h.words
         assert lat.num_arcs > 0
+
+
+def test_nbest_lattices_pool_matches_serial():
+    """nbest_lattices (host thread pool) returns each lattice's own n-best."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_lattices, nbest_lattices, synth
+
+    s = _system(num_units=12, num_words=40, order=3, seed=4, min_pron=1, max_pron=4)
+    utts = synth.planted_utterances(s, 8, 30, seed=9, gap=3.0, noise=1.0)
+    lats = decode_lattices(s.graph, DecoderConfig(beam=14.0, max_active=300), utts, lattice_beam=4.0)
+    serial = [lat.nbest(5) for lat in lats]
+    pooled = nbest_lattices(lats, 5, workers=4)
+    assert [[(h.words, h.total_cost) for h in x] for x in pooled] == \
+        [[(h.words, h.total_cost) for h in x] for x in serial]
