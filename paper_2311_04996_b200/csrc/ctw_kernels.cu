@@ -53,6 +53,18 @@
 #ifndef CTW_LD256
 #define CTW_LD256 1  // token-table reads as one 256-bit load per entry (one L2 request, not two)
 #endif
+#ifndef CTW_EMPF
+#define CTW_EMPF 1  // emitting stage: next round's arc load issued ahead (-3% emit cycles)
+#endif
+// Guided work chunks: chunk size once fewer than 32 items per warp of the
+// lane remain (measured: 16 for the emitting stage; the epsilon passes are
+// fastest without shrinking -- more claims cost more than the shorter tail)
+#ifndef CTW_EMIT_TAIL_SZ
+#define CTW_EMIT_TAIL_SZ 16
+#endif
+#ifndef CTW_EPS_TAIL_SZ
+#define CTW_EPS_TAIL_SZ 32
+#endif
 #ifndef CTW_IDLE_PROF
 #define CTW_IDLE_PROF 0
 #endif
@@ -651,19 +663,24 @@ __device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const Gra
     // warps grab 32 frontier items at a time and spread the items' epsilon
     // arcs over their lanes
     const int lane = tid & 31, w = tid >> 5;
-    // guided chunks: 32 items, 8 near the end of the pass (shorter tail
-    // before the barrier); a claim is (base << 1) | (size == 8)
+    // chunks of 32 items (CTW_EPS_TAIL_SZ near the end of the pass when
+    // guided); a claim is (base << 1) | (size == CTW_EPS_TAIL_SZ)
     auto claim = [&]() -> int {
       int c = 0;
       if (lane == 0) {
+#if CTW_EPS_TAIL_SZ < 32
         const bool small = n_cur - *((volatile int*)&G->pw[q]) < tail;
-        c = (atomicAdd(&G->pw[q], small ? 8 : 32) << 1) | (small ? 1 : 0);
+#else
+        const bool small = false;  // (no remote read of the counter)
+        (void)tail;
+#endif
+        c = (atomicAdd(&G->pw[q], small ? CTW_EPS_TAIL_SZ : 32) << 1) | (small ? 1 : 0);
       }
       return __shfl_sync(0xFFFFFFFFu, c, 0);
     };
     for (;;) {
       const int cur_claim = claim();
-      const int base = cur_claim >> 1, gsz = (cur_claim & 1) ? 8 : 32;
+      const int base = cur_claim >> 1, gsz = (cur_claim & 1) ? CTW_EPS_TAIL_SZ : 32;
       if (base >= n_cur) break;
       const int nv = min(gsz, n_cur - base);
       if (lane == 0) atomicAdd(&sm.eps_items, nv);
@@ -1358,7 +1375,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       int c = 0;
       if (lane_ == 0) {
         const bool small = n_src - *((volatile int*)&fc->work_e) < 32 * CTW_WARPS * R;
-        c = (atomicAdd(&fc->work_e, small ? 8 : 32) << 1) | (small ? 1 : 0);
+        c = (atomicAdd(&fc->work_e, small ? CTW_EMIT_TAIL_SZ : 32) << 1) | (small ? 1 : 0);
       }
       return __shfl_sync(0xFFFFFFFFu, c, 0);
     };
@@ -1367,7 +1384,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       // the lanes (warp scan of out-degrees); sources with more than
       // CTW_BIG arcs go to the arc-parallel list instead
       const int cur_claim = claim_e();
-      const int base = cur_claim >> 1, gsz = (cur_claim & 1) ? 8 : 32;
+      const int base = cur_claim >> 1, gsz = (cur_claim & 1) ? CTW_EMIT_TAIL_SZ : 32;
       if (base >= n_src) break;
       const int nv = min(gsz, n_src - base);
       int deg = 0;
@@ -1402,6 +1419,44 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
       if (lane_ == 0) atomicAdd(&sm.arcs_f, total);
       __syncwarp();
+#if CTW_EMPF
+      // software pipeline over the rounds of 32 arcs: the next round's arc
+      // load is in flight while this round's destination is located and
+      // relaxed
+      auto src_of = [&](int k) -> int {  // last source with off <= k
+        int lo = 0, hi = nv - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.em.off[w][mid] <= k) lo = mid;
+          else hi = mid - 1;
+        }
+        return lo;
+      };
+      int lo = 0;
+      uint32_t ai = 0;
+      CtwArc arc{};
+      if (lane_ < total) {
+        lo = src_of(lane_);
+        ai = sm.em.beg[w][lo] + (uint32_t)(lane_ - sm.em.off[w][lo]);
+        arc = ld_arc(g.arcs, ai);
+      }
+      for (int k = lane_; k < total; k += 32) {
+        const int kn = k + 32;
+        int lon = 0;
+        uint32_t ain = 0;
+        CtwArc arcn{};
+        if (kn < total) {
+          lon = src_of(kn);
+          ain = sm.em.beg[w][lon] + (uint32_t)(kn - sm.em.off[w][lon]);
+          arcn = ld_arc(g.arcs, ain);
+        }
+        emit_arc_loaded<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, ai, sm.em.cost[w][lo],
+                             (uint32_t)(base + lo), FSA ? (uint32_t)src[base + lo].state : 0u, arc);
+        lo = lon;
+        ai = ain;
+        arc = arcn;
+      }
+#else
       for (int k = lane_; k < total; k += 32) {
         int lo = 0, hi = nv - 1;  // last source with off <= k
         while (lo < hi) {
@@ -1413,6 +1468,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
                  sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]), sm.em.cost[w][lo], (uint32_t)(base + lo),
                  FSA ? (uint32_t)src[base + lo].state : 0u);
       }
+#endif
       __syncwarp();
     }
     __syncthreads();
