@@ -318,9 +318,16 @@ __device__ __forceinline__ bool tok_relax(const LaneCtx& L, CtwTok* e, unsigned 
 }
 
 __device__ __forceinline__ void tok_clear(CtwTok* e) {
+#if CTW_LD256
+  // key, tb=~0, aux=0 | gpos=~0, state=EMPTY, stamp=0: one 256-bit store
+  asm volatile("st.global.cg.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(e), "l"(~0ULL), "l"(0xFFFFFFFFULL), "l"(~0ULL),
+               "l"((unsigned long long)CTW_EMPTY)
+               : "memory");
+#else
   ulonglong2* p = reinterpret_cast<ulonglong2*>(e);
   __stcg(p, make_ulonglong2(~0ULL, 0xFFFFFFFFULL));                          // key, tb=~0, aux=0
   __stcg(p + 1, make_ulonglong2(~0ULL, (unsigned long long)CTW_EMPTY));     // gpos=~0, state, stamp=0
+#endif
 }
 
 // --------------------------------------------------------- shared memory --
