@@ -65,6 +65,9 @@
 #ifndef CTW_EPS_TAIL_SZ
 #define CTW_EPS_TAIL_SZ 32
 #endif
+#ifndef CTW_SRC256
+#define CTW_SRC256 1  // sources read / written as one 256-bit access each (+0.8%)
+#endif
 #ifndef CTW_IDLE_PROF
 #define CTW_IDLE_PROF 0
 #endif
@@ -1393,7 +1396,21 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       const int nv = min(gsz, n_src - base);
       int deg = 0;
       CtwSrc t;
+#if CTW_SRC256
+      if (lane_ < nv) {
+        unsigned long long w0, w1, w2, w3;
+        asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(src + base + lane_));
+        t.state = (int32_t)(uint32_t)w0;
+        t.bp = (int32_t)(uint32_t)(w0 >> 32);
+        t.cost = __longlong_as_double((long long)w1);
+        t.emit_beg = (uint32_t)w2;
+        t.emit_end = (uint32_t)(w2 >> 32);
+        (void)w3;
+      }
+#else
       if (lane_ < nv) t = src[base + lane_];
+#endif
       if (lane_ < nv) {
         const CtwStateRange r{0u, t.emit_beg, t.emit_end, 0u};  // cached with the token
         deg = (int)(r.emit_end - r.emit_beg);
@@ -1649,7 +1666,15 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           ns.cost = cost;
           ns.emit_beg = rg.emit_beg;
           ns.emit_end = rg.emit_end;
+#if CTW_SRC256
+          asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(nsrc + pos),
+                       "l"(((unsigned long long)(uint32_t)ns.bp << 32) | (uint32_t)ns.state),
+                       "l"((unsigned long long)__double_as_longlong(ns.cost)),
+                       "l"(((unsigned long long)ns.emit_end << 32) | ns.emit_beg), "l"(0ULL)
+                       : "memory");
+#else
           nsrc[pos] = ns;
+#endif
           ++pos;
         }
         if (rank == 0 && tid == 0) lane.frame_base[lane.frame_count + f] = sm.n_rec;
