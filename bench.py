@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--lattice", type=int, default=64,
                     help="utterances in the lattice leg (decode + lattice + 10-best; 0 = skip)")
     ap.add_argument("--lattice-beam", type=float, default=6.0)
+    ap.add_argument("--search", default="fast", choices=["fast", "exact"],
+                    help="lane search mode of the timed decode (decoder.SEARCH_MODES)")
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"],
                     help="c2: 3-gram TLG (default, the headline); c3: 4-gram ~50M-arc TLG; "
                          "c5: c2 + a 100-word boost table per utterance")
@@ -451,7 +453,7 @@ def main():
     host_np = host.numpy()
     dev_ll = host.to(f"cuda:{dev}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
-    pool = fg.device_graph(dev).pool(cfg, fg.num_states)
+    pool = fg.device_graph(dev).pool(cfg, fg.num_states, args.search)
 
     def barrier():
         if world > 1:
@@ -460,7 +462,7 @@ def main():
             dist.barrier()
 
     for _ in range(args.warmup):
-        out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts)
+        out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts, search=args.search)
     assert all(isinstance(h, Hypothesis) for h in out), [h for h in out if not isinstance(h, Hypothesis)][:2]
 
     # ---- value: inputs resident in HBM ----
@@ -473,7 +475,7 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record()
-            out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts)
+            out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts, search=args.search)
             ev[i][1].record()
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -499,7 +501,7 @@ def main():
     for i in range(args.steps):
         flush.zero_()
         ev2[i][0].record()
-        out_e2e = decode_batch(fg, cfg, host_np, device=dev, boost=boosts)
+        out_e2e = decode_batch(fg, cfg, host_np, device=dev, boost=boosts, search=args.search)
         ev2[i][1].record()
     torch.cuda.synchronize()
     e2e_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps

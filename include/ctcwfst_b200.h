@@ -132,6 +132,19 @@ void ctw_lanes_destroy(ctw_lanes* l);
 /* Number of lanes; grows the set to at least n (new lanes start unseeded). */
 int ctw_lanes_reserve(ctw_lanes* l, int32_t n);
 
+/* Search mode of the lane set (default 0):
+ *   0 exact -- the reference's kernel reproduced record for record
+ *     (_kernel.pyx:233-444: Gauss-Seidel epsilon order, every slot, every
+ *     prev pointer), the mode behind ctw_lane_export / history parity;
+ *   1 fast  -- words-exact search for throughput: best-path words identical,
+ *     costs the exact min over paths (within the reference's relax_eps stop
+ *     rule), out-of-beam candidates never inserted, 16 B token entries.
+ * A launch falls back to exact when a lane does not meet the fast mode's
+ * preconditions (negative epsilon increments, tight max_ne_iters caps).
+ * ctw_lanes_search_info: out3 = {mode, fast launches, decode launches}. */
+int ctw_lanes_set_search(ctw_lanes* l, int32_t mode);
+int ctw_lanes_search_info(ctw_lanes* l, int64_t* out3);
+
 /* Seed lanes: fresh channel = start token + epsilon closure, zero frames, empty
  * history (decoder.py:173-229). boosts[i] is a host f64 vector of
  * boost_lens[i] >= max_olabel + 1 entries or NULL (no boost: bit-identical to

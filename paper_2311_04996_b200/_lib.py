@@ -80,6 +80,8 @@ _SIGS = {
     "ctw_lanes_reset_stats": (I32, [P]),
     "ctw_lanes_profile": (I32, [P, P]),
     "ctw_lanes_host_timing": (I32, [P, P]),
+    "ctw_lanes_set_search": (I32, [P, I32]),
+    "ctw_lanes_search_info": (I32, [P, P]),
     "ctw_lanes_stream": (P, [P]),
     "ctw_lane_lattice": (I32, [P, P, I32, P, I32, I32, P, I32, F64, P]),
     "ctw_lattice_free": (None, [C.POINTER(CtwLattice)]),

@@ -34,7 +34,7 @@
 
 extern "C" int ctw_launch_decode(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                  const double*, const void*, int, int, const long long*, const int*,
-                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, int, cudaStream_t);
+                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, int, int, int, cudaStream_t);
 extern "C" int ctw_launch_seed(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                const double*, const int*, int, int, const CtwDecodeCfg*, CtwLaneOut*,
                                cudaStream_t);
@@ -110,6 +110,10 @@ struct ctw_graph {
   double w_min_emit = 0.0;  // min(0, smallest emitting arc weight): lattice source bound
   bool eps_olabel = false; // some epsilon arc carries an output label (boost applies)
   int64_t S = 0, A = 0, start = 0, max_il = 0, max_ol = 0;
+  // fast search mode (ctw_kernels.cu): winner words hold an emitting-arc
+  // offset in `ebits` bits and an epsilon-arc offset above the table index
+  int64_t max_emit_deg = 0, max_eps_deg = 0;
+  uint32_t ebits = 0;
   CtwStateRange* ranges = nullptr;
   CtwArc* arcs = nullptr;
   int32_t* olabel = nullptr;
@@ -186,6 +190,8 @@ struct ctw_lanes {
   int64_t h_reruns = 0, h_calls = 0;
   int64_t h_grow[4] = {0, 0, 0, 0};  // lanes re-run for: table, history, pool, sources
   int64_t prof[CTW_NPROF] = {0};
+  int32_t search = 0;         // 0 exact (reference histories), 1 fast (words-exact)
+  int64_t fast_launches = 0;  // decode launches that ran the fast mode
   uint32_t tlog2_hint = 0;  // largest token-table size any lane of this set grew to
   std::mutex mu;
 };
@@ -415,16 +421,43 @@ int reserve_lanes(ctw_lanes* l, int n) {
 }
 
 // Early beam pruning is exact when epsilon increments cannot be negative
-// (see CtwLane::prune_ok); tight user caps on max_ne_iters keep the full
-// Gauss-Seidel pass accounting.
-int32_t prune_flag(const ctw_lanes* l, const double* boost, int64_t len) {
+// (see CtwLane::prune_ok) and the cap on Gauss-Seidel passes cannot bind: with
+// non-negative epsilon weights a closure over K distinct token keys converges
+// in at most K passes (Bellman-Ford: shortest epsilon paths have < K arcs) plus
+// one quiet pass, so max_ne_iters >= K + 1 never triggers ERR_EPS_ITERS -- the
+// default cap 2 x num_states (decoder.py:164-168) always qualifies. Below that
+// (a tight user cap) the pass accounting must include out-of-beam slots.
+// `keys` = token-key space (states, x automaton states with a phrase FSA).
+int64_t prune_cap_needed(const ctw_lanes* l, int64_t keys) {
+  return std::min<int64_t>((int64_t)1 << 16, keys + 1);
+}
+
+int32_t prune_flag(const ctw_lanes* l, const double* boost, int64_t len, int64_t keys) {
   const ctw_graph* g = l->g;
-  if (!g->eps_nonneg || l->cfg.max_ne_iters < (1 << 16)) return 0;
-  if (getenv("CTW_NOPRUNE")) return 0;  // diagnostics: every candidate valued (full closure)
+  if (!g->eps_nonneg || l->cfg.max_ne_iters < prune_cap_needed(l, keys)) return 0;
   if (boost && g->eps_olabel)
     for (int64_t i = 0; i < len; ++i)
       if (!(boost[i] >= 0.0)) return 0;
   return 1;
+}
+
+int64_t key_space(const ctw_lanes* l, const CtwLane& L) {
+  return L.fsa_next ? l->g->S * (int64_t)std::max(1, L.fsa_states) : l->g->S;
+}
+
+// Fast search mode for a launch over `ids`: requested, and every lane fits its
+// preconditions -- early pruning exact (prune_ok), winner words wide enough
+// for the source capacity and the epsilon out-degree at the lane's table size.
+bool fast_launch(const ctw_lanes* l, const int* ids, int n) {
+  const ctw_graph* g = l->g;
+  if (l->search != 1 || g->ebits > 24) return false;
+  for (int k = 0; k < n; ++k) {
+    const CtwLane& L = l->h[ids[k]];
+    if (!L.prune_ok) return false;
+    if ((uint64_t)L.scap >= (1ull << (31 - g->ebits))) return false;
+    if ((uint64_t)g->max_eps_deg > (1ull << (31 - L.tlog2))) return false;
+  }
+  return true;
 }
 
 void update_from_out(CtwLane& L, const CtwLaneOut& o) {
@@ -540,10 +573,12 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
   if (start < 0 || start >= num_states) return fail(-1, "start state out of range");
   if (off[0] != 0 || off[num_states] != num_arcs) return fail(-1, "off[] does not span the arcs");
   std::vector<CtwStateRange> r((size_t)num_states);
-  int64_t max_il = 0, max_ol = 0;
+  int64_t max_il = 0, max_ol = 0, max_emit_deg = 0, max_eps_deg = 0;
   for (int64_t s = 0; s < num_states; ++s) {
     if (off[s + 1] < off[s] || eps_end[s] < off[s] || eps_end[s] > off[s + 1])
       return fail(-1, "inconsistent CSR offsets");
+    max_eps_deg = std::max<int64_t>(max_eps_deg, eps_end[s] - off[s]);
+    max_emit_deg = std::max<int64_t>(max_emit_deg, off[s + 1] - eps_end[s]);
     r[s] = CtwStateRange{(uint32_t)off[s], (uint32_t)eps_end[s], (uint32_t)off[s + 1], 0u};
   }
   std::vector<CtwArc> arcs((size_t)std::max<int64_t>(num_arcs, 1));
@@ -577,6 +612,9 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
   g->eps_nonneg = eps_nonneg;
   g->eps_olabel = eps_olabel;
   g->w_min_emit = w_min_emit;
+  g->max_emit_deg = max_emit_deg;
+  g->max_eps_deg = max_eps_deg;
+  g->ebits = ceil_log2((uint64_t)max_emit_deg + 1);
   auto bail = [&](int code) {
     ctw_graph_destroy(g);
     return code;
@@ -797,7 +835,8 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
       L.boost = nullptr;
       L.boost_len = 0;
     }
-    L.prune_ok = prune_flag(l, b, b ? boost_lens[i] : 0) && !(L.fsa_next && l->g->eps_olabel && l->fsa_min[lane] < 0);
+    L.prune_ok = prune_flag(l, b, b ? boost_lens[i] : 0, key_space(l, L)) &&
+                 !(L.fsa_next && l->g->eps_olabel && l->fsa_min[lane] < 0);
     L.n_src = 0;
     L.src_buf = 0;
     L.frame_count = 0;
@@ -857,7 +896,8 @@ int ctw_lane_set_boost(ctw_lanes* l, int32_t lane, const double* boost, int64_t 
     L.boost = nullptr;
     L.boost_len = 0;
   }
-  L.prune_ok = prune_flag(l, boost, boost_len) && !(L.fsa_next && l->g->eps_olabel && l->fsa_min[lane] < 0);
+  L.prune_ok = prune_flag(l, boost, boost_len, key_space(l, L)) &&
+               !(L.fsa_next && l->g->eps_olabel && l->fsa_min[lane] < 0);
   if (int r = sync_lane(l, lane)) return r;
   CUDA_TRY(cudaStreamSynchronize(l->stream));
   return 0;
@@ -968,8 +1008,11 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     CUDA_TRY(cudaEventRecord(l->ev0, l->stream));
     int any_fsa = 0;
     for (int k = 0; k < m; ++k) any_fsa |= l->h[todo[k]].fsa_next != nullptr;
+    const bool fast = fast_launch(l, l->h_ids, m);
+    l->fast_launches += fast;
     if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
-                          l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, l->stream))
+                          l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, fast ? 1 : 0, (int)g->ebits,
+                          l->stream))
       return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
     CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
     l->launches++;
@@ -1022,6 +1065,21 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     todo.swap(again);
     l->h_post += secs(tw, clk::now());
   }
+  return 0;
+}
+
+int ctw_lanes_set_search(ctw_lanes* l, int32_t mode) {
+  if (mode != 0 && mode != 1) return fail(-1, "search mode must be 0 (exact) or 1 (fast)");
+  std::lock_guard<std::mutex> lk(l->mu);
+  l->search = mode;
+  return 0;
+}
+
+int ctw_lanes_search_info(ctw_lanes* l, int64_t* out3) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  out3[0] = l->search;
+  out3[1] = l->fast_launches;
+  out3[2] = l->decode_launches;
   return 0;
 }
 
@@ -1418,6 +1476,7 @@ int ctw_lanes_stats(ctw_lanes* l, int64_t* launches, int64_t* decode_launches, d
 int ctw_lanes_reset_stats(ctw_lanes* l) {
   std::lock_guard<std::mutex> lk(l->mu);
   l->launches = l->decode_launches = l->arcs = l->srcs = l->frames = l->max_slots = 0;
+  l->fast_launches = 0;
   l->h_stage = l->h_presize = l->h_wait = l->h_post = 0;
   l->h_reruns = l->h_calls = 0;
   for (auto& x : l->h_grow) x = 0;
@@ -1548,7 +1607,7 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
     L.pend_valid = any_pend ? 1 : 0;
     L.boost = dboost;
     L.boost_len = (int32_t)boost_len;
-    L.prune_ok = prune_flag(l, boost, boost_len);
+    L.prune_ok = prune_flag(l, boost, boost_len, key_space(l, L));
     l->seeded[0] = 1;
     return sync_lane(l, 0);
   };

@@ -163,7 +163,116 @@ struct LaneCtx {
   const double* fcost;
   int32_t fwidth;
   uint32_t sbits, smask;
+  // fast search mode (FastEnt table view of the same allocation, see below)
+  ulonglong2* V;
+  uint32_t tlog2, ebits;
 };
+
+// ------------------------------------------------------ fast search mode --
+//
+// Words-exact search (north star: best-path words bit-exact, cost within
+// 1e-4) without the Gauss-Seidel slot-position machinery of the exact mode:
+//  * a 16 B token entry {f64 cost key, u32 state, u32 winner} -- two entries
+//    per 32 B sector, probed and relaxed with one 128-bit access each
+//    (the north star's "packed atomicMin": the cost key and its backpointer
+//    change together in one atom.cas.b128);
+//  * candidates above the running cutoff (running min + beam) are never
+//    inserted (exact for the final beam: the frame minimum only decreases and
+//    epsilon increments are >= 0 -- CtwLane::prune_ok is required);
+//  * the epsilon closure is a plain label-correcting fixpoint over the
+//    in-beam states (full propagation: costs are the exact min over paths,
+//    <= the reference's relax_eps-stopped values by at most ~relax_eps);
+//  * exact-cost ties: emitting candidates by the lowest arc index (the
+//    reference's first writer, _kernel.pyx:256-285), an emitting winner stays
+//    against epsilon candidates (_kernel.pyx:332), epsilon candidates among
+//    themselves by the lowest arc index (deterministic; the reference orders
+//    them by Gauss-Seidel event time).
+// Winner word: emitting = src_idx << ebits | arc offset in the source's
+// emitting range; epsilon = EPS | offset << tlog2 | predecessor table index.
+// The table allocation is the exact mode's (32 B x tcap); the fast view uses
+// its first 16 B x tcap. A clean fast entry {~0, EMPTY, 0} is bytewise the
+// clean exact pattern (every even 64-bit word ~0, every odd one 0xFFFFFFFF),
+// so both views stay valid between frames and a lane set may switch modes.
+#define CTW_FEPS 0x80000000u
+
+__device__ __forceinline__ uint32_t fwin_emit(uint32_t src_idx, uint32_t off, uint32_t ebits) {
+  return (src_idx << ebits) | off;
+}
+
+// Find-or-insert `d` in the fast table; *v gets a historical snapshot of the
+// entry (only ever used as a CAS expected value / lower bound).
+__device__ __forceinline__ uint32_t ftok_locate(const LaneCtx& L, uint32_t d, ulonglong2* v, bool& is_new) {
+  uint32_t h = tok_hash(d, L.shift);
+  for (uint32_t probe = 0; probe <= L.mask; ++probe) {
+    const ulonglong2 val = __ldcg(&L.V[h]);
+    const uint32_t k = (uint32_t)val.y;
+    if (k == d) {
+      *v = val;
+      return h;
+    }
+    if (k == CTW_EMPTY) {
+      const uint32_t old = atomicCAS(reinterpret_cast<uint32_t*>(&L.V[h]) + 2, CTW_EMPTY, d);
+      if (old == CTW_EMPTY || old == d) {
+        is_new = old == CTW_EMPTY;
+        *v = make_ulonglong2(~0ULL, (unsigned long long)d);  // the claimed entry's first value
+        return h;
+      }
+    }
+    h = (h + 1) & L.mask;
+  }
+  return CTW_EMPTY;
+}
+
+// Arc index behind a fast winner word (exact-tie resolution, walks).
+__device__ __forceinline__ uint32_t fwin_arc(const LaneCtx& L, const GraphDev& g, const CtwSrc* src, uint32_t w) {
+  // (sources are written by this kernel: coherent loads, not the read-only path)
+  if (!(w & CTW_FEPS)) return __ldcg(&src[w >> L.ebits].emit_beg) + (w & ((1u << L.ebits) - 1u));
+  const uint32_t pred = w & L.mask;
+  const uint32_t st = (uint32_t)__ldcg(&L.V[pred]).y & L.smask;
+  return __ldg(&g.ranges[st].eps_beg) + ((w & ~CTW_FEPS) >> L.tlog2);
+}
+
+// Relax fast entry e with candidate (key, winner w over arc `arc`).
+__device__ __forceinline__ bool ftok_relax(const LaneCtx& L, const GraphDev& g, const CtwSrc* src, ulonglong2* e,
+                                           unsigned long long key, uint32_t w, uint32_t arc, ulonglong2 seen,
+                                           unsigned long long* old_key) {
+  if (key > seen.x) return false;
+  unsigned long long clo = seen.x, chi = seen.y;
+  if (key == clo) snap128(e, clo, chi);
+  for (;;) {
+    if (key > clo) return false;
+    if (key == clo) {
+      const uint32_t cw = (uint32_t)(chi >> 32);
+      if (!(w & CTW_FEPS)) {
+        if (!(cw & CTW_FEPS) && arc >= fwin_arc(L, g, src, cw)) return false;
+      } else {
+        if (!(cw & CTW_FEPS)) return false;  // an equal-cost emitting winner stays
+        if (arc >= fwin_arc(L, g, src, cw)) return false;
+      }
+    }
+    unsigned long long olo, ohi;
+    const unsigned long long nhi = (chi & 0xFFFFFFFFULL) | ((unsigned long long)w << 32);
+    cas128(e, clo, chi, key, nhi, olo, ohi);
+    if (olo == clo && ohi == chi) {
+      *old_key = clo;
+      return true;
+    }
+    clo = olo;
+    chi = ohi;
+  }
+}
+
+__device__ __forceinline__ void ftok_clear(ulonglong2* e) {
+  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(e), "l"(~0ULL), "l"(0xFFFFFFFFULL) : "memory");
+}
+
+// The (key, winner) value of table entry h in either view: exact mode keeps
+// (key, tb | aux << 32) in the first 16 B of its 32 B entry; fast mode's 16 B
+// entry is (key, state | winner << 32).
+template <bool FAST>
+__device__ __forceinline__ ulonglong2* tval(const LaneCtx& L, uint32_t h) {
+  return FAST ? L.V + h : reinterpret_cast<ulonglong2*>(&L.T[h]);
+}
 
 // Destination key and boost of an arc with output label ol leaving the token
 // with key `key` (reference order: the boost is added after the arc weight,
@@ -799,27 +908,52 @@ struct WalkEnd {
   bool ok;
 };
 
-// v0 = the survivor's own (key, tb|aux), already gathered.
+// One hop back along a winner chain from the value v: 0 = seed (no arc),
+// 1 = emitting arc `arc` from source `idx` (the chain ends), 2 = epsilon arc
+// `arc` (v becomes the predecessor's value).
+template <bool FAST>
+__device__ __forceinline__ int hop_step(const LaneCtx& L, const GraphDev& g, const CtwSrc* src, ulonglong2& v,
+                                        uint32_t& arc, uint32_t& idx) {
+  if (FAST) {
+    const uint32_t win = (uint32_t)(v.y >> 32);
+    if (!(win & CTW_FEPS)) {
+      idx = win >> L.ebits;
+      arc = __ldcg(&src[idx].emit_beg) + (win & ((1u << L.ebits) - 1u));
+      return 1;
+    }
+    v = __ldcg(&L.V[win & L.mask]);
+    arc = __ldg(&g.ranges[(uint32_t)v.y & L.smask].eps_beg) + ((win & ~CTW_FEPS) >> L.tlog2);
+    return 2;
+  }
+  const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
+  if (tb == CTW_SEED_TB) return 0;
+  arc = tb & ~CTW_EPS_BIT;
+  if (!(tb & CTW_EPS_BIT)) {
+    idx = aux;
+    return 1;
+  }
+  v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[aux & CTW_PRED_MASK]));
+  return 2;
+}
+
+// v0 = the survivor's own (key, winner), already gathered.
+template <bool FAST>
 __device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, ulonglong2 v0, const CtwSrc* src,
                                         const int32_t* pend, int hop_cap) {
   WalkEnd w{-1, 0, 0, 0, true};
   ulonglong2 v = v0;
   for (int hop = 0; hop < hop_cap; ++hop) {
-    if (hop) {
-      // epsilon winner: continue at the predecessor
-      v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[(uint32_t)(v.y >> 32) & CTW_PRED_MASK]));
-    }
-    const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
-    if (tb == CTW_SEED_TB) return w;
-    const uint32_t a = tb & ~CTW_EPS_BIT;
+    uint32_t a = 0, idx = 0;
+    const int k = hop_step<FAST>(L, g, src, v, a, idx);
+    if (k == 0) return w;
     const int32_t ol = g.olabel[a];
     if (ol != 0) {
       ++w.n;
       w.last = ol;
     }
-    if (!(tb & CTW_EPS_BIT)) {
-      w.bp = src[aux].bp;
-      w.pend = pend ? pend[aux] : 0;
+    if (k == 1) {
+      w.bp = src[idx].bp;
+      w.pend = pend ? pend[idx] : 0;
       return w;
     }
   }
@@ -833,7 +967,9 @@ __device__ __forceinline__ int code_len(const int32_t* pool, int32_t code) {
 
 // Olabel code of a record: 0 none, >0 one label, <0 pool segment
 // -(offset+1) holding [n, l1..ln].
-__device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, uint32_t h, const WalkEnd& w) {
+template <bool FAST>
+__device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, const CtwSrc* src, ulonglong2 v0,
+                               const WalkEnd& w) {
   const int np = code_len(L.pool, w.pend);
   const int n = np + w.n;
   if (n == 0) return 0;
@@ -849,15 +985,14 @@ __device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, ui
   else
     for (int i = 0; i < np; ++i) seg[1 + i] = L.pool[-w.pend - 1 + 1 + i];
   int pos = n;  // walk again, writing newest-first labels from the back
+  ulonglong2 v = v0;
   for (int hop = 0; hop < 1 << 20; ++hop) {
-    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h]));
-    const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
-    if (tb == CTW_SEED_TB) break;
-    const uint32_t a = tb & ~CTW_EPS_BIT;
+    uint32_t a = 0, idx = 0;
+    const int k = hop_step<FAST>(L, g, src, v, a, idx);
+    if (k == 0) break;
     const int32_t ol = g.olabel[a];
     if (ol != 0) seg[pos--] = ol;
-    if (!(tb & CTW_EPS_BIT)) break;
-    h = aux & CTW_PRED_MASK;
+    if (k == 1) break;
   }
   return -(off + 1);
 }
@@ -979,6 +1114,7 @@ struct ChunkArgs {
   const int* lane_ids;      // per batch entry
   int width;
   int is_f64;
+  int ebits;  // fast mode: bits of the emitting-arc offset in a winner word
   CtwDecodeCfg cfg;
 };
 
@@ -1006,6 +1142,9 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int n
   L.fwidth = lane.fsa_width;
   L.sbits = lane.sbits;
   L.smask = lane.smask;
+  L.V = reinterpret_cast<ulonglong2*>(lane.table);
+  L.tlog2 = lane.tlog2;
+  L.ebits = 0;
   return L;
 }
 
@@ -1037,6 +1176,7 @@ __device__ __forceinline__ int cost_bin(unsigned long long key, double min_cost,
 // ib[j] = (table index, state) for j < in-beam count (cluster-wide list, warp-
 // aggregated appends); the select and record stages then sweep only those.
 // Without it (seeding) sv[i] holds slot i's value for every slot.
+template <bool FAST>
 __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* sv, uint2* ib, int n_all,
                           long long max_ne_iters, unsigned long long cut_key, double min_cost, double bin_scale,
                           bool hist) {
@@ -1060,7 +1200,7 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
       const int i = i0 + u * L.swstride;
-      if (i < n_all) v[u] = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[h[u].x]));
+      if (i < n_all) v[u] = __ldcg(tval<FAST>(L, h[u].x));
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u) {
@@ -1076,7 +1216,7 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
           ib[j] = h[u];
         }
       }
-      if ((uint32_t)v[u].y & CTW_EPS_BIT) mpd = max(mpd, (int)((uint32_t)(v[u].y >> 32) >> CTW_PRED_BITS));
+      if (!FAST && ((uint32_t)v[u].y & CTW_EPS_BIT)) mpd = max(mpd, (int)((uint32_t)(v[u].y >> 32) >> CTW_PRED_BITS));
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -1108,6 +1248,7 @@ __device__ int count_pass(Smem& sm, const LaneCtx& L, FrameCtr* fc, ulonglong2* 
 
 // Reset this rank's share of the frame's table entries; slot loads batched
 // ahead of the stores.
+template <bool FAST>
 __device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_all) {
   for (int i0 = L.sw0 + threadIdx.x; i0 < n_all; i0 += CTW_UNR * L.swstride) {
     uint32_t h[CTW_UNR];
@@ -1118,7 +1259,10 @@ __device__ __forceinline__ void reset_slots(const LaneCtx& L, int n_all) {
     }
 #pragma unroll
     for (int u = 0; u < CTW_UNR; ++u)
-      if (h[u] != CTW_EMPTY) tok_clear(&L.T[h[u]]);
+      if (h[u] != CTW_EMPTY) {
+        if (FAST) ftok_clear(&L.V[h[u]]);
+        else tok_clear(&L.T[h[u]]);
+      }
   }
 }
 
@@ -1230,12 +1374,13 @@ __device__ void select_threshold(Smem& sm, const LaneCtx& L, FrameCtr* fc, const
 
 // Relax one emitting arc: ((c + (-scale * ll)) + w) (+ boost), then
 // find-or-insert the destination and install the candidate if it wins
-// (_kernel.pyx:243-287).
-template <bool FSA>
+// (_kernel.pyx:243-287). `off` = the arc's offset in its source's emitting
+// range (fast mode's winner word).
+template <bool FSA, bool FAST>
 __device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
                                                 const double* nll_s, bool smem_ll, long long row0, double neg_scale,
                                                 const double* boost, uint32_t arc_i, double cost, uint32_t src_idx,
-                                                uint32_t src_key, const CtwArc& arc) {
+                                                uint32_t src_key, const CtwArc& arc, const CtwSrc* src, uint32_t off) {
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
   double ac;
   if (smem_ll) ac = nll_s[arc.ilabel - 1];
@@ -1252,6 +1397,22 @@ __device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, cons
     if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
   }
   if (!(nc < INF)) return;
+  if (FAST) {
+    // never inserted above the running cutoff (cannot make the final beam)
+    if (nc > running_cut(sm, a.cfg.beam)) return;
+    bool is_new = false;
+    ulonglong2 seen;
+    const uint32_t d = ftok_locate(L, dkey, &seen, is_new);
+    if (d == CTW_EMPTY) {
+      atomicMax(&sm.status_l, CTW_GROW_TABLE);
+      return;
+    }
+    if (is_new) slot_append(sm, L, d, dkey);
+    unsigned long long oldk;
+    const unsigned long long nk = d2key(nc);
+    if (ftok_relax(L, g, src, &L.V[d], nk, fwin_emit(src_idx, off, L.ebits), arc_i, seen, &oldk)) track_min(sm, nk);
+    return;
+  }
   bool is_new = false;
   ulonglong2 seen;
   const uint32_t d = tok_locate(L, dkey, &seen, is_new);
@@ -1270,18 +1431,144 @@ __device__ __forceinline__ void emit_arc_loaded(Smem& sm, const LaneCtx& L, cons
   if (tok_relax_from(L, ed, nk, arc_i, src_idx, 0ULL, seen, &oldk)) track_min(sm, nk);
 }
 
-template <bool FSA>
+template <bool FSA, bool FAST>
 __device__ __forceinline__ void emit_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const ChunkArgs& a,
                                          const double* nll_s, bool smem_ll, long long row0, double neg_scale,
                                          const double* boost, uint32_t arc_i, double cost, uint32_t src_idx,
-                                         uint32_t src_key) {
+                                         uint32_t src_key, const CtwSrc* src, uint32_t off) {
   const CtwArc arc = ld_arc(g.arcs, arc_i);
-  emit_arc_loaded<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, arc_i, cost, src_idx, src_key, arc);
+  emit_arc_loaded<FSA, FAST>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, arc_i, cost, src_idx, src_key, arc,
+                             src, off);
+}
+
+// Fast mode: relax one epsilon arc a (offset o) of the frontier item lo of
+// warp w; queue the destination for the next pass when it improved.
+template <bool FSA>
+__device__ __forceinline__ void feps_arc(Smem& sm, const LaneCtx& L, const GraphDev& g, const double* boost, int w,
+                                         int lo, uint32_t o, uint32_t a, const CtwArc& arc, double beam, uint2* out,
+                                         int* ctr, uint32_t fcap) {
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  double nc = __dadd_rn(sm.ep.cost[w][lo], arc.weight);
+  uint32_t dkey = (uint32_t)arc.nextstate;
+  if (FSA) dkey = arc_dest<FSA>(L, boost, (uint32_t)sm.ep.gu[w][lo], g.olabel[a], dkey, nc);
+  else if (boost) {
+    const int32_t ol = g.olabel[a];
+    if (ol != 0) nc = __dadd_rn(nc, boost[ol]);
+  }
+  if (!(nc < INF)) return;
+  if (nc > running_cut(sm, beam)) return;
+  bool is_new = false;
+  ulonglong2 seen;
+  const uint32_t d = ftok_locate(L, dkey, &seen, is_new);
+  if (d == CTW_EMPTY) {
+    atomicMax(&sm.status_l, CTW_GROW_TABLE);
+    return;
+  }
+  if (is_new) slot_append(sm, L, d, dkey);
+  unsigned long long oldk;
+  const unsigned long long nk = d2key(nc);
+  const uint32_t win = CTW_FEPS | (o << L.tlog2) | sm.ep.aux[w][lo];
+  if (!ftok_relax(L, g, nullptr, &L.V[d], nk, win, a, seen, &oldk)) return;
+  track_min(sm, nk);
+  const int p = agg_alloc(ctr, nullptr);
+  if ((uint32_t)p < fcap) out[p] = make_uint2(d, dkey);
+  else atomicMax(&sm.status_l, CTW_GROW_TABLE);
+}
+
+// Fast mode epsilon closure: label-correcting passes over the states that
+// improved in the previous pass (pass 1: every slot of the frame), skipping
+// predecessors and candidates above the running cutoff; ends when a pass
+// improves nothing. Two frontier sets of 2 x seg items (pass parity); work is
+// handed out cluster-wide in 32-item chunks. Returns CTW_OK or
+// CTW_ERR_EPS_ITERS (divergence).
+template <bool FSA>
+__device__ CTW_EPS_INLINE int eps_fast(Smem& sm, const LaneCtx& L, const GraphDev& g, const double* boost,
+                                       double beam, long long pass_cap) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int tid = threadIdx.x;
+  const int R = L.nranks, rank = L.rank;
+  Smem* G = L.G;
+  const uint32_t fcap = 2 * L.seg;
+  const int lane = tid & 31, w = tid >> 5;
+  for (long long pass = 1;; ++pass) {
+    const int q = (int)(pass & 1);
+    uint2* out = L.front + (size_t)((pass - 1) & 1) * fcap;
+    int* ctr_out = G->pcnt[pass % 3];
+    if (tid == 0) {
+      if (pass == 1) {
+        int tot = 0;
+        for (int k = 0; k < R; ++k) tot += cl.map_shared_rank(&sm, k)->snap_slots;  // once per frame
+        sm.in0 = L.slots;
+        sm.n_cur = min(tot, (int)L.seg);
+      } else {
+        sm.in0 = L.front + (size_t)((pass - 2) & 1) * fcap;
+        sm.n_cur = min(*((volatile const int*)&G->pcnt[(pass - 1) % 3][0]), (int)fcap);
+      }
+      if (rank == 0) {
+        sm.pw[q ^ 1] = 0;                // the next pass's chunk counter
+        sm.pcnt[(pass + 1) % 3][0] = 0;  // written in pass + 1; last read at the start of pass - 1
+      }
+      sm.passes = (int)pass;
+    }
+    __syncthreads();
+    const int n_cur = sm.n_cur;
+    if (n_cur == 0) return CTW_OK;  // (the same count in every rank)
+    if (pass > pass_cap) return CTW_ERR_EPS_ITERS;
+    const uint2* in = sm.in0;
+    for (;;) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&G->pw[q], 32);
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (base >= n_cur) break;
+      const int nv = min(32, n_cur - base);
+      if (lane == 0) atomicAdd(&sm.eps_items, nv);
+      int deg = 0;
+      if (lane < nv) {
+        const uint2 it = in[base + lane];
+        // the range and the entry are independent loads: issue them together
+        const CtwStateRange r = ld_range(g.ranges, FSA ? (it.y & L.smask) : it.y);
+        const ulonglong2 v = __ldcg(&L.V[it.x]);
+        const double c = key2d(v.x);
+        if (!(c > running_cut(sm, beam))) deg = (int)(r.emit_beg - r.eps_beg);
+        sm.ep.cost[w][lane] = c;
+        sm.ep.beg[w][lane] = r.eps_beg;
+        sm.ep.aux[w][lane] = it.x;
+        sm.ep.gu[w][lane] = it.y;
+      }
+      int incl = deg;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      sm.ep.off[w][lane] = incl - deg;
+      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (lane == 0) atomicAdd(&sm.eps_arcs, total);
+      __syncwarp();
+      for (int k = lane; k < total; k += 32) {
+        int lo = 0, hi = nv - 1;  // last item with off <= k
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.ep.off[w][mid] <= k) lo = mid;
+          else hi = mid - 1;
+        }
+        const uint32_t o = (uint32_t)(k - sm.ep.off[w][lo]);
+        const uint32_t a = sm.ep.beg[w][lo] + o;
+        const CtwArc arc = ld_arc(g.arcs, a);
+        feps_arc<FSA>(sm, L, g, boost, w, lo, o, a, arc, beam, out, ctr_out, fcap);
+      }
+      __syncwarp();
+    }
+    // the barrier ending the pass (also merges the ranks' running minima)
+    const int vst = csync(sm);
+    if (vst >= CTW_GROW_TABLE) return CTW_OK;  // caller handles the grow request
+  }
 }
 
 // FSA: some lane of the launch has a phrase automaton (token keys carry its
-// state); the plain instantiation keeps the hot path free of it.
-template <bool FSA>
+// state); the plain instantiation keeps the hot path free of it. FAST: the
+// words-exact search mode (see "fast search mode" above).
+template <bool FSA, bool FAST>
 __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lanes, const __grid_constant__ GraphDev g,
                                                                 const __grid_constant__ ChunkArgs a, CtwLaneOut* out) {
   extern __shared__ double nll_s[];
@@ -1294,6 +1581,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   CtwLane& lane = lanes[a.lane_ids[b]];
   LaneCtx L = lane_ctx(lane, rank, R, G);
   L.tie_ctr = &sm.eps_ties;
+  L.ebits = (uint32_t)a.ebits;
   const int F = a.nframes[b];
   const double* boost = lane.boost;
   const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
@@ -1471,8 +1759,9 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           ain = sm.em.beg[w][lon] + (uint32_t)(kn - sm.em.off[w][lon]);
           arcn = ld_arc(g.arcs, ain);
         }
-        emit_arc_loaded<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, ai, sm.em.cost[w][lo],
-                             (uint32_t)(base + lo), FSA ? (uint32_t)src[base + lo].state : 0u, arc);
+        emit_arc_loaded<FSA, FAST>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost, ai, sm.em.cost[w][lo],
+                                   (uint32_t)(base + lo), FSA ? (uint32_t)src[base + lo].state : 0u, arc, src,
+                                   ai - sm.em.beg[w][lo]);
         lo = lon;
         ai = ain;
         arc = arcn;
@@ -1485,9 +1774,10 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           if (sm.em.off[w][mid] <= k) lo = mid;
           else hi = mid - 1;
         }
-        emit_arc<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
-                 sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]), sm.em.cost[w][lo], (uint32_t)(base + lo),
-                 FSA ? (uint32_t)src[base + lo].state : 0u);
+        emit_arc<FSA, FAST>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
+                            sm.em.beg[w][lo] + (uint32_t)(k - sm.em.off[w][lo]), sm.em.cost[w][lo],
+                            (uint32_t)(base + lo), FSA ? (uint32_t)src[base + lo].state : 0u, src,
+                            (uint32_t)(k - sm.em.off[w][lo]));
       }
 #endif
       __syncwarp();
@@ -1532,9 +1822,9 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
             else hi = mid - 1;
           }
           const BigSrc bs = bigl[lo];  // (the listed source: a small, hot array)
-          emit_arc<FSA>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
-                   bs.beg + (uint32_t)(k - sm.bg.pref[lo]), bs.cost, (uint32_t)bs.idx,
-                   FSA ? (uint32_t)src[bs.idx].state : 0u);
+          emit_arc<FSA, FAST>(sm, L, g, a, nll_s, smem_ll, row0, neg_scale, boost,
+                              bs.beg + (uint32_t)(k - sm.bg.pref[lo]), bs.cost, (uint32_t)bs.idx,
+                              FSA ? (uint32_t)src[bs.idx].state : 0u, src, (uint32_t)(k - sm.bg.pref[lo]));
         }
       }
       __syncthreads();
@@ -1550,7 +1840,8 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     // ---- epsilon closure ----
     int st = CTW_OK;
     if (sm.st_all < CTW_GROW_TABLE)
-      st = eps_fixpoint<FSA>(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
+      st = FAST ? eps_fast<FSA>(sm, L, g, boost, a.cfg.beam, pass_cap)
+                : eps_fixpoint<FSA>(sm, L, g, fc, boost, a.cfg.relax_eps, a.cfg.beam, pass_cap);
     const int vote = sm.st_all;
     if (tid < 32) {
       int tot = tid < R ? cl.map_shared_rank(&sm, tid)->n_slots : 0;  // stable: the closure is over
@@ -1591,7 +1882,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     ulonglong2* sv = reinterpret_cast<ulonglong2*>(L.front);
     uint2* ib = L.front + 2 * (size_t)L.seg;
     if (status == CTW_OK)
-      status = count_pass(sm, L, fc, sv, ib, n_all, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
+      status = count_pass<FAST>(sm, L, fc, sv, ib, n_all, a.cfg.max_ne_iters, cut_key, min_cost, bin_scale, true);
     const int n_ib = sm.cnt_all;
     if (rank == 0 && tid == 0) {
       const long long t = clock64();
@@ -1647,12 +1938,12 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           const ulonglong2 v0 = sv[i];
           const unsigned long long key = v0.x;
           const uint2 it = ib[i];
-          const uint32_t h = it.x, st2 = it.y;
+          const uint32_t st2 = it.y;
           if (!keep(key, st2)) continue;
           const CtwStateRange rg = ld_range(g.ranges, FSA ? (st2 & L.smask) : st2);  // independent of the walk: overlaps it
-          const WalkEnd wk = walk(L, g, v0, src, pend, hop_cap);
+          const WalkEnd wk = walk<FAST>(L, g, v0, src, pend, hop_cap);
           if (!wk.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
-          const int32_t code = record_code(sm, L, g, h, wk);
+          const int32_t code = record_code<FAST>(sm, L, g, src, v0, wk);
           const long long r = sm.n_rec + pos;
           CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
           const int ro = (int)(r & (CTW_PAGE - 1));
@@ -1695,7 +1986,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
     }
 
     // ---- reset every table entry this rank created (also on failure) ----
-    reset_slots(L, n_all);
+    reset_slots<FAST>(L, n_all);
     __syncthreads();
     if (rank == 0 && tid == 0) prof[5] += clock64() - sm.tclk;
     if (status != CTW_OK) {
@@ -1802,13 +2093,13 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
   if (status == CTW_OK && (uint32_t)sm.n_slots > L.seg) status = CTW_GROW_TABLE;
   if (status == CTW_OK && n_own > lane.scap) status = CTW_GROW_SRC;
   ulonglong2* sv = reinterpret_cast<ulonglong2*>(lane.front);
-  if (status == CTW_OK) status = count_pass(sm, L, fc, sv, nullptr, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
+  if (status == CTW_OK)
+    status = count_pass<false>(sm, L, fc, sv, nullptr, n_own, cfg.max_ne_iters, 0ULL, 0.0, 1.0, false);
   if (status == CTW_OK) {
     CtwSrc* dst = lane.src[0];
     for (int i = tid; i < n_own; i += CTW_BS) {
-      const uint32_t h = L.slots[i].x;
       const ulonglong2 v0 = sv[i];
-      const WalkEnd w = walk(L, g, v0, nullptr, nullptr, n_own + 2);
+      const WalkEnd w = walk<false>(L, g, v0, nullptr, nullptr, n_own + 2);
       if (!w.ok) atomicMax(&sm.status_l, CTW_ERR_EPS_ITERS);
       CtwSrc s;
       s.state = (int32_t)L.slots[i].y;
@@ -1818,12 +2109,12 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
       s.emit_beg = rg.emit_beg;
       s.emit_end = rg.emit_end;
       dst[i] = s;
-      lane.pend[i] = record_code(sm, L, g, h, w);
+      lane.pend[i] = record_code<false>(sm, L, g, nullptr, v0, w);
     }
     __syncthreads();
     if (sm.status_l != CTW_OK) status = sm.status_l;
   }
-  reset_slots(L, n_own);
+  reset_slots<false>(L, n_own);
   __syncthreads();
   if (tid == 0) {
     CtwLaneOut o = {};
@@ -1977,10 +2268,13 @@ static int cluster_size(int n) {
 extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                  const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
                                  int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
-                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, cudaStream_t stream) {
+                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast, int ebits,
+                                 cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
-  void (*KFN)(CtwLane*, GraphDev, ChunkArgs, CtwLaneOut*) = any_fsa ? k_decode_chunk<true> : k_decode_chunk<false>;
-  ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, *cfg};
+  void (*KFN)(CtwLane*, GraphDev, ChunkArgs, CtwLaneOut*) =
+      fast ? (any_fsa ? k_decode_chunk<true, true> : k_decode_chunk<false, true>)
+           : (any_fsa ? k_decode_chunk<true, false> : k_decode_chunk<false, false>);
+  ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, ebits, *cfg};
   const size_t dyn = (width <= CTW_MAX_SMEM_WIDTH ? (size_t)width : 0) * sizeof(double);
   if (dyn + sizeof(Smem) > 48 * 1024)
     cudaFuncSetAttribute(KFN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);

@@ -29,6 +29,7 @@ import bisect
 import ctypes as C
 import math
 import threading
+import warnings
 import weakref
 from dataclasses import dataclass
 from typing import NamedTuple, Sequence
@@ -232,29 +233,53 @@ class DeviceGraph:
         self._lock = threading.Lock()
         self._fin = weakref.finalize(self, L.ctw_graph_destroy, h)
 
-    def pool(self, config: DecoderConfig, num_states: int) -> "LanePool":
+    def pool(self, config: DecoderConfig, num_states: int, search: str = "exact") -> "LanePool":
         ne = config.max_nonemitting_iters if config.max_nonemitting_iters is not None else 2 * num_states
         key = (config.beam, min(config.max_active, _MAX_ACTIVE_CAP), config.acoustic_scale,
                config.nonemitting_relax_epsilon, ne)
+        mode = _search_mode(search)
+        if ne < min(1 << 16, num_states + 1) and (key, mode) not in self.pools:
+            # ctw_api.cu prune_flag: a cap that could bind keeps the full
+            # Gauss-Seidel pass accounting (no early beam pruning, no fast mode)
+            warnings.warn(f"max_nonemitting_iters={ne} can bind before the epsilon closure converges "
+                          f"(< min(65536, num_states + 1)): early beam pruning and the fast search mode "
+                          f"are disabled for this configuration (exact but slower)", RuntimeWarning, stacklevel=3)
         with self._lock:
-            p = self.pools.get(key)
+            p = self.pools.get((key, mode))
             if p is None:
-                p = LanePool(self, key)
-                self.pools[key] = p
+                p = LanePool(self, key, mode)
+                self.pools[(key, mode)] = p
             return p
+
+
+SEARCH_MODES = ("exact", "fast")
+
+
+def _search_mode(search) -> str:
+    """Search mode of a lane pool (include/ctcwfst_b200.h ctw_lanes_set_search):
+    "exact" reproduces the reference kernel record for record (histories,
+    prev pointers); "fast" is the words-exact throughput mode (identical
+    best-path words, costs within the reference's relax_eps stop rule)."""
+    if search is None:
+        return "exact"
+    if search not in SEARCH_MODES:
+        raise ValueError(f"search must be one of {SEARCH_MODES}, got {search!r}")
+    return search
 
 
 class LanePool:
     """A ctw_lanes set (one decoder configuration on one device graph) with a
     free list; DecodeState objects borrow lanes from it."""
 
-    def __init__(self, dg: DeviceGraph, key):
+    def __init__(self, dg: DeviceGraph, key, search: str = "exact"):
         L = _lib.load()
         self.dg = dg
         self.cfg = _lib.CtwConfig(key[0], key[1], key[2], key[3], key[4])
         h = C.c_void_p()
         _lib.check(L.ctw_lanes_create(dg.handle, 0, C.byref(self.cfg), None, C.byref(h)), "lane set creation")
         self.handle = h
+        self.search = search
+        _lib.check(L.ctw_lanes_set_search(h, SEARCH_MODES.index(search)), "search mode")
         self.size = 0
         self.free: list[int] = []
         self.lock = threading.Lock()
@@ -337,6 +362,12 @@ class LanePool:
     def reset_stats(self) -> None:
         _lib.load().ctw_lanes_reset_stats(self.handle)
 
+    def search_info(self) -> dict:
+        """Requested search mode and how many decode launches ran fast."""
+        v = np.zeros(3, np.int64)
+        _lib.load().ctw_lanes_search_info(self.handle, _lib.ptr(v))
+        return {"search": SEARCH_MODES[int(v[0])], "fast_launches": int(v[1]), "decode_launches": int(v[2])}
+
 
 # ---------------------------------------------------- loglik marshalling ---
 
@@ -380,7 +411,8 @@ class DecodeState:
     Default: the channel is a lane in HBM. With ``kernel=`` the reference's
     host bookkeeping is used around that kernel callable (plug-in seam)."""
 
-    def __init__(self, graph, config: DecoderConfig, kernel=None, device: int | None = None):
+    def __init__(self, graph, config: DecoderConfig, kernel=None, device: int | None = None,
+                 search: str = "exact"):
         self.graph = flatten(graph)
         self.config = config
         self.frame_count = 0
@@ -391,7 +423,7 @@ class DecodeState:
                               else 2 * self.graph.num_states)
         if kernel is None:
             dg = self.graph.device_graph(device)
-            self._pool = dg.pool(config, self.graph.num_states)
+            self._pool = dg.pool(config, self.graph.num_states, search)
             self._lane = self._pool.acquire(1)[0]
             self._fin = weakref.finalize(self, self._pool.release, [self._lane])
             self._cache = None
@@ -796,7 +828,8 @@ def decode_utterance(graph, config: DecoderConfig, loglik, boost: np.ndarray | N
 
 
 def decode_batch(graph, config: DecoderConfig, utterances: Sequence, workers: int = 1, boost=None,
-                 *, device: int | None = None, max_lanes: int | None = None, lattice_beam: float | None = None) -> list:
+                 *, device: int | None = None, max_lanes: int | None = None, lattice_beam: float | None = None,
+                 search: str = "exact") -> list:
     """Decode utterances independently; results keep the input order,
     failures are reported per index (decoder.py:436-463).
 
@@ -804,7 +837,8 @@ def decode_batch(graph, config: DecoderConfig, utterances: Sequence, workers: in
     lanes of ONE kernel launch; ``workers`` is accepted for signature
     compatibility (parallelism is the lane batch). ``boost`` is one dense
     vector for every utterance, or a sequence with one vector/None per
-    utterance (per-utterance boosting)."""
+    utterance (per-utterance boosting). ``search="fast"`` selects the
+    words-exact throughput mode (identical words; see ``SEARCH_MODES``)."""
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
     fg = flatten(graph)
@@ -814,7 +848,7 @@ def decode_batch(graph, config: DecoderConfig, utterances: Sequence, workers: in
         raise ValueError("per-utterance boost list must match the number of utterances")
     results: list = [None] * n
     group = n if max_lanes is None else max(1, int(max_lanes))
-    pool = fg.device_graph(device).pool(config, fg.num_states)
+    pool = fg.device_graph(device).pool(config, fg.num_states, search)
     for g0 in range(0, n, group):
         idx = list(range(g0, min(n, g0 + group)))
         _decode_group(fg, config, pool, utterances, idx, boost, per_utt, results, lattice_beam)

@@ -235,14 +235,14 @@ class PhraseBoost:
 
 
 def decode_lattices(graph, config, utterances: Sequence, lattice_beam: float = 6.0, boost=None, *,
-                    device: int | None = None, max_lanes: int | None = None) -> list:
+                    device: int | None = None, max_lanes: int | None = None, search: str = "exact") -> list:
     """decode_batch plus a pruned lattice per utterance: a list of Lattice
     (``.best_path`` is decode_batch's Hypothesis) or DecodeFailure, in input
     order."""
     if not (lattice_beam >= 0):
         raise ValueError("lattice_beam must be >= 0")
     return decode_batch(graph, config, utterances, boost=boost, device=device, max_lanes=max_lanes,
-                        lattice_beam=float(lattice_beam))
+                        lattice_beam=float(lattice_beam), search=search)
 
 
 def build_lattices(pool, states, mats, on_dev, packed, hyps, lattice_beam: float) -> list:

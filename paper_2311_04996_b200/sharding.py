@@ -65,7 +65,7 @@ def _reindex(r, i):
 
 
 def decode_batch_devices(graph, config, utterances: Sequence, devices: Sequence[int], boost=None,
-                         decode_fn: Callable | None = None) -> list:
+                         decode_fn: Callable | None = None, **kw) -> list:
     """Decode on several GPUs from one process: shard, one host thread per
     device, gather in input order."""
     from .decoder import decode_batch, flatten
@@ -81,7 +81,7 @@ def decode_batch_devices(graph, config, utterances: Sequence, devices: Sequence[
         if not idx:
             return []
         b = [boost[i] for i in idx] if per_utt else boost
-        return fn(fg, config, [utterances[i] for i in idx], boost=b, device=devices[k])
+        return fn(fg, config, [utterances[i] for i in idx], boost=b, device=devices[k], **kw)
 
     with ThreadPoolExecutor(max_workers=len(devices)) as pool:
         parts = list(pool.map(run, range(len(devices))))
@@ -89,7 +89,7 @@ def decode_batch_devices(graph, config, utterances: Sequence, devices: Sequence[
 
 
 def decode_batch_distributed(graph, config, utterances: Sequence, boost=None, group=None,
-                             decode_fn: Callable | None = None, device: int | None = None) -> list:
+                             decode_fn: Callable | None = None, device: int | None = None, **kw) -> list:
     """Decode under torch.distributed: every rank passes the SAME utterance
     list, decodes its LPT shard on its local device and receives the full
     result list (input order)."""
@@ -105,7 +105,7 @@ def decode_batch_distributed(graph, config, utterances: Sequence, boost=None, gr
     idx = shards[rank]
     per_utt = isinstance(boost, (list, tuple))
     b = [boost[i] for i in idx] if per_utt else boost
-    mine = fn(flatten(graph), config, [utterances[i] for i in idx], boost=b, device=device) if idx else []
+    mine = fn(flatten(graph), config, [utterances[i] for i in idx], boost=b, device=device, **kw) if idx else []
     parts: list = [None] * world
     dist.all_gather_object(parts, mine, group=group)
     return _merge(n, shards, parts)
