@@ -126,6 +126,24 @@ int ctw_fst_compose(const ctw_fst* a, const ctw_fst* b, ctw_fst* out) {
     queue.emplace_back((int32_t)qa, (int32_t)qb);
     return id;
   };
+  // a's arcs grouped by (state, olabel), preserving order: a state with many
+  // more arcs than its partner (the lexicon's start state against a grammar
+  // state) is matched from b's side, then put back in the reference's
+  // (a arc, b arc) order -- identical output, no per-a-arc searches
+  std::vector<int64_t> aorder((size_t)a->num_arcs);
+  std::iota(aorder.begin(), aorder.end(), 0);
+  for (int64_t s = 0; s < a->num_states; ++s)
+    std::stable_sort(aorder.begin() + a->off[s], aorder.begin() + a->off[s + 1],
+                     [&](int64_t x, int64_t y) { return a->olabel[x] < a->olabel[y]; });
+  auto arange = [&](int64_t qa, int32_t lab, int64_t& lo, int64_t& hi) {
+    const int64_t* beg = aorder.data() + a->off[qa];
+    const int64_t* end = aorder.data() + a->off[qa + 1];
+    auto cmp1 = [&](int64_t x, int32_t v) { return a->olabel[x] < v; };
+    auto cmp2 = [&](int32_t v, int64_t x) { return v < a->olabel[x]; };
+    lo = std::lower_bound(beg, end, lab, cmp1) - aorder.data();
+    hi = std::upper_bound(beg, end, lab, cmp2) - aorder.data();
+  };
+  std::vector<std::pair<int64_t, int64_t>> pairs;  // (a arc, border position or -1 for an eps-output a arc)
   state_of(a->start, b->start);
   Arcs arcs;
   std::vector<double> fin;
@@ -134,17 +152,49 @@ int ctw_fst_compose(const ctw_fst* a, const ctw_fst* b, ctw_fst* out) {
     const int64_t src = (int64_t)head;
     const double fa = a->final_w[qa], fb = b->final_w[qb];
     fin.push_back((std::isfinite(fa) && std::isfinite(fb)) ? fa + fb : INFINITY);
-    for (int64_t k = a->off[qa]; k < a->off[qa + 1]; ++k) {
-      if (a->olabel[k] == 0) {
-        const int32_t d = state_of(a->nextstate[k], qb);
-        arcs.add(src, a->ilabel[k], 0, a->weight[k], d);
-      } else {
-        int64_t lo, hi;
-        brange(qb, a->olabel[k], lo, hi);
-        for (int64_t p = lo; p < hi; ++p) {
-          const int64_t j = border[p];
+    const int64_t na = a->off[qa + 1] - a->off[qa], nb = b->off[qb + 1] - b->off[qb];
+    if (na > 8 * (nb + 1)) {
+      pairs.clear();
+      int64_t lo, hi;
+      arange(qa, 0, lo, hi);
+      for (int64_t p = lo; p < hi; ++p) pairs.emplace_back(aorder[p], -1);
+      for (int64_t p = b->off[qb]; p < b->off[qb + 1];) {
+        const int32_t lab = b->ilabel[border[p]];
+        int64_t q = p;
+        while (q < b->off[qb + 1] && b->ilabel[border[q]] == lab) ++q;
+        if (lab != 0) {
+          int64_t alo, ahi;
+          arange(qa, lab, alo, ahi);
+          for (int64_t x = alo; x < ahi; ++x)
+            for (int64_t y = p; y < q; ++y) pairs.emplace_back(aorder[x], y);
+        }
+        p = q;
+      }
+      std::sort(pairs.begin(), pairs.end());
+      for (const auto& pr : pairs) {
+        const int64_t k = pr.first;
+        if (pr.second < 0) {
+          const int32_t d = state_of(a->nextstate[k], qb);
+          arcs.add(src, a->ilabel[k], 0, a->weight[k], d);
+        } else {
+          const int64_t j = border[pr.second];
           const int32_t d = state_of(a->nextstate[k], b->nextstate[j]);
           arcs.add(src, a->ilabel[k], b->olabel[j], a->weight[k] + b->weight[j], d);
+        }
+      }
+    } else {
+      for (int64_t k = a->off[qa]; k < a->off[qa + 1]; ++k) {
+        if (a->olabel[k] == 0) {
+          const int32_t d = state_of(a->nextstate[k], qb);
+          arcs.add(src, a->ilabel[k], 0, a->weight[k], d);
+        } else {
+          int64_t lo, hi;
+          brange(qb, a->olabel[k], lo, hi);
+          for (int64_t p = lo; p < hi; ++p) {
+            const int64_t j = border[p];
+            const int32_t d = state_of(a->nextstate[k], b->nextstate[j]);
+            arcs.add(src, a->ilabel[k], b->olabel[j], a->weight[k] + b->weight[j], d);
+          }
         }
       }
     }

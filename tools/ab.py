@@ -33,16 +33,16 @@ def child(args):
     ll = torch.from_numpy(bench.workload(s, args.batch, args.frames, 0)).cuda()
     boosts = bench.boost_tables(s, args.batch, 0) if args.config == "c5" else None
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    pool = fg.device_graph(0).pool(cfg, fg.num_states)
+    pool = fg.device_graph(0).pool(cfg, fg.num_states, args.search)
     for _ in range(args.warmup):
-        out = decode_batch(fg, cfg, ll, device=0, boost=boosts)
+        out = decode_batch(fg, cfg, ll, device=0, boost=boosts, search=args.search)
     pool.reset_stats()
     ms = []
     for _ in range(args.steps):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        out = decode_batch(fg, cfg, ll, device=0, boost=boosts)
+        out = decode_batch(fg, cfg, ll, device=0, boost=boosts, search=args.search)
         b.record()
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
@@ -59,6 +59,7 @@ def child(args):
                                                                     "records", "reset")) / (frames / 1),
                       "stage": {k: prof[k] / frames for k in ("emit", "eps", "beam_count", "select", "records", "r15",
                                                               "reset")},
+                      "slots": prof["slots"] / frames, "eps_items": prof["eps_items"] / frames,
                       "digest": h.hexdigest()[:16]}))
 
 
@@ -70,6 +71,7 @@ def main():
     ap.add_argument("--batch", type=int, default=512)
     ap.add_argument("--frames", type=int, default=250)
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--search", default="fast")
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--rounds", type=int, default=1, help="repeat the whole variant list (interleaved)")
     args = ap.parse_args()
@@ -80,7 +82,8 @@ def main():
         for lib in args.libs:
             env = dict(os.environ, CTW_B200_LIB=str(Path(lib).resolve()))
             cmd = [sys.executable, __file__, "--child", "--steps", str(args.steps), "--warmup", str(args.warmup),
-                   "--batch", str(args.batch), "--frames", str(args.frames), "--config", args.config]
+                   "--batch", str(args.batch), "--frames", str(args.frames), "--config", args.config,
+                   "--search", args.search]
             r = subprocess.run(cmd, env=env, capture_output=True, text=True)
             line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-2000:]
             print(Path(lib).name, line, flush=True)

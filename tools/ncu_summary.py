@@ -1,7 +1,7 @@
 """Summarise an ncu launch list (csv) and one --set full capture into the
 profiles/ evidence files bench.py reads.
 
-    python tools/ncu_summary.py LAUNCHES.csv FULL.ncu-rep TAG
+    python tools/ncu_summary.py LAUNCHES.csv FULL.ncu-rep TAG [SEARCH]
 
 writes profiles/TAG_launches.json, profiles/TAG_full_metrics.json and
 refreshes profiles/traffic.json + profiles/ncu_metrics.json (the numbers
@@ -97,16 +97,18 @@ def full(path):
 
 def main():
     lcsv, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    search = sys.argv[4] if len(sys.argv) > 4 else "fast"  # bench.py --search of the captured runs
     L = launches(lcsv)
     L["command"] = ("ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
-                    "lts__t_sector_hit_rate.pct --clock-control none --csv python bench.py --steps 1 --warmup 3 "
-                    "--no-cpu --streams 0 --lattice 0")
+                    "lts__t_sector_hit_rate.pct --clock-control none --csv python bench.py --search " + search +
+                    " --steps 1 --warmup 3 --no-cpu --streams 0 --lattice 0")
     L["note"] = ("serialised, cold-cache launch list (compare shares, not absolutes); the steady-state "
                  "k_decode_chunk launches are 512 lanes x 250 frames; short decode launches are first-call grow re-runs")
     (PROF / f"{tag}_launches.json").write_text(json.dumps(L, indent=1))
     F = full(rep)
     F["command"] = ("ncu --set full --clock-control none --import-source on -k regex:k_decode_chunk -s 4 -c 1 "
-                    "python bench.py --batch 512 --frames 80 --steps 1 --warmup 4 --no-cpu --streams 0 --lattice 0")
+                    "python bench.py --search " + search + " --batch 512 --frames 80 --steps 1 --warmup 4 --no-cpu "
+                    "--streams 0 --lattice 0")
     (PROF / f"{tag}_full_metrics.json").write_text(json.dumps(F, indent=1))
     ss = L["steady_state_decode"]
     dram = ss["mean_dram_gb"] * 1e9
