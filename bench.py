@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=512)
     ap.add_argument("--frames", type=int, default=250)
-    ap.add_argument("--cpu-sample", type=int, default=24, help="utterances in the CPU baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=128,
+                    help="utterances in the CPU baseline sample (also the transcript parity sample)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small", action="store_true", help="tiny graph smoke run (not a bench number)")
     ap.add_argument("--streams", type=int, default=2000, help="C4 streaming channels (0 = skip)")
@@ -324,7 +325,7 @@ def graph_load_run(fg, dev):
             "note": "mmap of a page-cached .ctwg + ctw_graph_create (validation, packing, H2D)"}
 
 
-def lattice_run(fg, cfg, dev_ll, beam, dev):
+def lattice_run(fg, cfg, dev_ll, beam, dev, search="exact"):
     """Lattice leg: the same utterances decoded with a
     pruned lattice (device) and a 10-best list (host A*) per utterance.
     Reports throughput of decode+lattice and of the lattice stage alone."""
@@ -333,15 +334,25 @@ def lattice_run(fg, cfg, dev_ll, beam, dev):
     from paper_2311_04996_b200 import decode_batch, decode_lattices
 
     n = int(dev_ll.shape[0])
-    decode_lattices(fg, cfg, dev_ll, lattice_beam=beam, device=dev)  # warm-up
+    decode_lattices(fg, cfg, dev_ll, lattice_beam=beam, device=dev, search=search)  # warm-up
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    hyps = decode_batch(fg, cfg, dev_ll, device=dev)
+    hyps = decode_batch(fg, cfg, dev_ll, device=dev, search=search)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    lats = decode_lattices(fg, cfg, dev_ll, lattice_beam=beam, device=dev)
+    lats = decode_lattices(fg, cfg, dev_ll, lattice_beam=beam, device=dev, search=search)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
+    # lattice statuses (0 ok, 4 no final path; a closure overflow surfaces as
+    # a DecodeFailure, never as a truncated lattice)
+    from collections import Counter
+
+    from paper_2311_04996_b200 import Lattice
+
+    status_hist = dict(Counter(str(x.status) if isinstance(x, Lattice) else "failure" for x in lats))
+    keep = [i for i, x in enumerate(lats) if isinstance(x, Lattice)]
+    lats = [lats[i] for i in keep]
+    hyps = [hyps[i] for i in keep]
     nb = [lat.nbest(10) for lat in lats]
     t3 = time.perf_counter()
     from paper_2311_04996_b200 import nbest_lattices
@@ -361,7 +372,7 @@ def lattice_run(fg, cfg, dev_ll, beam, dev):
     t5 = time.perf_counter()
     audio = n * int(dev_ll.shape[1]) * FRAME_S
     arcs = [lat.num_arcs for lat in lats]
-    return {"utterances": n, "lattice_beam": beam,
+    return {"utterances": n, "lattice_beam": beam, "status_hist": status_hist,
             "decode_s": t1 - t0, "decode_lattice_s": t2 - t1, "nbest10_host_s": t3 - t2,
             "nbest10_pool_s": tp1 - tp0, "nbest_pool_threads": min(n, os.cpu_count() or 1),
             "nbest_pool_identical": [[h.words for h in x] for x in nb_pool] == [[h.words for h in x] for x in nb],
@@ -579,7 +590,7 @@ def main():
     # optional legs: a failure is recorded in the line instead of losing it
     if args.lattice > 0 and world == 1:
         try:
-            line["lattice"] = lattice_run(fg, cfg, dev_ll[: args.lattice], args.lattice_beam, dev)
+            line["lattice"] = lattice_run(fg, cfg, dev_ll[: args.lattice], args.lattice_beam, dev, args.search)
         except Exception as e:  # noqa: BLE001
             line["lattice"] = {"error": f"{type(e).__name__}: {e}"}
     try:

@@ -46,7 +46,7 @@ extern "C" int ctw_launch_hist_mark(const CtwLane*, const int*, uint32_t* const*
 extern "C" int ctw_launch_hist_compact(CtwLane*, const int*, uint32_t* const*, int32_t* const*,
                                        CtwRecPage* const* const*, long long*, int, cudaStream_t);
 extern "C" int ctw_launch_lattice(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
-                                  CtwLatEntry*, int, const void*, int, int, double, double, cudaStream_t);
+                                  CtwLatEntry*, int, const void*, int, int, double, double, int, int, cudaStream_t);
 
 namespace {
 
@@ -1679,6 +1679,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
   // per-entry buffers; arc / label capacities grow and the lane re-runs on overflow
   std::vector<CtwLatEntry> ent(n);
   std::vector<int32_t> arc_cap(n), lab_cap(n);
+  std::vector<char> big(n, 0);  // re-run with the large closure capacities
   for (int i = 0; i < n; ++i) {
     arc_cap[i] = 4096 + 256 * frames[i];  // ~40 kept arcs per frame at lattice beam 6 on C2
     lab_cap[i] = 4 * arc_cap[i];
@@ -1736,8 +1737,27 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       ent[k] = e;
     }
     CUDA_TRY(cudaMemcpyAsync(d_ent, ent.data(), m * sizeof(CtwLatEntry), cudaMemcpyHostToDevice, l->stream));
+    // CTAs per lane: up to 8 while the batch leaves SMs idle, bounded so a
+    // rank's share of a layer fits its slice of the lane's frontier scratch;
+    // a re-run after a closure overflow takes the large-capacity kernel on
+    // one CTA per lane
+    bool any_big = false;
+    int ranks = 8;
+    {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      while (ranks > 1 && (int64_t)m * ranks > 4LL * sms) ranks >>= 1;
+      for (int k = 0; k < m; ++k) {
+        any_big |= big[todo[k]] != 0;
+        const int64_t seg = (int64_t)CTW_LOAD(1ull << l->h[lane_ids[todo[k]]].tlog2);
+        while (ranks > 1 && 512LL * ranks > 3 * seg) ranks >>= 1;
+      }
+      if (any_big) ranks = 1;
+      if (const char* e = getenv("CTW_LAT_RANKS")) ranks = std::max(1, std::min(8, atoi(e)));  // diagnostics
+    }
     if (ctw_launch_lattice(l->d, g->ranges, g->arcs, g->olabel, g->final_w, d_ent, m, dev_ll, dtype, width,
-                           l->cfg.acoustic_scale, lattice_beam, l->stream)) {
+                           l->cfg.acoustic_scale, lattice_beam, ranks, any_big ? 1 : 0, l->stream)) {
       release();
       return fail(-1, std::string("lattice launch: ") + cudaGetErrorString(cudaGetLastError()));
     }
@@ -1755,7 +1775,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
     for (int k = 0; k < m; ++k) {
       const int i = todo[k];
       const CtwLatEntry& e = ent[k];
-      if (e.status == 1 || e.status == 2) continue;
+      if (e.status == 1 || e.status == 2 || (e.status == 3 && !big[i])) continue;
       const int lane = lane_ids[i];
       const CtwLane& L = l->h[lane];
       Host& h = hb[k];
@@ -1785,6 +1805,11 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       if (e.status == 1 || e.status == 2) {
         arc_cap[i] = std::max<int32_t>(4 * arc_cap[i], e.n_arcs + 1024);
         lab_cap[i] = std::max<int32_t>(4 * lab_cap[i], e.lpool_used + 4096);
+        again.push_back(i);
+        continue;
+      }
+      if (e.status == 3 && !big[i]) {  // a local closure overflowed: re-run with the large capacities
+        big[i] = 1;
         again.push_back(i);
         continue;
       }

@@ -19,14 +19,19 @@
 //
 // The kernel walks the layers backwards so beta is known when a layer's
 // arcs are generated and pruning happens as arcs are produced (a full
-// unpruned lattice would be ~10^7 arcs per utterance). One CTA per lane:
-// per layer, the surviving destination nodes go into the lane's (empty)
-// token table as a state -> node map, every (source, emitting arc) pair is a
-// work item that runs its own small epsilon closure, and kept arcs are
-// appended to the lane's arc buffer.
+// unpruned lattice would be ~10^7 arcs per utterance). One thread-block
+// cluster per lane (1..8 CTAs: several when the batch leaves SMs idle): per
+// layer, the surviving destination nodes go into the lane's (empty) token
+// table as a state -> node map, every (source, emitting arc) pair is a work
+// item that runs its own small epsilon closure, and kept arcs are appended to
+// the lane's arc buffer. A closure that outgrows its local capacity marks
+// the lane (status 3) and the host re-runs it with the large instantiation.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <cub/block/block_scan.cuh>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "ctw_common.h"
 
@@ -35,6 +40,8 @@
 #endif
 #define LAT_CL 48       // local epsilon-closure capacity per work item
 #define LAT_QL 128      // local relaxation budget per work item
+#define LAT_CL_BIG 256  // ... of the re-run for items that overflowed
+#define LAT_QL_BIG 1024
 
 namespace {
 
@@ -76,6 +83,8 @@ __device__ __forceinline__ uint32_t lat_dest(const CtwLane& lane, uint32_t key, 
 }
 
 }  // namespace
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -134,46 +143,177 @@ struct __align__(16) LatSmem {
   int32_t sst[LAT_BS];
   int32_t node[LAT_BS];
   double sc[LAT_BS];
-  int n_arcs, lpool_used, status, nput;
+  int nput, final_mode;
   unsigned long long ac_min;  // min over the frame row of -scale * ll (sortable key)
-  unsigned long long min_beta;
+  unsigned long long min_beta;  // this rank's minimum over its destinations
+  unsigned long long mb_pub;    // ... published to the cluster
+  unsigned long long mb_all;    // cluster-wide minimum
   unsigned long long best;
-  int final_mode;
   unsigned long long items, pruned;
 };
 
 #ifndef LAT_MINB
 #define LAT_MINB 4  // 4 CTAs (64 warps) per SM: every lane of a 512-lane batch resident (61 -> 32 registers; lattice stage -32 %)
 #endif
+
+// One work item: emitting arc ai out of source node `node` (state sst, cost
+// sc) into layer f, with its local epsilon closure of capacity CL states /
+// QL relaxations (overflow -> status 3; the host re-runs the lane with the
+// large-capacity instantiation).
+template <int CL, int QL>
+__device__ __forceinline__ void lat_item(const LatArgs& a, CtwLatEntry& E, const CtwLane& lane, LatSmem& sm,
+                                         uint32_t shift, uint32_t mask, bool cut_ok, double cutoff, double min_beta,
+                                         int32_t sst, double sc, int node, int f, uint32_t ai, long long row0) {
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const CtwArc arc = a.g.arcs[ai];
+  double x;
+  {
+    const long long idx = row0 + arc.ilabel - 1;
+    x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+  }
+  double c0 = __dadd_rn(__dmul_rn(-a.acoustic_scale, x), arc.weight);
+  const int32_t ol0 = a.g.olabel[ai];
+  const uint32_t x0 = lat_dest(lane, (uint32_t)sst, ol0, (uint32_t)arc.nextstate, c0);
+  if (!(c0 < INF)) return;
+  if (cut_ok && sc + c0 + min_beta > cutoff) {
+    atomicAdd(&sm.pruned, 1ULL);
+    return;
+  }
+  atomicAdd(&sm.items, 1ULL);
+  // local epsilon closure from nextstate(e): (state, cost, pred, olabel)
+  typedef typename std::conditional<(CL > 127), int16_t, int8_t>::type Idx;  // closure entry index
+  int32_t cst[CL];
+  double ccost[CL];
+  Idx cpred[CL];
+  int32_t colab[CL];
+  int n = 1;
+  cst[0] = (int32_t)x0;
+  ccost[0] = c0;
+  cpred[0] = -1;
+  colab[0] = ol0;
+  Idx queue[QL];
+  int qh = 0, qt = 1;
+  queue[0] = 0;
+  bool overflow = false;
+  while (qh < qt) {
+    const int u = queue[qh++];
+    const CtwStateRange ru = a.g.ranges[(uint32_t)cst[u] & lane.smask];
+    for (uint32_t b = ru.eps_beg; b < ru.emit_beg; ++b) {
+      const CtwArc ea = a.g.arcs[b];
+      double cy = __dadd_rn(ccost[u], ea.weight);
+      const int32_t oly = a.g.olabel[b];
+      const int32_t ykey = (int32_t)lat_dest(lane, (uint32_t)cst[u], oly, (uint32_t)ea.nextstate, cy);
+      if (!(cy < INF)) continue;
+      if (cut_ok && sc + cy + min_beta > cutoff) continue;
+      int j = 0;
+      while (j < n && cst[j] != ykey) ++j;
+      if (j < n) {
+        if (!(cy < ccost[j])) continue;
+      } else {
+        if (n == CL) {
+          overflow = true;
+          continue;
+        }
+        ++n;
+        cst[j] = ykey;
+      }
+      ccost[j] = cy;
+      cpred[j] = (Idx)u;
+      colab[j] = oly;
+      if (qt == QL) {
+        overflow = true;
+        continue;
+      }
+      queue[qt++] = (Idx)j;
+    }
+  }
+  if (overflow) atomicMax(&E.status, 3);
+  // arcs to the surviving destinations
+  for (int j = 0; j < n; ++j) {
+    const int dn = lat_get(lane, shift, mask, (uint32_t)cst[j]);
+    if (dn < 0) continue;
+    const double bd = lat_key2d(__ldcg(&E.beta[dn]));
+    const double tail = __dadd_rn(ccost[j], bd);
+    atomicMin(&E.beta[node], lat_d2key(tail));
+    if (__dadd_rn(sc, tail) > cutoff) continue;
+    // labels of the minimising path, oldest first
+    int nl = 0;
+    int32_t last = 0;
+    for (int u = j; u >= 0; u = cpred[u])
+      if (colab[u] != 0) {
+        ++nl;
+        last = colab[u];
+      }
+    int32_t code = 0;
+    if (nl == 1) code = last;
+    else if (nl > 1) {
+      const int po = atomicAdd(&E.lpool_used, nl + 1);
+      if (po + nl + 1 > E.lpool_cap) {
+        atomicMax(&E.status, 2);
+        continue;
+      }
+      int32_t* seg = E.lpool + po;
+      seg[0] = nl;
+      int pos = nl;
+      for (int u = j; u >= 0; u = cpred[u])
+        if (colab[u] != 0) seg[pos--] = colab[u];
+      code = -(po + 1);
+    }
+    const int ia = atomicAdd(&E.n_arcs, 1);
+    if (ia >= E.arc_cap) {
+      atomicMax(&E.status, 1);
+      continue;
+    }
+    CtwLatArc la;
+    la.src = node;
+    la.dst = dn;
+    la.w = ccost[j];
+    la.code = code;
+    la.frame = f;
+    la.dst_state = cst[j];
+    la.src_state = sst;
+    E.arcs[ia] = la;
+  }
+}
+
+// One thread-block cluster of R CTAs ("ranks") per lane: the ranks split
+// every layer's destination records and source tiles and meet at cluster
+// barriers between the steps of a layer; counters live in the entry (global
+// atomics), the layer's minimum beta is exchanged through shared memory.
+template <int CL, int QL>
 __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
   __shared__ LatSmem sm;
+  cg::cluster_group cl = cg::this_cluster();
+  const int R = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const int tid = threadIdx.x;
-  CtwLatEntry& E = a.ent[blockIdx.x];
+  CtwLatEntry& E = a.ent[blockIdx.x / R];
   const CtwLane& lane = a.lanes[E.lane];
   const double INF = __longlong_as_double(0x7FF0000000000000LL);
   const uint32_t tlog2 = lane.tlog2;
   const uint32_t mask = (1u << tlog2) - 1, shift = 32 - tlog2;
   const int T = lane.frame_count;
-  const long long R = lane.n_rec;
+  const long long NR = lane.n_rec;
   const int S0 = E.n_seeds;
-  const double neg_scale = -a.acoustic_scale;
+  const long long stride = (long long)R * LAT_BS;
+  // this rank's list of destination-map entries (for the clear), a slice of
+  // the lane's frontier scratch (the host sizes R so a layer's share fits)
+  const int pcap = (int)((size_t)CTW_FRONT_LEN(1u << tlog2) / R);
+  uint2* plist = lane.front + (size_t)rank * pcap;
   if (tid == 0) {
-    sm.n_arcs = 0;
-    sm.lpool_used = 0;
-    sm.status = 0;
     sm.best = ~0ULL;
     sm.final_mode = 0;
     sm.items = 0;
     sm.pruned = 0;
   }
-  for (long long i = tid; i < S0 + R; i += LAT_BS) E.beta[i] = ~0ULL;
-  __syncthreads();
+  for (long long i = (long long)rank * LAT_BS + tid; i < S0 + NR; i += stride) E.beta[i] = ~0ULL;
+  cl.sync();  // beta cleared everywhere before any rank sets the last layer's
   if (T == 0) {
-    if (tid == 0) E.status = 4;
+    if (rank == 0 && tid == 0) E.status = 4;
     return;
   }
-  // ---- last layer: beta = final weight (final states if any survive, else 0)
-  const long long lf0 = lane.frame_base[T - 1], lf1 = R;
+  // ---- last layer: beta = final weight (final states if any survive, else 0);
+  // every rank derives final_mode and the best cost over the whole layer
+  const long long lf0 = lane.frame_base[T - 1], lf1 = NR;
   for (long long r = lf0 + tid; r < lf1; r += LAT_BS) {
     int32_t st;
     double c;
@@ -188,16 +328,16 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
     lat_rec(lane, r, &st, &c);
     const double fw = fm ? a.g.final_w[(uint32_t)st & lane.smask] : 0.0;
     if (fm && fw == INF) continue;
-    E.beta[S0 + r] = lat_d2key(fw);
     atomicMin(&sm.best, lat_d2key(c + fw));
+    if ((((r - lf0) / LAT_BS) % R) == rank) E.beta[S0 + r] = lat_d2key(fw);
   }
-  __syncthreads();
+  cl.sync();  // beta initialised and the last layer's set in every rank's share
   const double best = lat_key2d(sm.best);
   const double cutoff = __dadd_rn(best, a.lattice_beam);
   const bool cut_ok = lane.prune_ok != 0;  // epsilon continuations never lower a cost
 
   for (int f = T - 1; f >= 0; --f) {
-    const long long d0 = lane.frame_base[f], d1 = (f + 1 < T) ? lane.frame_base[f + 1] : R;
+    const long long d0 = lane.frame_base[f], d1 = (f + 1 < T) ? lane.frame_base[f + 1] : NR;
     // ---- destination map: nodes of layer f that can lie on a kept path
     if (tid == 0) {
       sm.min_beta = ~0ULL;
@@ -210,10 +350,10 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
       const long long rr = E.ll_off + (long long)f * a.width;
       for (int v = tid; v < a.width; v += LAT_BS) {
         const double x = a.is_f64 ? ((const double*)a.loglik)[rr + v] : (double)((const float*)a.loglik)[rr + v];
-        atomicMin(&sm.ac_min, lat_d2key(__dmul_rn(neg_scale, x)));
+        atomicMin(&sm.ac_min, lat_d2key(__dmul_rn(-a.acoustic_scale, x)));
       }
     }
-    for (long long r = d0 + tid; r < d1; r += LAT_BS) {
+    for (long long r = d0 + (long long)rank * LAT_BS + tid; r < d1; r += stride) {
       const unsigned long long bk = E.beta[S0 + r];
       if (bk == ~0ULL) continue;
       int32_t st;
@@ -221,20 +361,33 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
       lat_rec(lane, r, &st, &c);
       if (c + lat_key2d(bk) > cutoff) continue;
       const uint32_t h = lat_put(lane, shift, mask, (uint32_t)st, (uint32_t)(S0 + r));
-      if (h != CTW_EMPTY) lane.slots[atomicAdd(&sm.nput, 1)] = make_uint2(h, (uint32_t)st);  // for the clear
+      if (h != CTW_EMPTY) {
+        const int p = atomicAdd(&sm.nput, 1);
+        if (p < pcap) plist[p] = make_uint2(h, (uint32_t)st);  // for the clear
+        else atomicMax(&E.status, 3);
+      }
       atomicMin(&sm.min_beta, bk);
     }
     __syncthreads();
-    const double min_beta = sm.min_beta == ~0ULL ? INF : lat_key2d(sm.min_beta);
-    // ---- sources: layer f-1 (records) or the seeds
+    if (tid == 0) sm.mb_pub = sm.min_beta;
+    cl.sync();  // the whole layer is in the map; every rank's minimum published
+    if (tid < 32) {
+      unsigned long long m = tid < R ? cl.map_shared_rank(&sm, tid)->mb_pub : ~0ULL;
+      for (int d = 16; d; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, m, d);
+        if (o < m) m = o;
+      }
+      if (tid == 0) sm.mb_all = m;
+    }
+    __syncthreads();
+    const double min_beta = sm.mb_all == ~0ULL ? INF : lat_key2d(sm.mb_all);
+    // ---- sources: layer f-1 (records) or the seeds, tiles split over the ranks
     const long long s0 = f > 0 ? lane.frame_base[f - 1] : 0;
     const long long s1 = f > 0 ? d0 : S0;
     const long long nsrc = s1 - s0;
     const long long row0 = E.ll_off + (long long)f * a.width;
     if (min_beta != INF) {
-      // work items = (source, emitting arc): each thread takes sources and
-      // runs every emitting arc of its source
-      for (long long t0 = 0; t0 < nsrc; t0 += LAT_BS) {
+      for (long long t0 = (long long)rank * LAT_BS; t0 < nsrc; t0 += stride) {
         const long long si = t0 + tid;
         int deg = 0;
         const double step_lb = lat_key2d(sm.ac_min) + E.emit_lb;  // any emitting step costs at least this
@@ -271,139 +424,30 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
             if (sm.off[mid] <= item) lo = mid;
             else hi = mid - 1;
           }
-          const int32_t sst = sm.sst[lo];
-          const double sc = sm.sc[lo];
-          const int node = sm.node[lo];
-          const uint32_t ai = sm.beg[lo] + (uint32_t)(item - sm.off[lo]);
-          const CtwArc arc = a.g.arcs[ai];
-          double x;
-          {
-            const long long idx = row0 + arc.ilabel - 1;
-            x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
-          }
-          double c0 = __dadd_rn(__dmul_rn(neg_scale, x), arc.weight);
-          const int32_t ol0 = a.g.olabel[ai];
-          const uint32_t x0 = lat_dest(lane, (uint32_t)sst, ol0, (uint32_t)arc.nextstate, c0);
-          if (!(c0 < INF)) continue;
-          if (cut_ok && sc + c0 + min_beta > cutoff) {
-            atomicAdd(&sm.pruned, 1ULL);
-            continue;
-          }
-          atomicAdd(&sm.items, 1ULL);
-          // local epsilon closure from nextstate(e): (state, cost, pred, olabel)
-          int32_t cst[LAT_CL];
-          double ccost[LAT_CL];
-          int8_t cpred[LAT_CL];
-          int32_t colab[LAT_CL];
-          int n = 1;
-          cst[0] = (int32_t)x0;
-          ccost[0] = c0;
-          cpred[0] = -1;
-          colab[0] = ol0;
-          uint8_t queue[LAT_QL];
-          int qh = 0, qt = 1;
-          queue[0] = 0;
-          bool overflow = false;
-          while (qh < qt) {
-            const int u = queue[qh++];
-            const CtwStateRange ru = a.g.ranges[(uint32_t)cst[u] & lane.smask];
-            for (uint32_t b = ru.eps_beg; b < ru.emit_beg; ++b) {
-              const CtwArc ea = a.g.arcs[b];
-              double cy = __dadd_rn(ccost[u], ea.weight);
-              const int32_t oly = a.g.olabel[b];
-              const int32_t ykey = (int32_t)lat_dest(lane, (uint32_t)cst[u], oly, (uint32_t)ea.nextstate, cy);
-              if (!(cy < INF)) continue;
-              if (cut_ok && sc + cy + min_beta > cutoff) continue;
-              int j = 0;
-              while (j < n && cst[j] != ykey) ++j;
-              if (j < n) {
-                if (!(cy < ccost[j])) continue;
-              } else {
-                if (n == LAT_CL) {
-                  overflow = true;
-                  continue;
-                }
-                ++n;
-                cst[j] = ykey;
-              }
-              ccost[j] = cy;
-              cpred[j] = (int8_t)u;
-              colab[j] = oly;
-              if (qt == LAT_QL) {
-                overflow = true;
-                continue;
-              }
-              queue[qt++] = (uint8_t)j;
-            }
-          }
-          if (overflow) atomicMax(&sm.status, 3);
-          // arcs to the surviving destinations
-          for (int j = 0; j < n; ++j) {
-            const int dn = lat_get(lane, shift, mask, (uint32_t)cst[j]);
-            if (dn < 0) continue;
-            const double bd = lat_key2d(__ldcg(&E.beta[dn]));
-            const double tail = __dadd_rn(ccost[j], bd);
-            atomicMin(&E.beta[node], lat_d2key(tail));
-            if (__dadd_rn(sc, tail) > cutoff) continue;
-            // labels of the minimising path, oldest first
-            int nl = 0;
-            int32_t last = 0;
-            for (int u = j; u >= 0; u = cpred[u])
-              if (colab[u] != 0) {
-                ++nl;
-                last = colab[u];
-              }
-            int32_t code = 0;
-            if (nl == 1) code = last;
-            else if (nl > 1) {
-              const int po = atomicAdd(&sm.lpool_used, nl + 1);
-              if (po + nl + 1 > E.lpool_cap) {
-                atomicMax(&sm.status, 2);
-                continue;
-              }
-              int32_t* seg = E.lpool + po;
-              seg[0] = nl;
-              int pos = nl;
-              for (int u = j; u >= 0; u = cpred[u])
-                if (colab[u] != 0) seg[pos--] = colab[u];
-              code = -(po + 1);
-            }
-            const int ia = atomicAdd(&sm.n_arcs, 1);
-            if (ia >= E.arc_cap) {
-              atomicMax(&sm.status, 1);
-              continue;
-            }
-            CtwLatArc la;
-            la.src = node;
-            la.dst = dn;
-            la.w = ccost[j];
-            la.code = code;
-            la.frame = f;
-            la.dst_state = cst[j];
-            la.src_state = sst;
-            E.arcs[ia] = la;
-          }
+          lat_item<CL, QL>(a, E, lane, sm, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo], sm.node[lo],
+                           f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
         }
         __syncthreads();  // the tile's smem is reused by the next tile
       }
     }
-    __syncthreads();
-    // ---- clear the destination map (the decoder's tok_clear image)
-    for (int i = tid; i < sm.nput; i += LAT_BS) {
-      ulonglong2* q = reinterpret_cast<ulonglong2*>(&lane.table[lane.slots[i].x]);
+    cl.sync();  // the layer's arcs are out; beta of layer f-1 final
+    // ---- clear this rank's destination-map entries (the decoder's tok_clear image)
+    const int np = min(sm.nput, pcap);
+    for (int i = tid; i < np; i += LAT_BS) {
+      ulonglong2* q = reinterpret_cast<ulonglong2*>(&lane.table[plist[i].x]);
       __stcg(q, make_ulonglong2(~0ULL, 0xFFFFFFFFULL));
       __stcg(q + 1, make_ulonglong2(~0ULL, (unsigned long long)CTW_EMPTY));
     }
-    __syncthreads();
+    cl.sync();  // the map is empty before the next layer's puts
   }
   if (tid == 0) {
-    E.n_arcs = sm.n_arcs;
-    E.lpool_used = sm.lpool_used;
-    E.status = sm.status ? sm.status : (sm.best == ~0ULL ? 4 : 0);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&E.closure_items), sm.items);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&E.closure_pruned), sm.pruned);
+  }
+  if (rank == 0 && tid == 0) {
+    if (E.status == 0 && sm.best == ~0ULL) E.status = 4;
     E.final_mode = sm.final_mode;
     E.best = best;
-    E.closure_items = (long long)sm.items;
-    E.closure_pruned = (long long)sm.pruned;
   }
 }
 
@@ -412,10 +456,23 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
 extern "C" int ctw_launch_lattice(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                   const int32_t* olabel, const double* final_w, CtwLatEntry* d_ent, int n,
                                   const void* loglik, int is_f64, int width, double acoustic_scale,
-                                  double lattice_beam, cudaStream_t stream) {
+                                  double lattice_beam, int ranks, int big, cudaStream_t stream) {
   LatArgs a{d_lanes, LatGraph{ranges, arcs, olabel, final_w}, d_ent, loglik, width, is_f64, acoustic_scale,
             lattice_beam};
+  void (*KFN)(LatArgs) = big ? k_lattice<LAT_CL_BIG, LAT_QL_BIG> : k_lattice<LAT_CL, LAT_QL>;
   (void)cudaGetLastError();
-  k_lattice<<<n, LAT_BS, 0, stream>>>(a);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(n * ranks));
+  lc.blockDim = dim3(LAT_BS);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)ranks;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, KFN, a);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }

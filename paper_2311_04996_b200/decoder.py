@@ -934,6 +934,6 @@ def _decode_group(fg, config, pool: LanePool, utterances, idx, boost, per_utt, r
                         lats = build_lattices(pool, [chans[k] for k in lk], [mats[k] for k in lk], on_dev, pk,
                                               [results[order[k]] for k in lk], lattice_beam)
                         for k, lat in zip(lk, lats):
-                            results[order[k]] = lat
+                            results[order[k]] = DecodeFailure(order[k], lat) if isinstance(lat, Exception) else lat
     finally:
         pool.release(lanes)

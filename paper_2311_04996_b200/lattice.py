@@ -264,7 +264,15 @@ def build_lattices(pool, states, mats, on_dev, packed, hyps, lattice_beam: float
     for k in range(n):
         c = _lib.CtwLattice()
         C.memmove(C.byref(c), C.byref(outs[k]), C.sizeof(_lib.CtwLattice))
-        res.append(Lattice(c, hyps[k]))
+        lat = Lattice(c, hyps[k])
+        if lat.status == 3:
+            # even the large-capacity re-run could not hold an epsilon
+            # closure: no silently truncated lattice (reported per index)
+            from .errors import DecodeError
+
+            lat = DecodeError("lattice: an epsilon closure exceeded the per-item capacity "
+                              "(the lattice would be incomplete)")
+        res.append(lat)
     return res
 
 

@@ -384,3 +384,80 @@ def test_long_utterance_history_pages(oracle_mod):
     h = best_path(ch)
     assert (h.words, h.total_cost, h.frame_count) == oc.best_path()
     assert sum(len(f) for f in ch.history_records()) > 65536
+
+
+# ------------------------------------------------ BASELINE configs 3 and 5 --
+
+
+@pytest.fixture(scope="module")
+def c3_graph(tmp_path_factory):
+    """BASELINE config 3's 4-gram TLG (16.5 M states, 52.3 M arcs) built once,
+    written as a .ctwg and loaded back through the memory-mapped loader."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    from paper_2311_04996_b200 import graphio
+
+    s = bench.system(False, "c3")
+    p = graphio.save_graph(s.graph, tmp_path_factory.mktemp("c3") / "c3.ctwg")
+    return s, graphio.load_graph(p)
+
+
+@pytest.mark.parametrize("search", ["exact", "fast"])
+def test_c3_4gram_matches_oracle(oracle_mod, c3_graph, search):
+    """Three Conformer-shaped utterances x 60 frames on the C3 graph (deep
+    backoff chains, 52 M arcs) at the bench configuration: words and cost ==
+    the CPU oracle; the exact mode also reproduces every record."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    from paper_2311_04996_b200 import DecoderConfig, DecodeState, best_path, decode_batch
+
+    s, fg = c3_graph
+    assert fg.num_arcs == s.graph.num_arcs > 50_000_000
+    utts = bench.workload(s, 3, 60, 0)
+    cfg = DecoderConfig(beam=bench.BEAM, max_active=bench.MAX_ACTIVE)
+    got = decode_batch(fg, cfg, utts, search=search)
+    for u, h in zip(utts, got):
+        ow, oc, ofc = oracle_mod.decode_utterance(fg, cfg, u.astype(np.float64))
+        assert h.words == ow and h.frame_count == ofc
+        assert math.isclose(h.total_cost, oc, rel_tol=COST_RTOL)
+        if search == "exact":
+            assert h.total_cost == oc
+    if search == "exact":
+        ch = DecodeState(fg, cfg)
+        ch.advance_frames(utts[0])
+        oc = oracle_mod.OracleChannel.from_config(fg, cfg)
+        oc.advance_frames(utts[0].astype(np.float64))
+        assert_history_equivalent(ch.history_records(), oc.history_records(), exact_prev=False)
+
+
+@pytest.mark.parametrize("search", ["exact", "fast"])
+def test_c5_boosted_matches_oracle(oracle_mod, search):
+    """BASELINE config 5: the C2 graph with a 100-word boost table per
+    utterance (magnitudes U(0.5, 8.5)), 4 utterances x 60 frames."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    from paper_2311_04996_b200 import DecoderConfig, decode_batch
+
+    s = bench.system(False, "c2")
+    utts = bench.workload(s, 4, 60, 0)
+    boosts = bench.boost_tables(s, 4, 0)
+    cfg = DecoderConfig(beam=bench.BEAM, max_active=bench.MAX_ACTIVE)
+    got = decode_batch(s.graph, cfg, utts, boost=boosts, search=search)
+    for u, b, h in zip(utts, boosts, got):
+        ow, oc, ofc = oracle_mod.decode_utterance(s.graph, cfg, u.astype(np.float64), boost=b)
+        assert h.words == ow and h.frame_count == ofc
+        assert math.isclose(h.total_cost, oc, rel_tol=COST_RTOL)
+        if search == "exact":
+            assert h.total_cost == oc

@@ -194,3 +194,61 @@ def test_nbest_lattices_pool_matches_serial():
     pooled = nbest_lattices(lats, 5, workers=4)
     assert [[(h.words, h.total_cost) for h in x] for x in pooled] == \
         [[(h.words, h.total_cost) for h in x] for x in serial]
+
+
+def test_wide_epsilon_closure_reruns_with_large_capacity():
+    """A hub state with 60 epsilon arcs: a work item's local closure outgrows
+    the fast kernel's 48 entries (status 3), the host re-runs the lane with
+    the large-capacity kernel, and the lattice equals the CPU restatement's
+    (never a silently truncated lattice)."""
+    import lattice_oracle as lo
+
+    from paper_2311_04996_b200 import DecoderConfig, FlatGraph, decode_lattices
+
+    n_leaf = 60
+    src, il, ol, w, ns = [0], [1], [1], [0.5], [1]
+    for k in range(2, 2 + n_leaf):
+        src += [1, k]
+        il += [0, 1 + k % 3]
+        ol += [k, 0]
+        w += [0.01 * k, 0.1]
+        ns += [k, 1]
+    final = np.full(2 + n_leaf, np.inf)
+    final[2:] = 0.0
+    fg = FlatGraph.from_arrays(2 + n_leaf, 0, src, il, ol, w, ns, final)
+
+    class Sys:
+        graph = fg
+
+    rng = np.random.default_rng(3)
+    frames = rng.normal(-1.0, 0.5, size=(6, 4))
+    cfg = DecoderConfig(beam=1e9, max_active=10_000)
+    beam = 1.5
+    lat = decode_lattices(fg, cfg, [frames], lattice_beam=beam)[0]
+    assert lat.status == 0
+    ora, seeds, (ow, oc, _) = _oracle_lattice(Sys, cfg, frames, beam)
+    assert lat.best_path.words == ow and abs(lat.best_cost - oc) <= 1e-9
+    inner = lo.kept(ora, beam, -1e-7)
+    outer = lo.kept(ora, beam, +1e-7)
+    assert len(inner) <= lat.num_arcs <= len(outer)
+
+
+def test_lattice_cluster_split_matches_single_cta(monkeypatch):
+    """The lattice kernel spreads a lane over up to 8 CTAs (a cluster) when
+    the batch leaves SMs idle: the lattices equal the one-CTA-per-lane ones
+    arc for arc."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_lattices, synth
+
+    s = _system(num_units=129, blank_id=128, num_words=300, order=3, seed=5, min_pron=1, max_pron=4,
+                followers=15)
+    utts = list(synth.conformer_logprobs(s, 12, 80, seed=2, delta=5.0, sigma=1.5, dtype=np.float32))
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    out = {}
+    for r in ("1", "8"):
+        monkeypatch.setenv("CTW_LAT_RANKS", r)
+        out[r] = decode_lattices(s.graph, cfg, utts, lattice_beam=5.0)
+    for a, b in zip(out["1"], out["8"]):
+        assert a.num_arcs == b.num_arcs > 0
+        assert (a.src == b.src).all() and (a.dst == b.dst).all() and (a.weight == b.weight).all()
+        assert a.labels == b.labels
+        assert [(h.words, h.total_cost) for h in a.nbest(5)] == [(h.words, h.total_cost) for h in b.nbest(5)]
