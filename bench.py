@@ -59,6 +59,11 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=128,
                     help="utterances in the CPU baseline sample (also the transcript parity sample)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=64,
+                    help="--impl reference: utterances per step (>= 4 waves of 16 workers)")
+    ap.add_argument("--ref-w1-sample", type=int, default=4,
+                    help="utterances of the reference's workers=1 figure")
+    ap.add_argument("--dump-ref-inputs", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--small", action="store_true", help="tiny graph smoke run (not a bench number)")
     ap.add_argument("--streams", type=int, default=2000, help="C4 streaming channels (0 = skip)")
     ap.add_argument("--stream-seconds", type=float, default=10.0, help="audio per stream in the C4 run")
@@ -237,7 +242,7 @@ def _stage_profile(prof, st):
     return out
 
 
-def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cores=1):
+def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cores=1, search="exact"):
     """BASELINE config 4: n_streams concurrent channels, 0.5 s chunks (12/13
     frames alternate via 12-frame chunks of 40 ms frames = 0.48 s), two chunks
     per second per stream, arrivals staggered; measured-service simulation of
@@ -263,8 +268,9 @@ def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cor
         from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, StreamPool
 
         pool = StreamPool(s.graph, DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE),
-                          BatcherConfig(max_batch=n_streams), device=device)
-        lp = s.graph.device_graph(device).pool(DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE), s.graph.num_states)
+                          BatcherConfig(max_batch=n_streams), device=device, search=search)
+        lp = s.graph.device_graph(device).pool(DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE), s.graph.num_states,
+                                               search)
         k0 = lp.stats()
         lp.reset_stats()
         k0 = lp.stats()
@@ -291,8 +297,8 @@ def streaming_leg(args, s, rank, world, dev, line):
         return
     # warm-up: one full run of the same shape (a serving process's steady
     # state: lane tables grown, history pages mapped and recycled)
-    streaming_run(s, args.streams, args.stream_seconds, rank + 100, device=dev)
-    st, finals, sutts = streaming_run(s, args.streams, args.stream_seconds, rank, device=dev)
+    streaming_run(s, args.streams, args.stream_seconds, rank + 100, device=dev, search=args.search)
+    st, finals, sutts = streaming_run(s, args.streams, args.stream_seconds, rank, device=dev, search=args.search)
     line["streaming"] = {"gpu": st}
     if world == 1 and not args.no_cpu and args.cpu_streams > 0:
         cores = cores_available()
@@ -399,32 +405,79 @@ def dist_setup(args):
     return world, rank, local
 
 
+REF_INPUT_KEYS = ("num_states", "start", "off", "eps_end", "ilabel", "olabel", "weight", "nextstate", "final",
+                  "max_ilabel", "max_olabel")
+
+
+def dump_ref_inputs(args):
+    """Child process of the reference arm: synthesise the graph and the
+    log-probs with this repo's builders and write them as plain arrays, so
+    the reference process itself never loads this repo's library."""
+    s = system(args.small, args.config)
+    fg = s.graph
+    n = max(args.ref_sample, args.ref_w1_sample)
+    arrs = {k: np.asarray(getattr(fg, k)) for k in REF_INPUT_KEYS}
+    arrs["utts"] = workload(s, n, args.frames, 0)
+    if args.config == "c5":
+        arrs["boosts"] = np.stack(boost_tables(s, n, 0))
+    arrs["describe"] = np.array(describe(args.config, fg, n, args.frames))
+    np.savez(args.dump_ref_inputs, **arrs)
+
+
+def load_ref_inputs(args):
+    import tempfile
+    from types import SimpleNamespace
+
+    with tempfile.TemporaryDirectory() as td:
+        path = Path(td) / "ref_inputs.npz"
+        cmd = [sys.executable, str(ROOT / "bench.py"), "--config", args.config, "--frames", str(args.frames),
+               "--ref-sample", str(args.ref_sample), "--ref-w1-sample", str(args.ref_w1_sample),
+               "--dump-ref-inputs", str(path)] + (["--small"] if args.small else [])
+        subprocess.run(cmd, check=True, env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
+        d = dict(np.load(path))
+    fg = SimpleNamespace(**{k: (d[k].item() if d[k].ndim == 0 else d[k]) for k in REF_INPUT_KEYS})
+    return fg, d["utts"], (list(d["boosts"]) if "boosts" in d else None), str(d["describe"])
+
+
 def reference_arm(args):
-    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    """--impl reference: the unmodified compiled reference (oracle/_ref) on
+    the box's host cores, rank 0 only; inputs generated by a child process
+    and read back as plain numpy arrays (no library of this repo is loaded
+    here). Each step decodes args.ref_sample utterances with
+    decode_batch(workers=all cores) (>= 4 waves of 16 workers); a
+    workers=1 figure on a smaller sample rides along."""
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    s = system(args.small, args.config)
-    n = args.cpu_sample
-    utts = list(workload(s, n, args.frames, 0))
-    boosts = boost_tables(s, n, 0) if args.config == "c5" else None
+    fg, utts_all, boosts_all, desc = load_ref_inputs(args)
+    n = args.ref_sample
+    utts = list(utts_all[:n])
+    boosts = boosts_all[:n] if boosts_all is not None else None
     cores = cores_available()
     for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_decode(utts[: max(1, cores)], s.graph, cores, None if boosts is None else boosts[: max(1, cores)])
+        cpu_decode(utts[: max(1, cores)], fg, cores, None if boosts is None else boosts[: max(1, cores)])
     times = []
     for _ in range(args.steps):
-        _, dt = cpu_decode(utts, s.graph, cores, boosts)
+        _, dt = cpu_decode(utts, fg, cores, boosts)
         times.append(dt)
     audio = n * args.frames * FRAME_S
     value = audio * len(times) / sum(times)
+    k1 = args.ref_w1_sample
+    _, dt1 = cpu_decode(list(utts_all[:k1]), fg, 1, boosts_all[:k1] if boosts_all is not None else None)
     line = {
         "impl": "reference", "metric": "decode RTFx (audio s / decode s)", "value": value, "unit": "x realtime",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(args.config, s.graph, n, args.frames) + "; CPU sample per step"},
+        "config": {"workload": desc + "; CPU sample per step"},
         "cpu_baseline": {"value": value, "unit": "x realtime", "cores": cores, "kind": "reference",
-                         "sample": f"{n} utterances x {args.frames} frames per step", "cpu": cpu_model()},
+                         "sample": f"{n} utterances x {args.frames} frames per step, decode_batch(workers={cores})",
+                         "cpu": cpu_model(),
+                         "workers_1": {"value": k1 * args.frames * FRAME_S / dt1, "unit": "x realtime",
+                                       "sample": f"{k1} utterances, decode_batch(workers=1)"}},
         "e2e": {"value": value, "unit": "x realtime", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libraries": sorted({ln.split()[-1] for ln in open("/proc/self/maps") if ln.rstrip().endswith(".so")
+                                    and ("/oracle/_ref/" in ln or "paper_2311_04996_b200" in ln)}),
     }
     print(json.dumps(line))
 
@@ -441,6 +494,9 @@ def lane_memory(pool):
 
 def main():
     args = parse()
+    if args.dump_ref_inputs:
+        dump_ref_inputs(args)
+        return
     if args.impl == "reference":
         reference_arm(args)
         return
@@ -533,11 +589,18 @@ def main():
     achieved = algo_bytes / (kernel_ms / 1e3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
+    # ncu's DRAM bytes of this kernel come from the committed capture of the
+    # same command (profiles/traffic.json); quoted only when that capture's
+    # workload and search mode are this run's, and stamped as such
+    traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tfile.read_text())
+            if (tj.get("search", "exact") == args.search and args.config == tj.get("config", "c2") and n == 512
+                    and F == 250):
+                traffic = tj.get("dram_bytes_per_launch")
+                traffic_src = tj.get("source") + " (not measured in this run; ncu replays the kernel)"
         except ValueError:
             traffic = None
     ncu = None
@@ -554,7 +617,7 @@ def main():
         "metric": "decode RTFx (audio s / decode s)", "value": value, "unit": "x realtime", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(args.config, fg, n, F),
+        "config": {"workload": describe(args.config, fg, n, F), "search": args.search,
                    "global_batch": world * n, "frames": F, "parallelism": f"utterance-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every step"},
         "utterances_per_s": world * n / (ms_max / 1e3),
@@ -562,15 +625,14 @@ def main():
                 "h2d_bytes_per_step": int(host_np.nbytes), "d2h_bytes_per_step": int(words_bytes)},
         "gpu_launches": int(st["launches"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_decode_chunk",
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "k_decode_chunk",
+                     "search": args.search,
                      "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms_per_launch": kernel_ms,
                      "bytes_model": "28*E_emit + 24*N_src (SURVEY 8(d))",
                      # the north star's evidence metric: DRAM bytes ncu measured for this kernel
                      # (profiles/traffic.json, C2 512x250 launches) over this run's launch time
-                     "measured_dram_gbs": (traffic / (kernel_ms / 1e3) / 1e9
-                                           if traffic and args.config == "c2" and n == 512 and F == 250 else None),
-                     "measured_dram_frac": (traffic / (kernel_ms / 1e3) / 1e9 / peak
-                                            if traffic and args.config == "c2" and n == 512 and F == 250 else None),
+                     "measured_dram_gbs": traffic / (kernel_ms / 1e3) / 1e9 if traffic else None,
+                     "measured_dram_frac": traffic / (kernel_ms / 1e3) / 1e9 / peak if traffic else None,
                      # the emitting-expansion stage alone (its share of the launch from the
                      # kernel's clock64 stage counters): the same bytes over its time
                      "emit_stage_ms": kernel_ms * emit_share,
@@ -612,11 +674,15 @@ def cpu_leg(args, fg, host_np, out, boosts, n, F, line):
         cores = cores_available()
         hyps, dt = cpu_decode([host_np[i] for i in range(k)], fg, cores, None if boosts is None else boosts[:k])
         cpu_rtfx = k * F * FRAME_S / dt
+        k1 = min(4, n)
+        _, dt1 = cpu_decode([host_np[i] for i in range(k1)], fg, 1, None if boosts is None else boosts[:k1])
         line["cpu_baseline"] = {"value": cpu_rtfx, "unit": "x realtime", "cores": cores, "kind": "reference",
                                 "sample": f"first {k} of the {n} utterances, reference " + (
                                     f"decode_batch(workers={cores})" if boosts is None else
                                     f"decode_utterance(boost=...) on {cores} threads"),
-                                "cpu": cpu_model()}
+                                "cpu": cpu_model(),
+                                "workers_1": {"value": k1 * F * FRAME_S / dt1, "unit": "x realtime",
+                                              "sample": f"first {k1} utterances, workers=1"}}
         same = all(getattr(h, "words", None) == g.words for h, g in zip(hyps, out[:k]))
         rel = max(abs(h.total_cost - g.total_cost) / max(1.0, abs(h.total_cost)) for h, g in zip(hyps, out[:k]))
         line["parity"] = {"utterances": k, "words_identical": bool(same), "max_cost_rel_diff": rel}

@@ -113,7 +113,7 @@ def main():
     ss = L["steady_state_decode"]
     dram = ss["mean_dram_gb"] * 1e9
     (PROF / "traffic.json").write_text(json.dumps({
-        "kernel": "k_decode_chunk", "dram_bytes_per_launch": dram,
+        "kernel": "k_decode_chunk", "dram_bytes_per_launch": dram, "search": search, "config": "c2",
         "source": f"profiles/{tag}_launches.json: mean of the steady-state 512x250 launches "
                   "(dram__bytes_read.sum + dram__bytes_write.sum)"}, indent=1))
     (PROF / "ncu_metrics.json").write_text(json.dumps({
