@@ -73,19 +73,54 @@ def parse():
     ap.add_argument("--lattice-beam", type=float, default=6.0)
     ap.add_argument("--search", default="fast", choices=["fast", "exact"],
                     help="lane search mode of the timed decode (decoder.SEARCH_MODES)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"],
-                    help="c2: 3-gram TLG (default, the headline); c3: 4-gram ~50M-arc TLG; "
-                         "c5: c2 + a 100-word boost table per utterance")
-    return ap.parse_args()
+    ap.add_argument("--config", default="auto", choices=["auto", "c2", "c3", "c5"],
+                    help="c2: 3-gram TLG (the N=1 headline, BASELINE configs[1]); c3: 4-gram ~50M-arc TLG "
+                         "(BASELINE configs[2], the utterance-sharded N>1 runs); c5: c2 + a 100-word boost table "
+                         "per utterance; auto: c2 for one GPU, c3 for N>1")
+    args = ap.parse_args()
+    if args.config == "auto":
+        args.config = "c3" if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.gpus > 1 else "c2"
+    return args
 
 
 def system(small: bool, config: str = "c2"):
     from paper_2311_04996_b200 import synth
 
+    return synth.build_system(spec_of(small, config))
+
+
+def spec_of(small: bool, config: str):
+    from paper_2311_04996_b200 import synth
+
     spec = dict(C3 if config == "c3" else C2)
     if small:
         spec.update(num_words=300, followers=10)
-    return synth.build_system(synth.SystemSpec(**spec))
+    return synth.SystemSpec(**spec)
+
+
+def shared_system(args, rank: int, world: int, barrier):
+    """N>1: rank 0 synthesises the graph once and writes it as a .ctwg; the
+    other ranks memory-map it (no per-rank re-synthesis of a 52 M-arc graph)."""
+    if world == 1:
+        return system(args.small, args.config)
+    import tempfile
+
+    from paper_2311_04996_b200 import graphio, synth
+
+    path = Path(tempfile.gettempdir()) / f"ctw_bench_{args.config}_{'s' if args.small else 'f'}_" \
+        f"{os.environ.get('MASTER_PORT', '0')}.ctwg"
+    s = None
+    if rank == 0:
+        s = system(args.small, args.config)
+        graphio.save_graph(s.graph, path.with_suffix(".tmp"))
+        os.replace(path.with_suffix(".tmp"), path)
+    barrier()
+    if rank != 0:
+        s = synth.system_with_graph(spec_of(args.small, args.config), graphio.load_graph(path))
+    barrier()
+    if rank == 0:
+        path.unlink(missing_ok=True)
+    return s
 
 
 def boost_tables(s, n, seed):
@@ -400,8 +435,14 @@ def dist_setup(args):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ndev = torch.cuda.device_count()
+        if world <= ndev:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # more ranks than GPUs (a functional check on a small box): gloo plumbing, shared devices
+            local = local % max(1, ndev)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -507,7 +548,13 @@ def main():
     torch.cuda.set_device(dev)
     from paper_2311_04996_b200 import DecoderConfig, Hypothesis, decode_batch
 
-    s = system(args.small, args.config)
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    s = shared_system(args, rank, world, barrier)
     fg = s.graph
     cfg = DecoderConfig(beam=BEAM, max_active=MAX_ACTIVE)
     n, F, V = args.batch, args.frames, s.num_units
@@ -521,12 +568,6 @@ def main():
     dev_ll = host.to(f"cuda:{dev}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     pool = fg.device_graph(dev).pool(cfg, fg.num_states, args.search)
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
 
     for _ in range(args.warmup):
         out = decode_batch(fg, cfg, dev_ll, device=dev, boost=boosts, search=args.search)
@@ -555,7 +596,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], device=f"cuda:{dev}")
+        t = torch.tensor([ms], device=f"cuda:{dev}" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     audio_total = world * n * F * FRAME_S
@@ -575,7 +616,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
+        t = torch.tensor([e2e_ms], device=f"cuda:{dev}" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     assert [h.words for h in out_e2e] == [h.words for h in out]

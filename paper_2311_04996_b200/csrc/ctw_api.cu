@@ -278,6 +278,11 @@ int grow_keep(cudaStream_t st, T*& p, int64_t keep, int64_t ncap) {
 int grow_hist(ctw_lanes* l, int i, int64_t need) {
   CtwLane& L = l->h[i];
   if (need <= L.rcap) return 0;
+  // record indices are int32 on the device (prev pointers, source
+  // backpointers): a channel's history is capped at 2^31 - 1 records
+  if (need > (int64_t)INT32_MAX)
+    return fail(-1, "channel history would exceed 2^31 records: compact it (DecodeState.compact_history, "
+                    "StreamPool(gc_every=...)) or start a new channel");
   auto& pg = l->hpages[i];
   while ((int64_t)pg.size() * CTW_PAGE < need) {
     CtwRecPage* p = nullptr;
@@ -983,7 +988,9 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     // rate when max_active is effectively unbounded)
     const double ema = l->surv_ema[lane];
     const double est = std::min<double>((double)l->cfg.max_active, std::max(ema < 0 ? 65536.0 : 2.0 * ema, 4096.0));
-    const int64_t need = L.n_rec + (int64_t)std::ceil(est * frames[i]) + 64;
+    // (a presize estimate never asks for more than the int32 record range;
+    // the kernel's exact request is checked when it is made)
+    const int64_t need = std::min<int64_t>(L.n_rec + (int64_t)std::ceil(est * frames[i]) + 64, INT32_MAX);
     if (need > L.rcap)
       if (int r = grow_hist(l, lane, need)) return r;
   }
@@ -1040,7 +1047,10 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
         again.push_back(lane);
       } else if (o.status == CTW_GROW_HIST) {
         const int64_t per = (o.rec_need - L.n_rec) / std::max(1, o.err_frame + 1) + 1;
-        if (int r = grow_hist(l, lane, L.n_rec + (int64_t)(per * 1.5 * frames[i]) + 64)) return r;
+        const int64_t want = L.n_rec + (int64_t)(per * 1.5 * frames[i]) + 64;
+        if (int r = grow_hist(l, lane, o.rec_need > INT32_MAX ? o.rec_need
+                                                               : std::min<int64_t>(want, INT32_MAX)))
+          return r;
         again.push_back(lane);
       } else if (o.status == CTW_GROW_POOL) {
         if (int r = grow_pool(l, lane, 2 * (int64_t)L.pcap)) return r;

@@ -372,9 +372,17 @@ class LanePool:
 # ---------------------------------------------------- loglik marshalling ---
 
 
-def _as_frames(x):
-    """(array, on_device, dtype_code) for a (frames, tokens) matrix given as
-    numpy, torch (CPU or CUDA) or any DLPack producer."""
+def _to_lane_device(x, device: int):
+    """A CUDA tensor on another GPU than the lane set's is copied to the lane
+    set's device (the kernels dereference raw device pointers)."""
+    if getattr(x, "is_cuda", False) and x.device.index != device:
+        return x.to(f"cuda:{device}")
+    return x
+
+
+def _as_frames(x, device: int | None = None):
+    """(array, on_device) for a (frames, tokens) matrix given as numpy, torch
+    (CPU or CUDA) or any DLPack producer; CUDA tensors end up on `device`."""
     if isinstance(x, np.ndarray):
         return x, False
     try:
@@ -388,6 +396,8 @@ def _as_frames(x):
             if x.is_cuda:
                 if x.dtype not in (torch.float32, torch.float64):
                     x = x.double()
+                if device is not None:
+                    x = _to_lane_device(x, device)
                 return x.contiguous(), True
             x = x.numpy()
     return np.asarray(x), False
@@ -601,7 +611,7 @@ class DecodeState:
         leaves the channel unchanged (decoder.py:264-341)."""
         if self._pool is None:
             return self._host_advance(np.ascontiguousarray(loglik, dtype=np.float64))
-        x, on_dev = _as_frames(loglik)
+        x, on_dev = _as_frames(loglik, self._pool.dg.device if self._pool is not None else None)
         if x.ndim != 2:
             raise DecodeError("log-likelihoods must be a (frames, tokens) matrix")
         if x.shape[0] == 0:
@@ -847,15 +857,51 @@ def decode_batch(graph, config: DecoderConfig, utterances: Sequence, workers: in
     if per_utt and len(boost) != n:
         raise ValueError("per-utterance boost list must match the number of utterances")
     results: list = [None] * n
-    group = n if max_lanes is None else max(1, int(max_lanes))
     pool = fg.device_graph(device).pool(config, fg.num_states, search)
+    group = _auto_group(pool, config, utterances, n) if max_lanes is None else max(1, int(max_lanes))
     for g0 in range(0, n, group):
-        idx = list(range(g0, min(n, g0 + group)))
-        _decode_group(fg, config, pool, utterances, idx, boost, per_utt, results, lattice_beam)
+        _decode_split(fg, config, pool, utterances, list(range(g0, min(n, g0 + group))), boost, per_utt, results,
+                      lattice_beam)
     return results
 
 
-def _packed_source(utterances):
+def _auto_group(pool: "LanePool", config: DecoderConfig, utterances, n: int) -> int:
+    """Lanes per launch when the caller does not say: everything that fits in
+    the device's free memory (history reserved at min(max_active, 65536)
+    records x 20 B per frame, as ctw_advance pre-sizes it, plus ~8 MB of
+    table-sized buffers per lane), at least 64."""
+    if n <= 64:
+        return n
+    try:
+        import torch
+
+        free, _ = torch.cuda.mem_get_info(pool.dg.device)
+        frames = int(utterances.shape[1]) if getattr(utterances, "ndim", 0) == 3 else \
+            max(int(np.shape(u)[0]) for u in utterances)
+    except Exception:  # noqa: BLE001 - no estimate: one group, OOM splits below
+        return n
+    per_lane = 20 * min(config.max_active, 65536) * max(1, frames) + (8 << 20)
+    return max(64, min(n, len(pool.free) + int(0.8 * free) // per_lane))
+
+
+def _decode_split(fg, config, pool, utterances, idx, boost, per_utt, results, lattice_beam):
+    """_decode_group, halving the group when the device runs out of memory;
+    a single utterance that does not fit fails with MemoryError at its index
+    (the reference's C_ERR_OOM, _kernel.pyx:491-492)."""
+    try:
+        _decode_group(fg, config, pool, utterances, idx, boost, per_utt, results, lattice_beam)
+    except RuntimeError as e:
+        if "out of memory" not in str(e):
+            raise
+        if len(idx) == 1:
+            results[idx[0]] = DecodeFailure(idx[0], MemoryError(str(e)))
+            return
+        h = len(idx) // 2
+        _decode_split(fg, config, pool, utterances, idx[:h], boost, per_utt, results, lattice_beam)
+        _decode_split(fg, config, pool, utterances, idx[h:], boost, per_utt, results, lattice_beam)
+
+
+def _packed_source(utterances, device: int | None = None):
     """(buffer, on_device, frames, width) when the batch is one contiguous
     (n, F, V) numpy array or CUDA tensor -- decoded without per-utterance
     copies; else None."""
@@ -869,6 +915,8 @@ def _packed_source(utterances):
     if isinstance(utterances, torch.Tensor) and utterances.ndim == 3:
         t = utterances if utterances.dtype in (torch.float32, torch.float64) else utterances.double()
         if t.is_cuda:
+            if device is not None:
+                t = _to_lane_device(t, device)
             return t.contiguous(), True
         return np.ascontiguousarray(t.numpy()), False
     return None
@@ -876,7 +924,7 @@ def _packed_source(utterances):
 
 def _decode_group(fg, config, pool: LanePool, utterances, idx, boost, per_utt, results, lattice_beam=None):
     lanes = pool.acquire(len(idx))
-    packed_src = _packed_source(utterances)
+    packed_src = _packed_source(utterances, pool.dg.device)
     try:
         boosts = [(boost[i] if per_utt else boost) for i in idx]
         st = pool.reset(lanes, boosts)
@@ -889,7 +937,8 @@ def _decode_group(fg, config, pool: LanePool, utterances, idx, boost, per_utt, r
                 results[i] = DecodeFailure(i, DecodeError("epsilon iteration cap exceeded while seeding the channel"))
                 continue
             try:
-                x, on_dev = (packed_src[0][i], packed_src[1]) if packed_src is not None else _as_frames(utterances[i])
+                x, on_dev = ((packed_src[0][i], packed_src[1]) if packed_src is not None
+                             else _as_frames(utterances[i], pool.dg.device))
                 if x.ndim != 2:
                     raise DecodeError("log-likelihoods must be a (frames, tokens) matrix")
                 if x.shape[0] == 0:

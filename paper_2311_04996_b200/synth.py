@@ -391,8 +391,7 @@ class System:
         return self.spec.num_units
 
 
-def build_system(spec: SystemSpec) -> System:
-    rng = np.random.default_rng(spec.seed)
+def _draw_prons(spec: SystemSpec, rng) -> list:
     nb = [u for u in range(spec.num_units) if u != spec.blank_id]
     prons: set = set()
     tries = 0
@@ -402,7 +401,19 @@ def build_system(spec: SystemSpec) -> System:
         tries += 1
         if tries > 100 * spec.num_words:
             raise ValueError("cannot draw enough distinct pronunciations")
-    prons_l = sorted(prons)
+    return sorted(prons)
+
+
+def system_with_graph(spec: SystemSpec, graph: FlatGraph) -> System:
+    """The System of `spec` around an already built graph (e.g. a .ctwg
+    written by another process): pronunciations redrawn (what the log-prob
+    generators need), grammar / lexicon FSTs not rebuilt."""
+    return System(spec, _draw_prons(spec, np.random.default_rng(spec.seed)), None, None, None, None, None, graph)
+
+
+def build_system(spec: SystemSpec) -> System:
+    rng = np.random.default_rng(spec.seed)
+    prons_l = _draw_prons(spec, rng)
     model = random_ngram(rng, spec.num_words, spec.order, spec.followers, spec.tri_contexts, spec.tri_followers)
     t = ctc_topo_compact(spec.num_units, spec.blank_id)
     l = lexicon_fst(prons_l, list(range(1, spec.num_words + 1)))

@@ -247,8 +247,18 @@ def test_lattice_cluster_split_matches_single_cta(monkeypatch):
     for r in ("1", "8"):
         monkeypatch.setenv("CTW_LAT_RANKS", r)
         out[r] = decode_lattices(s.graph, cfg, utts, lattice_beam=5.0)
+    def canon(lat):  # node ids follow the decoder's (free) record order: compare by (layer, state)
+        return sorted(zip(lat.frame.tolist(), lat.src_state.tolist(), lat.dst_state.tolist(), lat.weight.tolist(),
+                          lat.labels))
+
     for a, b in zip(out["1"], out["8"]):
         assert a.num_arcs == b.num_arcs > 0
-        assert (a.src == b.src).all() and (a.dst == b.dst).all() and (a.weight == b.weight).all()
-        assert a.labels == b.labels
-        assert [(h.words, h.total_cost) for h in a.nbest(5)] == [(h.words, h.total_cost) for h in b.nbest(5)]
+        assert canon(a) == canon(b)
+        # same n-best up to f64 summation order (the search adds arc weights
+        # in node order, and node ids follow the free record order)
+        na, nb = a.nbest(5), b.nbest(5)
+        assert len(na) == len(nb)
+        for x, y in zip(na, nb):
+            assert abs(x.total_cost - y.total_cost) <= 1e-9 * abs(x.total_cost)
+        assert {h.words for h in na} == {h.words for h in nb} or \
+            abs(na[-1].total_cost - na[-2].total_cost) <= 1e-9 * abs(na[-1].total_cost)

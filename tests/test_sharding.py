@@ -112,3 +112,87 @@ def test_distributed_driver_gloo_world2():
             assert kind == "DecodeFailure" and index == i
         else:
             assert words == (i, owner[i])
+
+
+def test_decode_split_halves_groups_on_device_oom(monkeypatch):
+    """decode_batch's out-of-memory handling: a group that
+    does not fit is halved until it does; a single utterance that cannot fit
+    fails with MemoryError at its own index -- never the whole batch."""
+    from paper_2311_04996_b200 import decoder as D
+
+    calls = []
+
+    def fake_group(fg, config, pool, utterances, idx, boost, per_utt, results, lattice_beam=None):
+        calls.append(list(idx))
+        if len(idx) > 2 or 5 in idx:
+            raise RuntimeError("lane reset failed (-102): salloc(...): out of memory")
+        for i in idx:
+            results[i] = Hypothesis(words=(i,), total_cost=0.0, frame_count=1)
+
+    monkeypatch.setattr(D, "_decode_group", fake_group)
+    results = [None] * 8
+    D._decode_split(None, None, None, None, list(range(8)), None, False, results, None)
+    assert [type(r).__name__ for r in results] == ["Hypothesis"] * 5 + ["DecodeFailure"] + ["Hypothesis"] * 2
+    assert isinstance(results[5].error, MemoryError) and results[5].index == 5
+    assert all(r.words == (i,) for i, r in enumerate(results) if isinstance(r, Hypothesis))
+    with pytest.raises(RuntimeError, match="boom"):
+        monkeypatch.setattr(D, "_decode_group", lambda *a, **k: (_ for _ in ()).throw(RuntimeError("boom")))
+        D._decode_split(None, None, None, None, [0, 1], None, False, [None, None], None)
+
+
+@pytest.mark.gpu
+def test_devices_driver_with_real_decoder():
+    """decode_batch_devices over a (repeated) device list with the real GPU
+    decoder == decode_batch, in input order, failures at their index."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_batch, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=12, num_words=30, order=2, seed=3))
+    utts = synth.planted_utterances(s, 9, 40, seed=5)
+    utts[4] = np.zeros((0, 12))
+    cfg = DecoderConfig(beam=12.0, max_active=300)
+    want = decode_batch(s.graph, cfg, utts, search="fast")
+    got = decode_batch_devices(s.graph, cfg, utts, devices=[0, 0, 0], search="fast")
+    assert [type(x) for x in got] == [type(x) for x in want]
+    for a, b in zip(got, want):
+        if isinstance(b, Hypothesis):
+            assert a == b
+        else:
+            assert a.index == b.index
+
+
+def _nccl_worker(rank, world, port, out):
+    import torch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    from paper_2311_04996_b200 import DecoderConfig, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=12, num_words=30, order=2, seed=3))
+    utts = synth.planted_utterances(s, 7, 40, seed=6)
+    cfg = DecoderConfig(beam=12.0, max_active=300)
+    got = decode_batch_distributed(s.graph, cfg, utts, device=0, search="fast")
+    out.put([(h.words, h.total_cost) for h in got])
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_distributed_driver_nccl_world_1_with_real_decoder():
+    """decode_batch_distributed under a world-size-1 NCCL process group with
+    the real decoder == decode_batch."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_batch, synth
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    p = ctx.Process(target=_nccl_worker, args=(0, 1, port, q))
+    p.start()
+    got = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    s = synth.build_system(synth.SystemSpec(num_units=12, num_words=30, order=2, seed=3))
+    utts = synth.planted_utterances(s, 7, 40, seed=6)
+    want = decode_batch(s.graph, DecoderConfig(beam=12.0, max_active=300), utts, search="fast")
+    assert got == [(h.words, h.total_cost) for h in want]
