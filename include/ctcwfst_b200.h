@@ -184,6 +184,17 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
 int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* words, int64_t words_cap,
                   int64_t* word_off, double* total_cost, int64_t* frame_count, int32_t* status);
 
+/* ctw_advance followed by ctw_best_path of the same lanes in one call: the
+ * best-path kernel is enqueued right behind the frame kernel and both come
+ * back with one synchronisation (streaming partial hypotheses per chunk,
+ * streaming.py:114-137). Outputs as ctw_advance (status, err_frame) and
+ * ctw_best_path (words .. bstatus); a lane whose chunk failed keeps its
+ * committed state, and its best path is that of the committed frames. */
+int ctw_advance_best(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                     int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
+                     int32_t* status, int32_t* err_frame, int32_t* words, int64_t words_cap, int64_t* word_off,
+                     double* total_cost, int64_t* frame_count, int32_t* bstatus);
+
 /* Channel introspection: committed frame count, active tokens, records. */
 /* Partial-history garbage collection (long-running streams; SURVEY 8(f)
  * item 2): keep only the records reachable from each lane's active tokens

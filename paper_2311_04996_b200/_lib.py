@@ -69,6 +69,7 @@ _SIGS = {
     "ctw_lane_set_fsa": (I32, [P, I32, I32, P, P]),
     "ctw_advance": (I32, [P, P, I32, P, I32, I32, P, P, I32, P, P]),
     "ctw_best_path": (I32, [P, P, I32, P, I64, P, P, P, P]),
+    "ctw_advance_best": (I32, [P, P, I32, P, I32, I32, P, P, I32, P, P, P, I64, P, P, P, P]),
     "ctw_lane_compact": (I32, [P, P, I32, P]),
     "ctw_lanes_presize": (I32, [P, P, I32]),
     "ctw_lane_info": (I32, [P, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),

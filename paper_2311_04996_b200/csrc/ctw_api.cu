@@ -953,11 +953,139 @@ int ctw_lane_set_fsa(ctw_lanes* l, int32_t lane, int32_t n_states, const uint16_
   return 0;
 }
 
-int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
-                int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
-                int32_t* status, int32_t* err_frame) {
-  std::lock_guard<std::mutex> lk(l->mu);
+}  // extern "C"
+
+namespace {
+
+// Best-path scratch for n lanes (device arrays + pinned mirrors).
+int best_prepare(ctw_lanes* l, int n) {
+  if (n <= l->best_cap) return 0;
+  const int c = std::max(n, 2 * l->best_cap);
+  dfree(l->d_woff);
+  dfree(l->d_wcap);
+  dfree(l->d_nwords);
+  dfree(l->d_tcost);
+  dfree(l->d_bstatus);
+  for (void* p : {(void*)l->h_woff, (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus})
+    if (p) cudaFreeHost(p);
+  CUDA_TRY(dalloc(&l->d_woff, c));
+  CUDA_TRY(dalloc(&l->d_wcap, c));
+  CUDA_TRY(dalloc(&l->d_nwords, c));
+  CUDA_TRY(dalloc(&l->d_tcost, c));
+  CUDA_TRY(dalloc(&l->d_bstatus, c));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_woff, c * sizeof(long long)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_wcap, c * sizeof(int)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_nwords, c * sizeof(int)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_tcost, c * sizeof(double)));
+  CUDA_TRY(cudaMallocHost((void**)&l->h_bstatus, c * sizeof(int)));
+  l->best_cap = c;
+  return 0;
+}
+
+// Enqueue k_best_path over the n lanes whose ids are in l->d_ids (uploaded
+// from l->h_ids when `upload_ids`) with word windows caps[], and the copies
+// of its results into the pinned mirrors. No synchronisation.
+int best_enqueue(ctw_lanes* l, int n, const std::vector<int>& caps, bool upload_ids) {
   ctw_graph* g = l->g;
+  if (int r = best_prepare(l, n)) return r;
+  long long tot = 0;
+  for (int i = 0; i < n; ++i) {
+    l->h_woff[i] = tot;
+    l->h_wcap[i] = caps[i];
+    tot += caps[i];
+  }
+  if ((size_t)tot > l->words_cap) {
+    dfree(l->d_words);
+    CUDA_TRY(dalloc(&l->d_words, (size_t)tot + tot / 2));
+    l->words_cap = (size_t)tot + tot / 2;
+  }
+  if ((size_t)tot > l->h_words_cap) {
+    CUDA_TRY(cudaStreamSynchronize(l->stream));  // (the old pinned window may still be a copy target)
+    if (l->h_words) cudaFreeHost(l->h_words);
+    CUDA_TRY(cudaMallocHost((void**)&l->h_words, ((size_t)tot + tot / 2) * sizeof(int32_t)));
+    l->h_words_cap = (size_t)tot + tot / 2;
+  }
+  if (upload_ids) CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+  CUDA_TRY(cudaMemcpyAsync(l->d_woff, l->h_woff, n * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
+  CUDA_TRY(cudaMemcpyAsync(l->d_wcap, l->h_wcap, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+  if (ctw_launch_best(l->d, g->ranges, g->arcs, g->olabel, g->final_w, l->d_ids, n, l->d_words, l->d_woff,
+                      l->d_wcap, l->d_nwords, l->d_tcost, l->d_bstatus, l->stream))
+    return fail(-1, std::string("best-path launch: ") + cudaGetErrorString(cudaGetLastError()));
+  l->launches++;
+  CUDA_TRY(cudaMemcpyAsync(l->h_nwords, l->d_nwords, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
+  CUDA_TRY(cudaMemcpyAsync(l->h_tcost, l->d_tcost, n * sizeof(double), cudaMemcpyDeviceToHost, l->stream));
+  CUDA_TRY(cudaMemcpyAsync(l->h_bstatus, l->d_bstatus, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
+  if (tot) CUDA_TRY(cudaMemcpyAsync(l->h_words, l->d_words, (size_t)tot * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                    l->stream));
+  return 0;
+}
+
+// Results of a completed best_enqueue in the reference layout (status 2 = no
+// frames decoded yet; words oldest first, word_off[n] = total).
+int best_finish(ctw_lanes* l, const int32_t* lane_ids, int n, int32_t* words, int64_t words_cap, int64_t* word_off,
+                double* total_cost, int64_t* frame_count, int32_t* status) {
+  int64_t need = 0;
+  for (int i = 0; i < n; ++i) {
+    const CtwLane& L = l->h[lane_ids[i]];
+    word_off[i] = need;
+    frame_count[i] = L.frame_count;
+    if (L.frame_count == 0) {
+      status[i] = 2;
+      total_cost[i] = INFINITY;
+      continue;
+    }
+    status[i] = l->h_bstatus[i];
+    total_cost[i] = l->h_tcost[i];
+    if (status[i] == 0) need += l->h_nwords[i];
+  }
+  word_off[n] = need;
+  if (need > words_cap) return -2;
+  for (int i = 0; i < n; ++i) {
+    if (status[i] != 0 || l->h_nwords[i] == 0) continue;
+    std::memcpy(words + word_off[i], l->h_words + l->h_woff[i], l->h_nwords[i] * sizeof(int32_t));
+  }
+  return 0;
+}
+
+int best_path_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* words, int64_t words_cap,
+                   int64_t* word_off, double* total_cost, int64_t* frame_count, int32_t* status) {
+  ctw_graph* g = l->g;
+  CUDA_TRY(cudaSetDevice(g->device));
+  if (n <= 0) {
+    word_off[0] = 0;
+    return 0;
+  }
+  for (int i = 0; i < n; ++i)
+    if (lane_ids[i] < 0 || lane_ids[i] >= l->n) return fail(-1, "lane id out of range");
+  if (int r = ensure_scratch(l, n)) return r;
+  // capacity guess: one word per frame is generous for word-level graphs
+  std::vector<int> caps(n);
+  for (int i = 0; i < n; ++i) caps[i] = l->h[lane_ids[i]].frame_count + 8;
+  for (int i = 0; i < n; ++i) l->h_ids[i] = lane_ids[i];
+  for (int round = 0; round < 2; ++round) {
+    if (int r = best_enqueue(l, n, caps, true)) return r;
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
+    bool redo = false;
+    for (int i = 0; i < n; ++i)
+      if (l->h_nwords[i] > caps[i]) {
+        caps[i] = l->h_nwords[i];
+        redo = true;
+      }
+    if (!redo) break;
+  }
+  return best_finish(l, lane_ids, n, words, words_cap, word_off, total_cost, frame_count, status);
+}
+
+// The frame kernel over lanes `lane_ids` (grow-and-rerun protocol). With
+// `bp`, the partial best path of every lane is enqueued right behind the
+// first decode launch (the common case needs no re-run) and comes back with
+// the same synchronisation; *bp_valid says whether it can be used (false
+// after a re-run or a too-small word window: the caller runs it again).
+int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                 int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
+                 int32_t* status, int32_t* err_frame, std::vector<int>* bp, bool* bp_valid) {
+  ctw_graph* g = l->g;
+  if (bp_valid) *bp_valid = false;
   CUDA_TRY(cudaSetDevice(g->device));
   if (n <= 0) return 0;
   using clk = std::chrono::steady_clock;
@@ -1024,6 +1152,12 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
     CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
     l->launches++;
     l->decode_launches++;
+    if (bp && round == 0) {
+      // partial best paths behind the decode (lane ids already on the device)
+      bp->resize(m);
+      for (int k = 0; k < m; ++k) (*bp)[k] = l->h[todo[k]].frame_count + l->h_nframes[k] + 8;
+      if (int r = best_enqueue(l, m, *bp, false)) return r;
+    }
     CUDA_TRY(cudaMemcpyAsync(l->h_out, l->d_out, m * sizeof(CtwLaneOut), cudaMemcpyDeviceToHost, l->stream));
     CUDA_TRY(cudaStreamSynchronize(l->stream));
     const clk::time_point tw = clk::now();
@@ -1072,10 +1206,45 @@ int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* lo
         }
       }
     }
+    if (bp && round == 0 && again.empty()) {
+      *bp_valid = true;
+      for (int k = 0; k < m; ++k)
+        if (l->h_nwords[k] > (*bp)[k]) *bp_valid = false;  // a word window was too small
+    }
     todo.swap(again);
     l->h_post += secs(tw, clk::now());
   }
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctw_advance(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
+                int32_t* status, int32_t* err_frame) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  return advance_impl(l, lane_ids, n, loglik, dtype, location, ll_offsets, frames, width, status, err_frame,
+                      nullptr, nullptr);
+}
+
+int ctw_advance_best(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
+                     int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
+                     int32_t* status, int32_t* err_frame, int32_t* words, int64_t words_cap, int64_t* word_off,
+                     double* total_cost, int64_t* frame_count, int32_t* bstatus) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  if (n <= 0) {
+    word_off[0] = 0;
+    return 0;
+  }
+  std::vector<int> caps;
+  bool ok = false;
+  if (int r = advance_impl(l, lane_ids, n, loglik, dtype, location, ll_offsets, frames, width, status, err_frame,
+                           &caps, &ok))
+    return r;
+  if (!ok) return best_path_impl(l, lane_ids, n, words, words_cap, word_off, total_cost, frame_count, bstatus);
+  return best_finish(l, lane_ids, n, words, words_cap, word_off, total_cost, frame_count, bstatus);
 }
 
 int ctw_lanes_set_search(ctw_lanes* l, int32_t mode) {
@@ -1108,100 +1277,7 @@ int ctw_lanes_host_timing(ctw_lanes* l, double* out) {
 int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* words, int64_t words_cap,
                   int64_t* word_off, double* total_cost, int64_t* frame_count, int32_t* status) {
   std::lock_guard<std::mutex> lk(l->mu);
-  ctw_graph* g = l->g;
-  CUDA_TRY(cudaSetDevice(g->device));
-  if (n <= 0) {
-    word_off[0] = 0;
-    return 0;
-  }
-  for (int i = 0; i < n; ++i)
-    if (lane_ids[i] < 0 || lane_ids[i] >= l->n) return fail(-1, "lane id out of range");
-  if (n > l->best_cap) {
-    const int c = std::max(n, 2 * l->best_cap);
-    dfree(l->d_woff);
-    dfree(l->d_wcap);
-    dfree(l->d_nwords);
-    dfree(l->d_tcost);
-    dfree(l->d_bstatus);
-    for (void* p : {(void*)l->h_woff, (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus})
-      if (p) cudaFreeHost(p);
-    CUDA_TRY(dalloc(&l->d_woff, c));
-    CUDA_TRY(dalloc(&l->d_wcap, c));
-    CUDA_TRY(dalloc(&l->d_nwords, c));
-    CUDA_TRY(dalloc(&l->d_tcost, c));
-    CUDA_TRY(dalloc(&l->d_bstatus, c));
-    CUDA_TRY(cudaMallocHost((void**)&l->h_woff, c * sizeof(long long)));
-    CUDA_TRY(cudaMallocHost((void**)&l->h_wcap, c * sizeof(int)));
-    CUDA_TRY(cudaMallocHost((void**)&l->h_nwords, c * sizeof(int)));
-    CUDA_TRY(cudaMallocHost((void**)&l->h_tcost, c * sizeof(double)));
-    CUDA_TRY(cudaMallocHost((void**)&l->h_bstatus, c * sizeof(int)));
-    l->best_cap = c;
-  }
-  if (int r = ensure_scratch(l, n)) return r;
-  // capacity guess: one word per frame is generous for word-level graphs
-  std::vector<int> caps(n);
-  for (int i = 0; i < n; ++i) caps[i] = l->h[lane_ids[i]].frame_count + 8;
-  for (int round = 0; round < 2; ++round) {
-    long long tot = 0;
-    for (int i = 0; i < n; ++i) {
-      l->h_woff[i] = tot;
-      l->h_wcap[i] = caps[i];
-      l->h_ids[i] = lane_ids[i];
-      tot += caps[i];
-    }
-    if ((size_t)tot > l->words_cap) {
-      dfree(l->d_words);
-      CUDA_TRY(dalloc(&l->d_words, (size_t)tot + tot / 2));
-      l->words_cap = (size_t)tot + tot / 2;
-    }
-    CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(l->d_woff, l->h_woff, n * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(l->d_wcap, l->h_wcap, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
-    if (ctw_launch_best(l->d, g->ranges, g->arcs, g->olabel, g->final_w, l->d_ids, n, l->d_words, l->d_woff,
-                        l->d_wcap, l->d_nwords, l->d_tcost, l->d_bstatus, l->stream))
-      return fail(-1, std::string("best-path launch: ") + cudaGetErrorString(cudaGetLastError()));
-    l->launches++;
-    CUDA_TRY(cudaMemcpyAsync(l->h_nwords, l->d_nwords, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(l->h_tcost, l->d_tcost, n * sizeof(double), cudaMemcpyDeviceToHost, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(l->h_bstatus, l->d_bstatus, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
-    // the whole word window in one copy (pinned), sliced per lane below
-    if ((size_t)tot > l->h_words_cap) {
-      if (l->h_words) cudaFreeHost(l->h_words);
-      CUDA_TRY(cudaMallocHost((void**)&l->h_words, ((size_t)tot + tot / 2) * sizeof(int32_t)));
-      l->h_words_cap = (size_t)tot + tot / 2;
-    }
-    if (tot) CUDA_TRY(cudaMemcpyAsync(l->h_words, l->d_words, (size_t)tot * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                      l->stream));
-    CUDA_TRY(cudaStreamSynchronize(l->stream));
-    bool redo = false;
-    for (int i = 0; i < n; ++i)
-      if (l->h_nwords[i] > caps[i]) {
-        caps[i] = l->h_nwords[i];
-        redo = true;
-      }
-    if (!redo) break;
-  }
-  int64_t need = 0;
-  for (int i = 0; i < n; ++i) {
-    const CtwLane& L = l->h[lane_ids[i]];
-    word_off[i] = need;
-    frame_count[i] = L.frame_count;
-    if (L.frame_count == 0) {
-      status[i] = 2;
-      total_cost[i] = INFINITY;
-      continue;
-    }
-    status[i] = l->h_bstatus[i];
-    total_cost[i] = l->h_tcost[i];
-    if (status[i] == 0) need += l->h_nwords[i];
-  }
-  word_off[n] = need;
-  if (need > words_cap) return -2;
-  for (int i = 0; i < n; ++i) {
-    if (status[i] != 0 || l->h_nwords[i] == 0) continue;
-    std::memcpy(words + word_off[i], l->h_words + l->h_woff[i], l->h_nwords[i] * sizeof(int32_t));
-  }
-  return 0;
+  return best_path_impl(l, lane_ids, n, words, words_cap, word_off, total_cost, frame_count, status);
 }
 
 int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* kept) {
@@ -1581,7 +1657,7 @@ int ctw_advance_chunk_compat(const int64_t* off, const int64_t* eps_end, const i
   for (int64_t i = 0; i < n_src; ++i) {
     if (act_state[i] < 0 || act_state[i] >= num_states) return fail(-1, "active state out of range");
     const int32_t st = act_state[i];
-    srcs[i] = CtwSrc{st, (int32_t)(-2 - i), act_cost[i], (uint32_t)eps_end[st], (uint32_t)off[st + 1]};
+    srcs[i] = CtwSrc{st, (int32_t)(-2 - i), act_cost[i], (uint32_t)eps_end[st], (uint32_t)off[st + 1], -1, 0};
     const int64_t a0 = act_chain_off[i], a1 = act_chain_off[i + 1];
     if (a1 - a0 == 1) pend[i] = act_chain_pool[a0];
     else if (a1 - a0 > 1) {

@@ -78,6 +78,7 @@ struct CtwRecPage {
   int2 link[CTW_PAGE];      // {prev record, olabel code}
   int32_t state[CTW_PAGE];
   double cost[CTW_PAGE];
+  int32_t plab[CTW_PAGE];   // nearest strict ancestor record with output labels (-1: none)
 };
 
 // Active token (32 B): the frame's sources / survivors.
@@ -88,6 +89,10 @@ struct __align__(16) CtwSrc {
   // the state's emitting arc range, cached with the token so the expansion
   // reads arcs without a dependent range lookup
   uint32_t emit_beg, emit_end;
+  // nearest record at or before bp that carries output labels (-1: none):
+  // best-path walks follow these links, one hop per word instead of per frame
+  int32_t anc;
+  int32_t pad;
 };
 
 // Device-side descriptor of one lane (= one decoding channel). The host owns

@@ -93,17 +93,21 @@ __global__ void __launch_bounds__(HG_BS) k_hist_compact(CtwLane* lanes, const in
     const int oo = (int)(r & (CTW_PAGE - 1));
     int2 lk = op->link[oo];
     if (lk.x >= 0) lk.x = ni[lk.x];
+    const int pl = op->plab[oo];  // (an ancestor of a kept record: kept)
     CtwRecPage* pg = np[k >> CTW_PAGE_LOG2];
     const int o = k & (CTW_PAGE - 1);
     pg->link[o] = lk;
+    pg->plab[o] = pl >= 0 ? ni[pl] : pl;
     pg->state[o] = op->state[oo];
     pg->cost[o] = op->cost[oo];
   }
   // frame starts: kept records before the old start
   for (int f = tid; f < L.frame_count; f += HG_BS) L.frame_base[f] = ni[L.frame_base[f]];
   CtwSrc* src = L.src[L.src_buf];
-  for (int i = tid; i < L.n_src; i += HG_BS)
+  for (int i = tid; i < L.n_src; i += HG_BS) {
     if (src[i].bp >= 0) src[i].bp = ni[src[i].bp];
+    if (src[i].anc >= 0) src[i].anc = ni[src[i].anc];
+  }
   if (tid == 0) kept[blockIdx.x] = nk;
 }
 

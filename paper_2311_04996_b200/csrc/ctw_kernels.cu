@@ -902,6 +902,7 @@ __device__ CTW_EPS_INLINE int eps_fixpoint(Smem& sm, const LaneCtx& L, const Gra
 // (_kernel.pyx:400-416).
 struct WalkEnd {
   int32_t bp;
+  int32_t anc;   // the source's nearest labelled record (CtwSrc::anc)
   int32_t pend;  // olabel code of the source's pending chain
   int n;         // labels found on the walk (excluding pend)
   int32_t last;  // the single label when n == 1
@@ -940,7 +941,7 @@ __device__ __forceinline__ int hop_step(const LaneCtx& L, const GraphDev& g, con
 template <bool FAST>
 __device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, ulonglong2 v0, const CtwSrc* src,
                                         const int32_t* pend, int hop_cap) {
-  WalkEnd w{-1, 0, 0, 0, true};
+  WalkEnd w{-1, -1, 0, 0, 0, true};
   ulonglong2 v = v0;
   for (int hop = 0; hop < hop_cap; ++hop) {
     uint32_t a = 0, idx = 0;
@@ -953,6 +954,7 @@ __device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, ulo
     }
     if (k == 1) {
       w.bp = src[idx].bp;
+      w.anc = src[idx].anc;
       w.pend = pend ? pend[idx] : 0;
       return w;
     }
@@ -1948,6 +1950,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
           const int ro = (int)(r & (CTW_PAGE - 1));
           pg->link[ro] = make_int2(wk.bp, code);
+          pg->plab[ro] = wk.anc;
           pg->state[ro] = (int32_t)st2;
           const double cost = key2d(key);
           pg->cost[ro] = cost;
@@ -1957,11 +1960,13 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
           ns.cost = cost;
           ns.emit_beg = rg.emit_beg;
           ns.emit_end = rg.emit_end;
+          ns.anc = code != 0 ? (int32_t)r : wk.anc;
 #if CTW_SRC256
           asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(nsrc + pos),
                        "l"(((unsigned long long)(uint32_t)ns.bp << 32) | (uint32_t)ns.state),
                        "l"((unsigned long long)__double_as_longlong(ns.cost)),
-                       "l"(((unsigned long long)ns.emit_end << 32) | ns.emit_beg), "l"(0ULL)
+                       "l"(((unsigned long long)ns.emit_end << 32) | ns.emit_beg),
+                       "l"((unsigned long long)(uint32_t)ns.anc)
                        : "memory");
 #else
           nsrc[pos] = ns;
@@ -2104,6 +2109,8 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
       CtwSrc s;
       s.state = (int32_t)L.slots[i].y;
       s.bp = -1;
+      s.anc = -1;
+      s.pad = 0;
       s.cost = key2d(v0.x);
       const CtwStateRange rg = g.ranges[(uint32_t)s.state & L.smask];
       s.emit_beg = rg.emit_beg;
@@ -2141,14 +2148,18 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
 
 // ------------------------------------------------------- best path -------
 
-// One warp per lane: best token (final states preferred, ties -> lowest
+// One CTA per lane: best token (final states preferred, ties -> lowest
 // state; decoder.py:384-400), then the backpointer walk over the lane's
 // records. Words are written oldest-first into words[woff[b] .. + cap[b]);
 // nwords[b] always receives the true length (host retries when too small).
-__global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_ids, int n, int32_t* words,
-                            const long long* woff, const int* wcap, int* nwords, double* total_cost, int* status) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int ln = threadIdx.x & 31;
+#define CTW_BPB 256  // best path: threads per lane (the argmin over up to max_active tokens)
+__global__ void __launch_bounds__(CTW_BPB) k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_ids, int n,
+                                                      int32_t* words, const long long* woff, const int* wcap,
+                                                      int* nwords, double* total_cost, int* status) {
+  __shared__ double s_best[CTW_BPB / 32];
+  __shared__ int s_state[CTW_BPB / 32], s_i[CTW_BPB / 32];
+  const int warp = blockIdx.x;  // (the batch entry)
+  const int ln = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (warp >= n) return;
   const CtwLane& lane = lanes[lane_ids[warp]];
   const CtwSrc* src = lane.src[lane.src_buf];
@@ -2156,8 +2167,11 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
   // pass 0: final tokens; pass 1 (only if none final): all tokens
   double best = INF;
   int best_state = 0x7FFFFFFF, best_i = -1;
+  auto better = [](double ob, int os, int oi, double b, int bs, int bi) {
+    return oi >= 0 && (bi < 0 || ob < b || (ob == b && os < bs));
+  };
   for (int pass = 0; pass < 2 && best_i < 0; ++pass) {
-    for (int i = ln; i < lane.n_src; i += 32) {
+    for (int i = threadIdx.x; i < lane.n_src; i += CTW_BPB) {
       const CtwSrc t = src[i];
       double tot;
       if (pass == 0) {
@@ -2178,13 +2192,30 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
       const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
       const int os = __shfl_xor_sync(0xFFFFFFFFu, best_state, o);
       const int oi = __shfl_xor_sync(0xFFFFFFFFu, best_i, o);
-      if (oi >= 0 && (best_i < 0 || ob < best || (ob == best && os < best_state))) {
+      if (better(ob, os, oi, best, best_state, best_i)) {
         best = ob;
         best_state = os;
         best_i = oi;
       }
     }
+    if (ln == 0) {
+      s_best[wid] = best;
+      s_state[wid] = best_state;
+      s_i[wid] = best_i;
+    }
+    __syncthreads();
+    best = s_best[0];
+    best_state = s_state[0];
+    best_i = s_i[0];
+    for (int k = 1; k < CTW_BPB / 32; ++k)
+      if (better(s_best[k], s_state[k], s_i[k], best, best_state, best_i)) {
+        best = s_best[k];
+        best_state = s_state[k];
+        best_i = s_i[k];
+      }
+    __syncthreads();  // (the slots are rewritten by the next pass)
   }
+  if (threadIdx.x >= 32) return;  // the walk and the word move: warp 0
   if (best_i < 0) {
     if (ln == 0) {
       status[warp] = 1;
@@ -2201,8 +2232,11 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
   if (ln == 0) {
     status[warp] = 0;
     total_cost[warp] = best;
-    for (int r = src[best_i].bp; r >= 0;) {
-      const int2 lk = lane.pages[r >> CTW_PAGE_LOG2]->link[r & (CTW_PAGE - 1)];
+    // labelled records only: anc / plab skip the frames without output labels
+    for (int r = src[best_i].anc; r >= 0;) {
+      const CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
+      const int2 lk = pg->link[r & (CTW_PAGE - 1)];
+      const int nxt = pg->plab[r & (CTW_PAGE - 1)];
       const int c = lk.y;
       if (c > 0) {
         if (pos > 0) w[pos - 1] = c;
@@ -2217,7 +2251,7 @@ __global__ void k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_id
         }
         count += m;
       }
-      r = lk.x;
+      r = nxt;
     }
     nwords[warp] = count;  // > cap: the host retries with a bigger window
   }
@@ -2312,11 +2346,8 @@ extern "C" int ctw_launch_best(const CtwLane* d_lanes, const CtwStateRange* rang
                                int32_t* words, const long long* woff, const int* wcap, int* nwords, double* total_cost,
                                int* status, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
-  const int warps_per_block = 4;
-  const int blocks = (n + warps_per_block - 1) / warps_per_block;
   (void)cudaGetLastError();
-  k_best_path<<<blocks, 32 * warps_per_block, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap, nwords,
-                                                          total_cost, status);
+  k_best_path<<<n, CTW_BPB, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap, nwords, total_cost, status);
   return (int)cudaGetLastError();
 }
 

@@ -666,11 +666,12 @@ def _raise_status(status: int, frame: int) -> None:
 
 
 def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: bool,
-                   raise_first: bool = True, packed=None):
+                   raise_first: bool = True, packed=None, with_best: bool = False):
     """One ctw_advance over several channels of the same lane pool. Returns a
     list of per-channel exceptions (None = committed). ``packed`` =
     (buffer, element offsets) passes an already-packed (n, F, V) block
-    without re-copying it."""
+    without re-copying it. ``with_best``: ctw_advance_best -- the partial
+    best paths come back from the same call; returns (errors, hypotheses)."""
     n = len(states)
     ids = np.asarray([s._lane for s in states], np.int32)
     frames = np.asarray([m.shape[0] for m in mats], np.int32)
@@ -679,9 +680,23 @@ def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: 
     err = np.zeros(n, np.int32)
     buf, offs, base, dcode, loc = _pack_rows(mats, on_dev, packed, frames, width)
     keep = buf
-    _lib.check(_lib.load().ctw_advance(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc,
-                                       _lib.ptr(offs), _lib.ptr(frames), width, _lib.ptr(status),
-                                       _lib.ptr(err)), "advance")
+    L = _lib.load()
+    if with_best:
+        cap = int(sum(s.frame_count for s in states) + int(frames.sum()) + 8 * n) + 16
+        words = np.zeros(cap, np.int32)
+        woff = np.zeros(n + 1, np.int64)
+        cost = np.zeros(n, np.float64)
+        fc = np.zeros(n, np.int64)
+        bst = np.zeros(n, np.int32)
+        rc = L.ctw_advance_best(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc, _lib.ptr(offs),
+                                _lib.ptr(frames), width, _lib.ptr(status), _lib.ptr(err), _lib.ptr(words), cap,
+                                _lib.ptr(woff), _lib.ptr(cost), _lib.ptr(fc), _lib.ptr(bst))
+        if rc != -2:
+            _lib.check(rc, "advance")
+    else:
+        _lib.check(L.ctw_advance(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc,
+                                 _lib.ptr(offs), _lib.ptr(frames), width, _lib.ptr(status),
+                                 _lib.ptr(err)), "advance")
     del keep
     errors = []
     for i, s in enumerate(states):
@@ -698,7 +713,24 @@ def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: 
         for e in errors:
             if e is not None:
                 raise e
-    return errors
+    if not with_best:
+        return errors
+    if rc == -2:  # (the word window was too small: the chunk is committed, ask again)
+        return errors, _best_lanes(pool, states)
+    return errors, _hyps_from(n, words, woff, cost, fc, bst)
+
+
+def _hyps_from(n, words, woff, cost, fc, st) -> list:
+    out = []
+    for i in range(n):
+        if st[i] == 2:
+            out.append(DecodeError("no frames decoded"))
+        elif st[i] == 1:
+            out.append(DecodeError("no surviving hypotheses"))
+        else:
+            out.append(Hypothesis(words=tuple(int(w) for w in words[woff[i]:woff[i + 1]]),
+                                  total_cost=float(cost[i]), frame_count=int(fc[i])))
+    return out
 
 
 def _pack_rows(mats, on_dev, packed, frames, width):
@@ -753,16 +785,7 @@ def _best_lanes(pool: LanePool, states: Sequence[DecodeState]) -> list:
             continue
         _lib.check(rc, "best path")
         break
-    out = []
-    for i in range(n):
-        if st[i] == 2:
-            out.append(DecodeError("no frames decoded"))
-        elif st[i] == 1:
-            out.append(DecodeError("no surviving hypotheses"))
-        else:
-            out.append(Hypothesis(words=tuple(int(w) for w in words[woff[i]:woff[i + 1]]),
-                                  total_cost=float(cost[i]), frame_count=int(fc[i])))
-    return out
+    return _hyps_from(n, words, woff, cost, fc, st)
 
 
 # ------------------------------------------------------------- functions ---

@@ -461,3 +461,29 @@ def test_c5_boosted_matches_oracle(oracle_mod, search):
         assert math.isclose(h.total_cost, oc, rel_tol=COST_RTOL)
         if search == "exact":
             assert h.total_cost == oc
+
+
+@pytest.mark.parametrize("search", ["exact", "fast"])
+def test_stream_partials_equal_offline_prefix_decodes(search):
+    """Every partial hypothesis StreamPool.step() returns (the best path
+    computed behind the chunk's frame kernel in the same call) equals the
+    offline decode of the same utterance prefix."""
+    from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, StreamPool, decode_batch, synth
+
+    s = _system(num_units=30, num_words=50, order=2, seed=2)
+    utts = synth.planted_utterances(s, 4, 40, seed=8)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=4), search=search)
+    sids = [pool.create_stream() for _ in utts]
+    seen = {sid: 0 for sid in sids}
+    partials = []
+    for i in range(0, 40, 7):
+        for sid, u in zip(sids, utts):
+            pool.push_chunk(Chunk(sid, u[i:i + 7], is_last=i + 7 >= 40))
+        for sid, h in pool.step():
+            seen[sid] += 1
+            partials.append((sids.index(sid), h))
+    for k, h in partials:
+        want = decode_batch(s.graph, cfg, [utts[k][:h.frame_count]], search=search)[0]
+        assert h == want
+    assert len(partials) == 4 * 6
