@@ -1990,9 +1990,6 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
       sm.tclk = t;
     }
 
-#ifdef CTW_EXTRA_SYNC  // experiment: the marginal cost of a cluster barrier per frame
-    for (int k = 0; k < CTW_EXTRA_SYNC; ++k) csync(sm);
-#endif
     // ---- reset every table entry this rank created (also on failure) ----
     reset_slots<FAST>(L, n_all);
     __syncthreads();
