@@ -34,7 +34,8 @@
 
 extern "C" int ctw_launch_decode(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                  const double*, const void*, int, int, const long long*, const int*,
-                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, int, int, int, cudaStream_t);
+                                 const int*, int, const CtwDecodeCfg*, CtwLaneOut*, int, int, int, int,
+                                 cudaStream_t);
 extern "C" int ctw_launch_seed(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                const double*, const int*, int, int, const CtwDecodeCfg*, CtwLaneOut*,
                                cudaStream_t);
@@ -1147,7 +1148,7 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
     l->fast_launches += fast;
     if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
                           l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, fast ? 1 : 0, (int)g->ebits,
-                          l->stream))
+                          g->eps_olabel ? 1 : 0, l->stream))
       return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
     CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
     l->launches++;

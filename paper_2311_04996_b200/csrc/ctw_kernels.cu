@@ -166,6 +166,7 @@ struct LaneCtx {
   // fast search mode (FastEnt table view of the same allocation, see below)
   ulonglong2* V;
   uint32_t tlog2, ebits;
+  bool eps_lab;  // some epsilon arc of the graph carries an output label
 };
 
 // ------------------------------------------------------ fast search mode --
@@ -911,7 +912,10 @@ struct WalkEnd {
 
 // One hop back along a winner chain from the value v: 0 = seed (no arc),
 // 1 = emitting arc `arc` from source `idx` (the chain ends), 2 = epsilon arc
-// `arc` (v becomes the predecessor's value).
+// `arc` (v becomes the predecessor's value). On a graph whose epsilon arcs
+// carry no output labels an epsilon hop needs no arc (CTW_NOARC): only the
+// predecessor's entry is loaded.
+#define CTW_NOARC 0xFFFFFFFFu
 template <bool FAST>
 __device__ __forceinline__ int hop_step(const LaneCtx& L, const GraphDev& g, const CtwSrc* src, ulonglong2& v,
                                         uint32_t& arc, uint32_t& idx) {
@@ -923,7 +927,8 @@ __device__ __forceinline__ int hop_step(const LaneCtx& L, const GraphDev& g, con
       return 1;
     }
     v = __ldcg(&L.V[win & L.mask]);
-    arc = __ldg(&g.ranges[(uint32_t)v.y & L.smask].eps_beg) + ((win & ~CTW_FEPS) >> L.tlog2);
+    arc = L.eps_lab ? __ldg(&g.ranges[(uint32_t)v.y & L.smask].eps_beg) + ((win & ~CTW_FEPS) >> L.tlog2)
+                    : CTW_NOARC;
     return 2;
   }
   const uint32_t tb = (uint32_t)v.y, aux = (uint32_t)(v.y >> 32);
@@ -933,6 +938,7 @@ __device__ __forceinline__ int hop_step(const LaneCtx& L, const GraphDev& g, con
     idx = aux;
     return 1;
   }
+  if (!L.eps_lab) arc = CTW_NOARC;
   v = __ldcg(reinterpret_cast<const ulonglong2*>(&L.T[aux & CTW_PRED_MASK]));
   return 2;
 }
@@ -947,7 +953,7 @@ __device__ __forceinline__ WalkEnd walk(const LaneCtx& L, const GraphDev& g, ulo
     uint32_t a = 0, idx = 0;
     const int k = hop_step<FAST>(L, g, src, v, a, idx);
     if (k == 0) return w;
-    const int32_t ol = g.olabel[a];
+    const int32_t ol = a == CTW_NOARC ? 0 : g.olabel[a];
     if (ol != 0) {
       ++w.n;
       w.last = ol;
@@ -992,7 +998,7 @@ __device__ int32_t record_code(Smem& sm, const LaneCtx& L, const GraphDev& g, co
     uint32_t a = 0, idx = 0;
     const int k = hop_step<FAST>(L, g, src, v, a, idx);
     if (k == 0) break;
-    const int32_t ol = g.olabel[a];
+    const int32_t ol = a == CTW_NOARC ? 0 : g.olabel[a];
     if (ol != 0) seg[pos--] = ol;
     if (k == 1) break;
   }
@@ -1117,6 +1123,7 @@ struct ChunkArgs {
   int width;
   int is_f64;
   int ebits;  // fast mode: bits of the emitting-arc offset in a winner word
+  int eps_lab; // some epsilon arc carries an output label
   CtwDecodeCfg cfg;
 };
 
@@ -1147,6 +1154,7 @@ __device__ __forceinline__ LaneCtx lane_ctx(const CtwLane& lane, int rank, int n
   L.V = reinterpret_cast<ulonglong2*>(lane.table);
   L.tlog2 = lane.tlog2;
   L.ebits = 0;
+  L.eps_lab = true;
   return L;
 }
 
@@ -1584,6 +1592,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   LaneCtx L = lane_ctx(lane, rank, R, G);
   L.tie_ctr = &sm.eps_ties;
   L.ebits = (uint32_t)a.ebits;
+  L.eps_lab = a.eps_lab != 0;
   const int F = a.nframes[b];
   const double* boost = lane.boost;
   const bool smem_ll = a.width <= CTW_MAX_SMEM_WIDTH;
@@ -2303,12 +2312,12 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
                                  const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
                                  int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
                                  const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast, int ebits,
-                                 cudaStream_t stream) {
+                                 int eps_lab, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
   void (*KFN)(CtwLane*, GraphDev, ChunkArgs, CtwLaneOut*) =
       fast ? (any_fsa ? k_decode_chunk<true, true> : k_decode_chunk<false, true>)
            : (any_fsa ? k_decode_chunk<true, false> : k_decode_chunk<false, false>);
-  ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, ebits, *cfg};
+  ChunkArgs a{loglik, ll_off, nframes, lane_ids, width, is_f64, ebits, eps_lab, *cfg};
   const size_t dyn = (width <= CTW_MAX_SMEM_WIDTH ? (size_t)width : 0) * sizeof(double);
   if (dyn + sizeof(Smem) > 48 * 1024)
     cudaFuncSetAttribute(KFN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
