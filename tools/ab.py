@@ -58,7 +58,7 @@ def child(args):
                       "cycles_per_lane_frame": sum(prof[k] for k in ("emit", "eps", "beam_count", "select",
                                                                     "records", "reset")) / (frames / 1),
                       "stage": {k: prof[k] / frames for k in ("emit", "eps", "beam_count", "select", "records", "r15",
-                                                              "reset")},
+                                                              "reset", "ties")},
                       "slots": prof["slots"] / frames, "eps_items": prof["eps_items"] / frames,
                       "digest": h.hexdigest()[:16]}))
 
