@@ -27,6 +27,8 @@
 #include <unordered_map>
 #include <unordered_set>
 #include <string>
+#include <atomic>
+#include <thread>
 #include <vector>
 
 #include "../../include/ctcwfst_b200.h"
@@ -1886,6 +1888,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
         CUDA_TRY(cudaMemcpyAsync(h.pool.data(), L.pool, h.pool.size() * 4, cudaMemcpyDeviceToHost, l->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(l->stream));
+    std::vector<int> done;
     for (int k = 0; k < m; ++k) {
       const int i = todo[k];
       const CtwLatEntry& e = ent[k];
@@ -1900,7 +1903,13 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
         again.push_back(i);
         continue;
       }
-      // ---- host copy of the kept lattice
+      done.push_back(k);
+    }
+    // ---- host copy of the kept lattices (canonical arc order, labels
+    // expanded): independent per lane, spread over host threads
+    auto post = [&](int k) {
+      const int i = todo[k];
+      const CtwLatEntry& e = ent[k];
       const int lane = lane_ids[i];
       const CtwLane& L = l->h[lane];
       ctw_lattice& o = out[i];
@@ -1977,6 +1986,18 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       }
       o.arc_lab = cmalloc<int32_t>(al.size());
       std::copy(al.begin(), al.end(), o.arc_lab);
+    };
+    const int nt = (int)std::min<size_t>(done.size(), std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (nt <= 1) {
+      for (int k : done) post(k);
+    } else {
+      std::atomic<size_t> next{0};
+      std::vector<std::thread> th;
+      for (int t = 0; t < nt; ++t)
+        th.emplace_back([&]() {
+          for (size_t j; (j = next.fetch_add(1)) < done.size();) post(done[j]);
+        });
+      for (auto& t : th) t.join();
     }
     todo.swap(again);
   }
