@@ -1176,22 +1176,33 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
       CtwLane& L = l->h[lane];
       l->max_slots = std::max<int64_t>(l->max_slots, o.n_slots_max);
       if (o.status >= CTW_GROW_TABLE && o.status <= CTW_GROW_SRC) l->h_grow[o.status - CTW_GROW_TABLE]++;
+      // a grow that cannot be satisfied (device memory, or the int32
+      // record range) fails this lane alone with CTW_ERR_OOM -- its chunk is
+      // not committed and the lane keeps its state -- while the other lanes
+      // of the launch go on (the reference's per-channel MemoryError)
+      int gr = 0;
       if (o.status == CTW_GROW_TABLE) {
-        if (int r = alloc_table(l, lane, L.tlog2 + 1)) return r;
-        again.push_back(lane);
+        gr = alloc_table(l, lane, L.tlog2 + 1);
       } else if (o.status == CTW_GROW_SRC) {
-        if (int r = alloc_table(l, lane, L.tlog2, std::max<int64_t>(o.rec_need, 2 * (int64_t)L.scap))) return r;
-        again.push_back(lane);
+        gr = alloc_table(l, lane, L.tlog2, std::max<int64_t>(o.rec_need, 2 * (int64_t)L.scap));
       } else if (o.status == CTW_GROW_HIST) {
         const int64_t per = (o.rec_need - L.n_rec) / std::max(1, o.err_frame + 1) + 1;
         const int64_t want = L.n_rec + (int64_t)(per * 1.5 * frames[i]) + 64;
-        if (int r = grow_hist(l, lane, o.rec_need > INT32_MAX ? o.rec_need
-                                                               : std::min<int64_t>(want, INT32_MAX)))
-          return r;
-        again.push_back(lane);
+        gr = grow_hist(l, lane, o.rec_need > INT32_MAX ? o.rec_need : std::min<int64_t>(want, INT32_MAX));
       } else if (o.status == CTW_GROW_POOL) {
-        if (int r = grow_pool(l, lane, 2 * (int64_t)L.pcap)) return r;
-        again.push_back(lane);
+        gr = grow_pool(l, lane, 2 * (int64_t)L.pcap);
+      }
+      if (o.status >= CTW_GROW_TABLE && o.status <= CTW_GROW_SRC) {
+        if (gr == 0) {
+          again.push_back(lane);
+        } else if (gr == -100 - (int)cudaErrorMemoryAllocation || gr == -1 || gr == -3) {
+          (void)cudaGetLastError();
+          status[i] = CTW_ERR_OOM;
+          err_frame[i] = 0;
+        } else {
+          return gr;
+        }
+        continue;
       } else {
         const int64_t before = L.n_rec;
         update_from_out(L, o);
