@@ -303,7 +303,8 @@ def test_bench_scale_history_matches_oracle(oracle_mod):
         assert (h.words, h.total_cost, h.frame_count) == oc.best_path()
 
 
-def test_history_compaction_keeps_best_paths():
+@pytest.mark.parametrize("search", ["exact", "fast"])
+def test_history_compaction_keeps_best_paths(search):
     """Partial-history garbage collection (ctw_lane_compact): offline and
     streamed best paths, partial hypotheses and final hypotheses unchanged;
     history shrinks."""
@@ -313,7 +314,7 @@ def test_history_compaction_keeps_best_paths():
     utts = synth.planted_utterances(s, 4, 80, seed=8, gap=4.0, noise=1.0)
     cfg = DecoderConfig(beam=14.0, max_active=500)
     for u in utts:
-        a, b = DecodeState(s.graph, cfg), DecodeState(s.graph, cfg)
+        a, b = DecodeState(s.graph, cfg, search=search), DecodeState(s.graph, cfg, search=search)
         for i in range(0, len(u), 10):
             a.advance_frames(u[i:i + 10])
             b.advance_frames(u[i:i + 10])
@@ -325,7 +326,7 @@ def test_history_compaction_keeps_best_paths():
     # streams with collection every 2 chunks == streams without
     finals = []
     for gc in (None, 2):
-        pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=3), gc_every=gc)
+        pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=3), gc_every=gc, search=search)
         sids = [pool.create_stream() for _ in utts]
         partial = []
         for sid, u in zip(sids, utts):

@@ -79,9 +79,12 @@ SPECS = [
 ]
 
 
+@pytest.mark.parametrize("search", ["exact", "fast"])
 @pytest.mark.parametrize("k", range(len(SPECS)))
 @pytest.mark.parametrize("beam", [0.0, 3.0, 8.0])
-def test_lattice_matches_oracle(k, beam):
+def test_lattice_matches_oracle(k, beam, search):
+    """(The fast mode keeps the same survivors with the same costs, so its
+    lattice is the same lattice.)"""
     import lattice_oracle as lo
 
     from paper_2311_04996_b200 import DecoderConfig, decode_lattices, synth
@@ -89,7 +92,7 @@ def test_lattice_matches_oracle(k, beam):
     s = _system(**SPECS[k])
     frames = synth.planted_utterances(s, 1, 30, seed=10 + k, gap=3.0, noise=1.0)[0]
     cfg = DecoderConfig(beam=14.0, max_active=400)
-    lat = decode_lattices(s.graph, cfg, [frames], lattice_beam=beam)[0]
+    lat = decode_lattices(s.graph, cfg, [frames], lattice_beam=beam, search=search)[0]
     ora, seeds, (ow, oc, _) = _oracle_lattice(s, cfg, frames, beam)
     assert lat.status == 0
     # the lattice's best complete path is the decoder's best path
