@@ -2057,6 +2057,7 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
   }
 }
 
+#ifndef CTW_WIDE  // (the wide translation unit carries only the frame kernel)
 // ------------------------------------------------------------ seeding ----
 
 // Fresh channel: token at the start state plus its epsilon closure
@@ -2280,39 +2281,19 @@ __global__ void k_clear_table(CtwTok* T, uint32_t n) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) tok_clear(&T[i]);
 }
+#endif  // CTW_WIDE
 
 }  // namespace
 
 // ------------------------------------------------------ launch wrappers ---
 
-// Ranks (CTAs) per lane for a launch of n lanes: CTW_CLUSTER overrides.
-// Otherwise 8 (best throughput when lanes fill the GPU: 71 clusters
-// resident), or 16 when even 16-CTA clusters leave SMs idle -- small
-// streaming steps, where per-lane latency is the metric (a 16-CTA lane runs
-// a frame in ~0.67 M cycles vs ~1.3 M with 8).
-static int cluster_size(int n) {
-  static int env = -1;
-  if (env < 0) {
-    const char* s = getenv("CTW_CLUSTER");
-    env = s ? atoi(s) : 0;
-    if (env < 0 || env > CTW_RMAX) env = 0;
-  }
-  if (env) return env;
-  static int resident = 0;  // CTAs resident on the device
-  if (!resident) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident = sms * CTW_MINB;
-  }
-  return (long long)n * 16 <= resident ? 16 : CTW_DEFAULT_CLUSTER;
-}
-
-extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
-                                 const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
-                                 int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
-                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast, int ebits,
-                                 int eps_lab, cudaStream_t stream) {
+// The frame kernel over n lanes with R CTAs (ranks) per lane, CTW_BS
+// threads per CTA (this translation unit's block size).
+static int launch_decode_r(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                           const int32_t* olabel, const double* final_w, const void* loglik, int is_f64, int width,
+                           const long long* ll_off, const int* nframes, const int* lane_ids, int n,
+                           const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast, int ebits, int eps_lab,
+                           cudaStream_t stream, int R) {
   GraphDev g{ranges, arcs, olabel, final_w};
   void (*KFN)(CtwLane*, GraphDev, ChunkArgs, CtwLaneOut*) =
       fast ? (any_fsa ? k_decode_chunk<true, true> : k_decode_chunk<false, true>)
@@ -2322,7 +2303,6 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
   if (dyn + sizeof(Smem) > 48 * 1024)
     cudaFuncSetAttribute(KFN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   (void)cudaGetLastError();  // drop stale errors of unchecked calls
-  const int R = cluster_size(n);
   if (R > 8) cudaFuncSetAttribute(KFN, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(n * R));
@@ -2339,6 +2319,58 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
   cudaError_t e = cudaLaunchKernelEx(&lc, KFN, d_lanes, g, a, out);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
+}
+
+#ifdef CTW_WIDE
+// 1024-thread CTAs, 16 per lane: twice the threads of a 512 x 16 lane, for
+// launches too small to fill the GPU (streaming steps: per-lane latency)
+extern "C" int ctw_launch_decode_wide(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                                      const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
+                                      int width, const long long* ll_off, const int* nframes, const int* lane_ids,
+                                      int n, const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast,
+                                      int ebits, int eps_lab, cudaStream_t stream) {
+  return launch_decode_r(d_lanes, ranges, arcs, olabel, final_w, loglik, is_f64, width, ll_off, nframes, lane_ids, n,
+                         cfg, out, any_fsa, fast, ebits, eps_lab, stream, 16);
+}
+#else
+extern "C" int ctw_launch_decode_wide(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
+                                      const void*, int, int, const long long*, const int*, const int*, int,
+                                      const CtwDecodeCfg*, CtwLaneOut*, int, int, int, int, cudaStream_t);
+
+// Ranks (CTAs) per lane for a launch of n lanes: CTW_CLUSTER overrides.
+// Otherwise 8 x 512 threads (best throughput when lanes fill the GPU: 74
+// clusters resident); launches too small to fill the GPU -- streaming steps,
+// where per-lane latency is the metric -- take 16 CTAs per lane, of 1024
+// threads while 16 x 1024-thread clusters still fit (C4: p50 2.79 -> 2.30 ms,
+// p99 4.13 -> 3.34 ms against 512-thread CTAs), else of 512.
+extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+                                 const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
+                                 int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
+                                 const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast, int ebits,
+                                 int eps_lab, cudaStream_t stream) {
+  static int env = -1;
+  if (env < 0) {
+    const char* s = getenv("CTW_CLUSTER");
+    env = s ? atoi(s) : 0;
+    if (env < 0 || env > CTW_RMAX) env = 0;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int R = CTW_DEFAULT_CLUSTER;
+  if (env) {
+    R = env;
+  } else if ((long long)n * 16 <= (long long)sms * (2048 / 1024) && !getenv("CTW_NO_WIDE")) {
+    return ctw_launch_decode_wide(d_lanes, ranges, arcs, olabel, final_w, loglik, is_f64, width, ll_off, nframes,
+                                  lane_ids, n, cfg, out, any_fsa, fast, ebits, eps_lab, stream);
+  } else if ((long long)n * 16 <= (long long)sms * CTW_MINB) {
+    R = 16;
+  }
+  return launch_decode_r(d_lanes, ranges, arcs, olabel, final_w, loglik, is_f64, width, ll_off, nframes, lane_ids, n,
+                         cfg, out, any_fsa, fast, ebits, eps_lab, stream, R);
 }
 
 extern "C" int ctw_launch_seed(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
@@ -2365,3 +2397,4 @@ extern "C" int ctw_launch_clear(CtwTok* T, uint32_t n, cudaStream_t stream) {
   k_clear_table<<<(n + 255) / 256, 256, 0, stream>>>(T, n);
   return (int)cudaGetLastError();
 }
+#endif  // CTW_WIDE
