@@ -38,7 +38,9 @@ for name in (golden_names()[:2] + ["kat_eps_olabels"] if QUICK else golden_names
             n_ok += 1
 print("goldens with matching words:", n_ok)
 
-os.environ["CTW_CLUSTER"] = "8"
+# launch shapes: a 2-lane launch runs the wide kernel (1024-thread CTAs, 16
+# per lane); a 40-lane launch the full-batch shape (512-thread CTAs, 8 per
+# lane); lattices on 8-CTA clusters
 os.environ["CTW_LAT_RANKS"] = "8"
 s = synth.build_system(synth.SystemSpec(num_units=129, blank_id=128, num_words=200, order=3, seed=5, min_pron=1,
                                         max_pron=4, followers=12))
@@ -46,6 +48,8 @@ utts = list(synth.conformer_logprobs(s, 2, 8 if QUICK else 30, seed=1, delta=5.0
 cfg = DecoderConfig(beam=14.0, max_active=300)
 for search in ("exact", "fast"):
     print(search, [h.words[:5] for h in decode_batch(s.graph, cfg, utts, search=search)])
+    many = list(synth.conformer_logprobs(s, 40, 6, seed=2, delta=5.0, sigma=1.5, dtype=np.float32))
+    print(search, "40 lanes:", sum(len(h.words) for h in decode_batch(s.graph, cfg, many, search=search)))
 if QUICK:
     sys.exit(0)
 lats = decode_lattices(s.graph, cfg, utts, lattice_beam=4.0)
