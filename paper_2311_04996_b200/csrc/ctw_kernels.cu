@@ -1923,19 +1923,15 @@ __global__ void __launch_bounds__(CTW_BS, CTW_MINB) k_decode_chunk(CtwLane* lane
         // one cluster counter for the rank's base, then independent
         // per-survivor writes (record order inside a frame is free: the
         // export orders by state) ----
-        const bool radix = select && sm.l_radix;
-        const int bsel = select ? sm.l_bin : CTW_NB;
-        const unsigned long long tk = sm.l_tk;
-        const uint32_t ts = sm.l_ts;
-        const int depth = sm.l_depth;
-        const unsigned long long ph = sm.l_ph;
-        const uint32_t pl = sm.l_pl;
+        // the select result is read from shared memory where it is used: held
+        // in registers it would stay live across the whole survivor loop
         auto keep = [&](unsigned long long key, uint32_t state) -> bool {
           if (key > cut_key) return false;
           if (!select) return true;
-          if (radix) return cmp_prefix(key, state, depth, ph, pl) <= 0;
+          if (sm.l_radix) return cmp_prefix(key, state, sm.l_depth, sm.l_ph, sm.l_pl) <= 0;
           const int bb = cost_bin(key, min_cost, bin_scale);
-          return bb < bsel || (bb == bsel && (key < tk || (key == tk && state <= ts)));
+          const unsigned long long tk = sm.l_tk;
+          return bb < sm.l_bin || (bb == sm.l_bin && (key < tk || (key == tk && state <= sm.l_ts)));
         };
         int mine = 0;
         for (int i = L.sw0 + tid; i < n_ib; i += L.swstride) mine += keep(sv[i].x, ib[i].y);
