@@ -106,8 +106,8 @@ def main():
                  "k_decode_chunk launches are 512 lanes x 250 frames; short decode launches are first-call grow re-runs")
     (PROF / f"{tag}_launches.json").write_text(json.dumps(L, indent=1))
     F = full(rep)
-    F["command"] = ("ncu --set full --clock-control none --import-source on -k regex:k_decode_chunk -s 4 -c 1 "
-                    "python bench.py --search " + search + " --batch 512 --frames 80 --steps 1 --warmup 4 --no-cpu "
+    F["command"] = ("ncu --set full --clock-control none --import-source on -k regex:k_decode_chunk -s 6 -c 1 "
+                    "python bench.py --search " + search + " --batch 512 --frames 80 --steps 1 --warmup 8 --no-cpu "
                     "--streams 0 --lattice 0")
     (PROF / f"{tag}_full_metrics.json").write_text(json.dumps(F, indent=1))
     ss = L["steady_state_decode"]
