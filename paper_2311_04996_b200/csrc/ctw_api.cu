@@ -49,7 +49,10 @@ extern "C" int ctw_launch_hist_mark(const CtwLane*, const int*, uint32_t* const*
 extern "C" int ctw_launch_hist_compact(CtwLane*, const int*, uint32_t* const*, int32_t* const*,
                                        CtwRecPage* const* const*, long long*, int, cudaStream_t);
 extern "C" int ctw_launch_lattice(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
-                                  CtwLatEntry*, int, const void*, int, int, double, double, int, int, cudaStream_t);
+                                  const uint32_t*, const CtwClo*, CtwLatEntry*, int, const void*, int, int, double,
+                                  double, int, int, cudaStream_t);
+extern "C" int ctw_build_closure_index(const CtwStateRange*, const CtwArc*, long long, uint32_t**, CtwClo**,
+                                       long long*, cudaStream_t);
 
 namespace {
 
@@ -122,6 +125,13 @@ struct ctw_graph {
   int32_t* olabel = nullptr;
   double* final_w = nullptr;
   std::vector<double> h_final;
+  // epsilon-closure index of the lattice kernel (ctw_lattice.cu), built on
+  // the first lattice request when no epsilon arc carries an output label
+  std::mutex clo_mu;
+  int clo_state = 0;  // 0 not built, 1 built, -1 not available
+  uint32_t* clo_off = nullptr;
+  CtwClo* clo_ent = nullptr;
+  long long clo_n = 0;
 };
 
 // ------------------------------------------------------------------ lanes --
@@ -706,6 +716,8 @@ void ctw_graph_destroy(ctw_graph* g) {
   dfree(g->arcs);
   dfree(g->olabel);
   dfree(g->final_w);
+  dfree(g->clo_off);
+  dfree(g->clo_ent);
   delete g;
 }
 
@@ -716,6 +728,7 @@ int ctw_graph_info(const ctw_graph* g, int64_t* num_states, int64_t* num_arcs, i
   if (max_ilabel) *max_ilabel = g->max_il;
   if (max_olabel) *max_olabel = g->max_ol;
   if (bytes) *bytes = g->S * (int64_t)(sizeof(CtwStateRange) + sizeof(double)) + g->A * (int64_t)(sizeof(CtwArc) + 4);
+  if (bytes && g->clo_state == 1) *bytes += (g->S + 1) * 4 + g->clo_n * (int64_t)sizeof(CtwClo);
   return 0;
 }
 
@@ -1784,6 +1797,18 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
     arc_cap[i] = 4096 + 256 * frames[i];  // ~40 kept arcs per frame at lattice beam 6 on C2
     lab_cap[i] = 4 * arc_cap[i];
   }
+  // closure index (once per graph; CTW_LAT_NOPRE=1 runs the general kernel)
+  const bool pre_env = getenv("CTW_LAT_NOPRE") == nullptr;
+  if (pre_env && !g->eps_olabel) {
+    std::lock_guard<std::mutex> gl(g->clo_mu);
+    if (g->clo_state == 0) {
+      const int rc = ctw_build_closure_index(g->ranges, g->arcs, g->S, &g->clo_off, &g->clo_ent, &g->clo_n,
+                                             l->stream);
+      if (rc > 0) return fail(-100 - rc, std::string("closure index: ") + cudaGetErrorString((cudaError_t)rc));
+      g->clo_state = rc == 0 ? 1 : -1;
+    }
+  }
+  const bool pre = pre_env && g->clo_state == 1;
   CtwLatEntry* d_ent = nullptr;
   CUDA_TRY(salloc(&d_ent, (size_t)n, l->stream));
   std::vector<int> todo(n);
@@ -1856,8 +1881,9 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       if (any_big) ranks = 1;
       if (const char* e = getenv("CTW_LAT_RANKS")) ranks = std::max(1, std::min(8, atoi(e)));  // diagnostics
     }
-    if (ctw_launch_lattice(l->d, g->ranges, g->arcs, g->olabel, g->final_w, d_ent, m, dev_ll, dtype, width,
-                           l->cfg.acoustic_scale, lattice_beam, ranks, any_big ? 1 : 0, l->stream)) {
+    if (ctw_launch_lattice(l->d, g->ranges, g->arcs, g->olabel, g->final_w, pre ? g->clo_off : nullptr,
+                           pre ? g->clo_ent : nullptr, d_ent, m, dev_ll, dtype, width, l->cfg.acoustic_scale,
+                           lattice_beam, ranks, any_big ? 1 : 0, l->stream)) {
       release();
       return fail(-1, std::string("lattice launch: ") + cudaGetErrorString(cudaGetLastError()));
     }

@@ -186,6 +186,18 @@ struct CtwLatArc {
   int32_t src_state;
 };
 
+// Epsilon-closure index entry (lattice kernel): for every state s, the
+// states reachable from s over epsilon arcs (s itself first) with the
+// minimum path weight from s. Built on the device once per graph when no
+// epsilon arc carries an output label (then the closure is the same for
+// every lane, boost and phrase automaton).
+struct __align__(16) CtwClo {
+  double w;
+  uint32_t state;
+  uint32_t pad;
+};
+#define CTW_CLO_NONE 0x80000000u  // flag in the offset word: closure not indexed (too large)
+
 // Per batch entry (lane) arguments and outputs, device pointers.
 struct CtwLatEntry {
   int32_t lane;

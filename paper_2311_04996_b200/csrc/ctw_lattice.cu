@@ -26,11 +26,24 @@
 // item that runs its own small epsilon closure, and kept arcs are appended to
 // the lane's arc buffer. A closure that outgrows its local capacity marks
 // the lane (status 3) and the host re-runs it with the large instantiation.
+//
+// When no epsilon arc carries an output label (C2, C3), the closures do not
+// depend on the lane (boosts and phrase automata only act on labelled arcs):
+// they are computed once per graph into an index (k_closure_index: per state
+// the epsilon-reachable states and their minimum path weight), and the work
+// item of the indexed kernel (PRE) reads its closure as one contiguous run of
+// 16-byte entries and probes a shared-memory copy of the layer's destination
+// map -- no per-thread closure arrays, no local memory, ~4 dependent memory
+// round trips per item instead of ~50. Arc weights are then c0 + (w1 + w2 +
+// ...) instead of ((c0 + w1) + w2) + ...: equal up to rounding (DESIGN.md
+// "Lattice").
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
 #include <stdint.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "ctw_common.h"
@@ -42,6 +55,9 @@
 #define LAT_QL 128      // local relaxation budget per work item
 #define LAT_CL_BIG 256  // ... of the re-run for items that overflowed
 #define LAT_QL_BIG 1024
+#define LAT_MAP 1024        // shared-memory destination map slots (<= LAT_MAP / 2 entries)
+#define CLO_CAP 64          // closure index: largest indexed closure
+#define CLO_QCAP 256        // ... and its relaxation budget
 
 namespace {
 
@@ -91,6 +107,8 @@ namespace {
 struct LatArgs {
   CtwLane* lanes;
   LatGraph g;
+  const uint32_t* clo_off;  // closure index (PRE kernel): per state offset | CTW_CLO_NONE
+  const CtwClo* clo_ent;
   CtwLatEntry* ent;
   const void* loglik;
   int width;
@@ -150,7 +168,27 @@ struct __align__(16) LatSmem {
   unsigned long long mb_all;    // cluster-wide minimum
   unsigned long long best;
   unsigned long long items, pruned;
+  int map_tot;            // destination-map entries over all ranks
+  int nput_r[8];          // ... per rank
 };
+
+// Shared-memory copy of the layer's destination map (PRE kernel): state ->
+// node and the node's beta, open addressing over LAT_MAP slots.
+struct LatMapSm {
+  uint32_t st[LAT_MAP];
+  int32_t node[LAT_MAP];
+  unsigned long long beta[LAT_MAP];
+};
+
+__device__ __forceinline__ int map_find(const LatMapSm& mp, uint32_t s) {
+  uint32_t h = lat_hash(s, 32 - 10) & (LAT_MAP - 1);
+  for (;;) {
+    const uint32_t k = mp.st[h];
+    if (k == s) return (int)h;
+    if (k == CTW_EMPTY) return -1;
+    h = (h + 1) & (LAT_MAP - 1);
+  }
+}
 
 #ifndef LAT_MINB
 #define LAT_MINB 4  // 4 CTAs (64 warps) per SM: every lane of a 512-lane batch resident (61 -> 32 registers; lattice stage -32 %)
@@ -276,13 +314,82 @@ __device__ __forceinline__ void lat_item(const LatArgs& a, CtwLatEntry& E, const
   }
 }
 
+// Work item of the indexed kernel: the closure of nextstate(e) comes from
+// the graph's closure index, destinations from the shared-memory map (or
+// the lane table when the layer's map is too large for it).
+__device__ __forceinline__ void lat_item_pre(const LatArgs& a, CtwLatEntry& E, const CtwLane& lane, LatSmem& sm,
+                                             const LatMapSm& mp, bool map_ok, uint32_t shift, uint32_t mask,
+                                             bool cut_ok, double cutoff, double min_beta, int32_t sst, double sc,
+                                             int node, int f, uint32_t ai, long long row0) {
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const CtwArc arc = a.g.arcs[ai];
+  double x;
+  {
+    const long long idx = row0 + arc.ilabel - 1;
+    x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+  }
+  double c0 = __dadd_rn(__dmul_rn(-a.acoustic_scale, x), arc.weight);
+  const int32_t ol0 = a.g.olabel[ai];
+  const uint32_t x0 = lat_dest(lane, (uint32_t)sst, ol0, (uint32_t)arc.nextstate, c0);
+  if (!(c0 < INF)) return;
+  if (cut_ok && sc + c0 + min_beta > cutoff) {
+    atomicAdd(&sm.pruned, 1ULL);
+    return;
+  }
+  atomicAdd(&sm.items, 1ULL);
+  const uint32_t s0 = x0 & lane.smask, hi = x0 & ~lane.smask;
+  const uint32_t ob = __ldg(&a.clo_off[s0]);
+  if (ob & CTW_CLO_NONE) {  // closure too large for the index: the host re-runs the lane
+    atomicMax(&E.status, 3);
+    return;
+  }
+  const uint32_t oe = __ldg(&a.clo_off[s0 + 1]) & ~CTW_CLO_NONE;
+  for (uint32_t k = ob; k < oe; ++k) {
+    const ulonglong2 ce = __ldg(reinterpret_cast<const ulonglong2*>(a.clo_ent + k));  // {w, state}
+    const double c = __dadd_rn(c0, __longlong_as_double((long long)ce.x));
+    if (!(c < INF)) continue;
+    if (cut_ok && sc + c + min_beta > cutoff) continue;
+    const uint32_t key = (uint32_t)ce.y | hi;
+    int dn;
+    double bd;
+    if (map_ok) {
+      const int slot = map_find(mp, key);
+      if (slot < 0) continue;
+      dn = mp.node[slot];
+      bd = lat_key2d(mp.beta[slot]);
+    } else {
+      dn = lat_get(lane, shift, mask, key);
+      if (dn < 0) continue;
+      bd = lat_key2d(__ldcg(&E.beta[dn]));
+    }
+    const double tail = __dadd_rn(c, bd);
+    atomicMin(&E.beta[node], lat_d2key(tail));
+    if (__dadd_rn(sc, tail) > cutoff) continue;
+    const int ia = atomicAdd(&E.n_arcs, 1);
+    if (ia >= E.arc_cap) {
+      atomicMax(&E.status, 1);
+      continue;
+    }
+    CtwLatArc la;
+    la.src = node;
+    la.dst = dn;
+    la.w = c;
+    la.code = ol0;
+    la.frame = f;
+    la.dst_state = (int32_t)key;
+    la.src_state = sst;
+    E.arcs[ia] = la;
+  }
+}
+
 // One thread-block cluster of R CTAs ("ranks") per lane: the ranks split
 // every layer's destination records and source tiles and meet at cluster
 // barriers between the steps of a layer; counters live in the entry (global
 // atomics), the layer's minimum beta is exchanged through shared memory.
-template <int CL, int QL>
+template <int CL, int QL, bool PRE>
 __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
   __shared__ LatSmem sm;
+  __shared__ typename std::conditional<PRE, LatMapSm, char>::type mp_;
   cg::cluster_group cl = cg::this_cluster();
   const int R = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const int tid = threadIdx.x;
@@ -344,6 +451,8 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
       sm.nput = 0;
       sm.ac_min = ~0ULL;
     }
+    if constexpr (PRE)
+      for (int i = tid; i < LAT_MAP; i += LAT_BS) mp_.st[i] = CTW_EMPTY;
     __syncthreads();
     {
       // smallest acoustic term of the frame (source-level pruning bound)
@@ -373,14 +482,39 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
     cl.sync();  // the whole layer is in the map; every rank's minimum published
     if (tid < 32) {
       unsigned long long m = tid < R ? cl.map_shared_rank(&sm, tid)->mb_pub : ~0ULL;
+      int np = tid < R ? min(cl.map_shared_rank(&sm, tid)->nput, pcap) : 0;
+      if (tid < 8) sm.nput_r[tid] = np;
       for (int d = 16; d; d >>= 1) {
         const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, m, d);
         if (o < m) m = o;
+        np += __shfl_xor_sync(0xFFFFFFFFu, np, d);
       }
-      if (tid == 0) sm.mb_all = m;
+      if (tid == 0) {
+        sm.mb_all = m;
+        sm.map_tot = np;
+      }
     }
     __syncthreads();
     const double min_beta = sm.mb_all == ~0ULL ? INF : lat_key2d(sm.mb_all);
+    // PRE: every rank copies the whole layer map (all ranks' lists) into its
+    // shared memory, with the nodes' beta (final since the previous layer)
+    const bool map_ok = PRE && sm.map_tot <= LAT_MAP / 2;
+    if constexpr (PRE) {
+      if (map_ok && min_beta != INF) {
+        for (int r = 0; r < R; ++r) {
+          const uint2* pl = lane.front + (size_t)r * pcap;
+          for (int i = tid; i < sm.nput_r[r]; i += LAT_BS) {
+            const uint2 e = __ldcg(&pl[i]);
+            const int32_t nd = (int32_t)__ldcg(&lane.table[e.x].tb);
+            uint32_t h = lat_hash(e.y, 32 - 10) & (LAT_MAP - 1);
+            while (atomicCAS(&mp_.st[h], CTW_EMPTY, e.y) != CTW_EMPTY) h = (h + 1) & (LAT_MAP - 1);
+            mp_.node[h] = nd;
+            mp_.beta[h] = __ldcg(&E.beta[nd]);
+          }
+        }
+      }
+      __syncthreads();
+    }
     // ---- sources: layer f-1 (records) or the seeds, tiles split over the ranks
     const long long s0 = f > 0 ? lane.frame_base[f - 1] : 0;
     const long long s1 = f > 0 ? d0 : S0;
@@ -424,8 +558,12 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
             if (sm.off[mid] <= item) lo = mid;
             else hi = mid - 1;
           }
-          lat_item<CL, QL>(a, E, lane, sm, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo], sm.node[lo],
-                           f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
+          if constexpr (PRE)
+            lat_item_pre(a, E, lane, sm, mp_, map_ok, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo],
+                         sm.node[lo], f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
+          else
+            lat_item<CL, QL>(a, E, lane, sm, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo],
+                             sm.node[lo], f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
         }
         __syncthreads();  // the tile's smem is reused by the next tile
       }
@@ -454,12 +592,15 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
 }  // namespace
 
 extern "C" int ctw_launch_lattice(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
-                                  const int32_t* olabel, const double* final_w, CtwLatEntry* d_ent, int n,
-                                  const void* loglik, int is_f64, int width, double acoustic_scale,
-                                  double lattice_beam, int ranks, int big, cudaStream_t stream) {
-  LatArgs a{d_lanes, LatGraph{ranges, arcs, olabel, final_w}, d_ent, loglik, width, is_f64, acoustic_scale,
-            lattice_beam};
-  void (*KFN)(LatArgs) = big ? k_lattice<LAT_CL_BIG, LAT_QL_BIG> : k_lattice<LAT_CL, LAT_QL>;
+                                  const int32_t* olabel, const double* final_w, const uint32_t* clo_off,
+                                  const CtwClo* clo_ent, CtwLatEntry* d_ent, int n, const void* loglik, int is_f64,
+                                  int width, double acoustic_scale, double lattice_beam, int ranks, int big,
+                                  cudaStream_t stream) {
+  LatArgs a{d_lanes, LatGraph{ranges, arcs, olabel, final_w}, clo_off, clo_ent, d_ent, loglik, width, is_f64,
+            acoustic_scale, lattice_beam};
+  void (*KFN)(LatArgs) = big       ? k_lattice<LAT_CL_BIG, LAT_QL_BIG, false>
+                         : clo_off ? k_lattice<1, 1, true>
+                                   : k_lattice<LAT_CL, LAT_QL, false>;
   (void)cudaGetLastError();
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(n * ranks));
@@ -475,4 +616,127 @@ extern "C" int ctw_launch_lattice(CtwLane* d_lanes, const CtwStateRange* ranges,
   cudaError_t e = cudaLaunchKernelEx(&lc, KFN, a);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------- closure index --
+
+namespace {
+
+// One thread per state: its epsilon closure (label-correcting, minimum path
+// weight from the state; the state itself first with weight 0). Pass 0
+// counts (0 = too large to index), pass 1 writes the entries.
+template <bool WRITE>
+__global__ void __launch_bounds__(128) k_closure_index(const CtwStateRange* ranges, const CtwArc* arcs, long long S,
+                                                       unsigned long long* cnt, const uint32_t* off, CtwClo* ent) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (WRITE && (off[s] & CTW_CLO_NONE)) return;
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  uint32_t cst[CLO_CAP];
+  double cw[CLO_CAP];
+  uint8_t q[CLO_QCAP];
+  int n = 1, qh = 0, qt = 1;
+  cst[0] = (uint32_t)s;
+  cw[0] = 0.0;
+  q[0] = 0;
+  bool ovf = false;
+  while (qh < qt && !ovf) {
+    const int u = q[qh++];
+    const CtwStateRange ru = ranges[cst[u]];
+    for (uint32_t b = ru.eps_beg; b < ru.emit_beg; ++b) {
+      const CtwArc ea = arcs[b];
+      const double cy = __dadd_rn(cw[u], ea.weight);
+      if (!(cy < INF)) continue;
+      int j = 0;
+      while (j < n && cst[j] != (uint32_t)ea.nextstate) ++j;
+      if (j < n) {
+        if (!(cy < cw[j])) continue;
+      } else {
+        if (n == CLO_CAP) {
+          ovf = true;
+          break;
+        }
+        ++n;
+        cst[j] = (uint32_t)ea.nextstate;
+      }
+      cw[j] = cy;
+      if (qt == CLO_QCAP) {
+        ovf = true;
+        break;
+      }
+      q[qt++] = (uint8_t)j;
+    }
+  }
+  if (!WRITE) {
+    cnt[s] = ovf ? 0ULL : (unsigned long long)n;
+    return;
+  }
+  CtwClo* o = ent + (off[s] & ~CTW_CLO_NONE);
+  for (int j = 0; j < n; ++j) {
+    CtwClo e;
+    e.w = cw[j];
+    e.state = cst[j];
+    e.pad = 0;
+    o[j] = e;
+  }
+}
+
+__global__ void k_closure_mark(const unsigned long long* cnt, const unsigned long long* off64, long long S,
+                               uint32_t* off) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s > S) return;
+  off[s] = (uint32_t)off64[s] | ((s < S && cnt[s] == 0) ? CTW_CLO_NONE : 0u);
+}
+
+}  // namespace
+
+// Build the closure index of a graph (S states). Returns 0 and device
+// arrays *off (S + 1 words) / *ent, or a CUDA error / -1 when the index
+// would exceed 2^31 entries (the caller then runs the general kernel).
+extern "C" int ctw_build_closure_index(const CtwStateRange* ranges, const CtwArc* arcs, long long S,
+                                       uint32_t** off_out, CtwClo** ent_out, long long* n_out,
+                                       cudaStream_t stream) {
+  *off_out = nullptr;
+  *ent_out = nullptr;
+  *n_out = 0;
+  unsigned long long *cnt = nullptr, *off64 = nullptr;
+  uint32_t* off = nullptr;
+  CtwClo* ent = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  unsigned long long total = 0;
+  int rc = 0;
+  const unsigned blocks = (unsigned)((S + 128) / 128);
+  auto done = [&](int r) {
+    cudaFree(cnt);
+    cudaFree(off64);
+    cudaFree(tmp);
+    if (r) {
+      cudaFree(off);
+      cudaFree(ent);
+    }
+    return r;
+  };
+  if ((rc = cudaMalloc(&cnt, (S + 1) * 8)) || (rc = cudaMalloc(&off64, (S + 1) * 8)) ||
+      (rc = cudaMalloc(&off, (S + 1) * 4)))
+    return done(rc);
+  if ((rc = cudaMemsetAsync(cnt + S, 0, 8, stream))) return done(rc);
+  k_closure_index<false><<<blocks, 128, 0, stream>>>(ranges, arcs, S, cnt, nullptr, nullptr);
+  if ((rc = cudaGetLastError())) return done(rc);
+  if ((rc = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off64, S + 1, stream))) return done(rc);
+  if ((rc = cudaMalloc(&tmp, tmp_bytes))) return done(rc);
+  if ((rc = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off64, S + 1, stream))) return done(rc);
+  if ((rc = cudaMemcpyAsync(&total, off64 + S, 8, cudaMemcpyDeviceToHost, stream))) return done(rc);
+  if ((rc = cudaStreamSynchronize(stream))) return done(rc);
+  if (total >= (1ULL << 31)) return done(-1);
+  k_closure_mark<<<(unsigned)((S + 256) / 256), 256, 0, stream>>>(cnt, off64, S, off);
+  if ((rc = cudaGetLastError())) return done(rc);
+  if ((rc = cudaMalloc(&ent, std::max<unsigned long long>(total, 1) * sizeof(CtwClo)))) return done(rc);
+  k_closure_index<true><<<blocks, 128, 0, stream>>>(ranges, arcs, S, nullptr, off, ent);
+  if ((rc = cudaGetLastError())) return done(rc);
+  if ((rc = cudaStreamSynchronize(stream))) return done(rc);
+  *off_out = off;
+  *ent_out = ent;
+  *n_out = (long long)total;
+  return done(0);
 }

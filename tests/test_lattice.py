@@ -265,3 +265,86 @@ def test_lattice_cluster_split_matches_single_cta(monkeypatch):
             assert abs(x.total_cost - y.total_cost) <= 1e-9 * abs(x.total_cost)
         assert {h.words for h in na} == {h.words for h in nb} or \
             abs(na[-1].total_cost - na[-2].total_cost) <= 1e-9 * abs(na[-1].total_cost)
+
+
+def _canon(lat):
+    return sorted(zip(lat.frame.tolist(), lat.src_state.tolist(), lat.dst_state.tolist(), lat.labels,
+                      lat.weight.tolist()))
+
+
+@pytest.mark.parametrize("search", ["exact", "fast"])
+def test_closure_index_matches_general_kernel(monkeypatch, search):
+    """Graphs whose epsilon arcs carry no output label take the indexed
+    lattice kernel (closures from the per-graph closure index, destinations
+    from a shared-memory map). Its lattices equal the general kernel's
+    (per-item closures) arc for arc; weights agree up to the summation order
+    c0 + (w1 + w2) vs (c0 + w1) + w2."""
+    from paper_2311_04996_b200 import DecoderConfig, decode_lattices, synth
+
+    s = _system(num_units=129, blank_id=128, num_words=300, order=3, seed=5, min_pron=1, max_pron=4,
+                followers=15)
+    fg = s.graph
+    eps = np.concatenate([np.arange(fg.off[i], fg.eps_end[i]) for i in range(fg.num_states)])
+    assert len(eps) and not np.any(np.asarray(fg.olabel)[eps])  # the indexed kernel applies
+    utts = list(synth.conformer_logprobs(s, 10, 80, seed=4, delta=5.0, sigma=1.5, dtype=np.float32))
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    rng = np.random.default_rng(1)
+    boosts = []
+    for i in range(len(utts)):
+        b = None
+        if i % 3 == 1:
+            b = np.zeros(fg.max_olabel + 1)
+            b[rng.choice(np.arange(1, fg.max_olabel + 1), 20, replace=False)] = -rng.uniform(0.5, 3.0, 20)
+        boosts.append(b)
+    out = {}
+    for mode in ("pre", "general"):
+        if mode == "general":
+            monkeypatch.setenv("CTW_LAT_NOPRE", "1")
+        out[mode] = decode_lattices(fg, cfg, utts, lattice_beam=5.0, boost=boosts, search=search)
+    for a, b in zip(out["pre"], out["general"]):
+        assert a.status == b.status == 0
+        assert a.num_arcs == b.num_arcs > 0
+        ca, cb = _canon(a), _canon(b)
+        assert [x[:4] for x in ca] == [x[:4] for x in cb]
+        assert all(abs(x[4] - y[4]) <= W_TOL * max(1.0, abs(y[4])) for x, y in zip(ca, cb))
+        assert a.best_path == b.best_path and abs(a.best_cost - b.best_cost) <= 1e-9
+        na, nb = a.nbest(5), b.nbest(5)
+        assert [h.words for h in na] == [h.words for h in nb] or \
+            abs(na[-1].total_cost - na[-2].total_cost) <= 1e-9 * abs(na[-1].total_cost)
+
+
+def test_closure_index_overflow_reruns_general_kernel():
+    """A hub with 80 unlabelled epsilon arcs: its closure is too large for the
+    closure index (64 entries), items reaching it mark the lane (status 3),
+    and the host re-runs it with the general large-capacity kernel; the
+    lattice equals the CPU restatement's."""
+    import lattice_oracle as lo
+
+    from paper_2311_04996_b200 import DecoderConfig, FlatGraph, decode_lattices
+
+    n_leaf = 80
+    src, il, ol, w, ns = [0], [1], [1], [0.5], [1]
+    for k in range(2, 2 + n_leaf):
+        src += [1, k]
+        il += [0, 1 + k % 3]
+        ol += [0, k]
+        w += [0.01 * k, 0.1]
+        ns += [k, 1]
+    final = np.full(2 + n_leaf, np.inf)
+    final[2:] = 0.0
+    fg = FlatGraph.from_arrays(2 + n_leaf, 0, src, il, ol, w, ns, final)
+
+    class Sys:
+        graph = fg
+
+    rng = np.random.default_rng(5)
+    frames = rng.normal(-1.0, 0.5, size=(6, 4))
+    cfg = DecoderConfig(beam=1e9, max_active=10_000)
+    beam = 1.5
+    lat = decode_lattices(fg, cfg, [frames], lattice_beam=beam)[0]
+    assert lat.status == 0
+    ora, seeds, (ow, oc, _) = _oracle_lattice(Sys, cfg, frames, beam)
+    assert lat.best_path.words == ow and abs(lat.best_cost - oc) <= 1e-9
+    inner = lo.kept(ora, beam, -1e-7)
+    outer = lo.kept(ora, beam, +1e-7)
+    assert len(inner) <= lat.num_arcs <= len(outer)
