@@ -157,6 +157,9 @@ struct ctw_lanes {
   std::vector<CtwSrc*> seed_src;
   std::vector<int32_t*> seed_pend;
   std::vector<int32_t> seed_n, seed_cap;
+  std::vector<int32_t> seed_pool;  // label-pool prefix written by the seeding (seed label codes)
+  char* lat_pin = nullptr;         // pinned staging of lattice results (grow-only)
+  size_t lat_pin_cap = 0;
   // phrase automata (ctw_lane_set_fsa), device copies per lane
   std::vector<uint16_t*> fsa_next;
   std::vector<double*> fsa_cost;
@@ -421,6 +424,7 @@ int reserve_lanes(ctw_lanes* l, int n) {
   l->seed_pend.resize(n, nullptr);
   l->seed_n.resize(n, 0);
   l->seed_cap.resize(n, 0);
+  l->seed_pool.resize(n, 0);
   l->fsa_next.resize(n, nullptr);
   l->fsa_cost.resize(n, nullptr);
   l->fsa_cap.resize(n, 0);
@@ -800,6 +804,7 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   for (CtwRecPage* p : l->slabs) sfree(p, l->stream);
   cudaStreamSynchronize(l->stream);
   if (l->h) cudaFreeHost(l->h);
+  if (l->lat_pin) cudaFreeHost(l->lat_pin);
   dfree(l->d);
   dfree(l->d_ids);
   dfree(l->d_nframes);
@@ -886,6 +891,7 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
       l->seed_cap[lane] = c;
     }
     l->seed_n[lane] = L.n_src;
+    l->seed_pool[lane] = L.pool_used;
     if (L.n_src) {
       CUDA_TRY(cudaMemcpyAsync(l->seed_src[lane], L.src[L.src_buf], (size_t)L.n_src * sizeof(CtwSrc),
                                cudaMemcpyDeviceToDevice, l->stream));
@@ -1464,7 +1470,7 @@ T* cmalloc(size_t n) {
   return (T*)malloc(std::max<size_t>(n, 1) * sizeof(T));
 }
 
-void expand_code(const std::vector<int32_t>& pool, int32_t code, std::vector<int32_t>& out) {
+void expand_code(const int32_t* pool, int32_t code, std::vector<int32_t>& out) {
   if (code > 0) out.push_back(code);
   else if (code < 0) {
     const int64_t off = -(int64_t)code - 1;
@@ -1542,7 +1548,7 @@ int ctw_lane_export(ctw_lanes* l, int32_t lane, int64_t frame_from, int64_t base
     out->rec_prev[k] = map_prev(link[r].x);
     out->rec_state[k] = st[r];
     out->rec_cost[k] = cost[r];
-    expand_code(pool, link[r].y, labs);
+    expand_code(pool.data(), link[r].y, labs);
     out->rec_olab_off[k + 1] = (int64_t)labs.size();
   }
   out->n_olab = (int64_t)labs.size();
@@ -1564,7 +1570,7 @@ int ctw_lane_export(ctw_lanes* l, int32_t lane, int64_t frame_from, int64_t base
     out->tok_state[k] = t.state;
     out->tok_cost[k] = t.cost;
     out->tok_bp[k] = map_prev(t.bp);
-    if (!pend.empty()) expand_code(pool, pend[to[k]], ch);
+    if (!pend.empty()) expand_code(pool.data(), pend[to[k]], ch);
     out->tok_chain_off[k + 1] = (int64_t)ch.size();
   }
   out->n_chain = (int64_t)ch.size();
@@ -1785,6 +1791,15 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
     if (l->compacted[lane_ids[i]]) return fail(-1, "lane history was garbage-collected: no lattice");
   }
   const size_t esz = dtype ? 8 : 4;
+  using clk = std::chrono::steady_clock;
+  const bool tm = getenv("CTW_LAT_TIMING") != nullptr;  // diagnostics: phase times on stderr
+  clk::time_point tp = clk::now();
+  auto lap = [&](const char* what) {
+    if (!tm) return;
+    const clk::time_point t = clk::now();
+    fprintf(stderr, "lattice %s %.3f ms\n", what, std::chrono::duration<double>(t - tp).count() * 1e3);
+    tp = t;
+  };
   std::vector<int32_t> frames(n);
   for (int i = 0; i < n; ++i) frames[i] = l->h[lane_ids[i]].frame_count;
   const char* dev_ll = nullptr;
@@ -1862,6 +1877,7 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       ent[k] = e;
     }
     CUDA_TRY(cudaMemcpyAsync(d_ent, ent.data(), m * sizeof(CtwLatEntry), cudaMemcpyHostToDevice, l->stream));
+    lap("setup");
     // CTAs per lane: up to 8 while the batch leaves SMs idle, bounded so a
     // rank's share of a layer fits its slice of the lane's frontier scratch;
     // a re-run after a closure overflow takes the large-capacity kernel on
@@ -1890,14 +1906,44 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
     l->launches++;
     CUDA_TRY(cudaMemcpyAsync(ent.data(), d_ent, m * sizeof(CtwLatEntry), cudaMemcpyDeviceToHost, l->stream));
     CUDA_TRY(cudaStreamSynchronize(l->stream));
+    lap("kernel");
     std::vector<int> again;
-    // stage every finished lane's device results first (one synchronisation)
+    // stage every finished lane's device results first, into one pinned
+    // buffer (one synchronisation): kept arcs, their label segments, the
+    // seeds and the label-pool prefix their codes point into
     struct Host {
-      std::vector<CtwLatArc> arcs;
-      std::vector<int32_t> lab, spend, pool;
-      std::vector<CtwSrc> seeds;
+      const CtwLatArc* arcs = nullptr;
+      const int32_t *lab = nullptr, *spend = nullptr, *pool = nullptr;
+      const CtwSrc* seeds = nullptr;
     };
     std::vector<Host> hb((size_t)m);
+    std::vector<size_t> hoff((size_t)m * 5, 0);
+    auto al16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    size_t pin_need = 0;
+    for (int k = 0; k < m; ++k) {
+      const int i = todo[k];
+      const CtwLatEntry& e = ent[k];
+      if (e.status == 1 || e.status == 2 || (e.status == 3 && !big[i])) continue;
+      const int lane = lane_ids[i];
+      const size_t ns = (size_t)l->seed_n[lane];
+      const size_t sz[5] = {(size_t)e.n_arcs * sizeof(CtwLatArc), (size_t)e.lpool_used * 4, ns * sizeof(CtwSrc),
+                            ns * 4, (size_t)l->seed_pool[lane] * 4};
+      for (int q = 0; q < 5; ++q) {
+        hoff[(size_t)k * 5 + q] = pin_need;
+        pin_need += al16(sz[q]);
+      }
+    }
+    if (pin_need > l->lat_pin_cap) {
+      if (l->lat_pin) cudaFreeHost(l->lat_pin);
+      l->lat_pin = nullptr;
+      l->lat_pin_cap = 0;
+      const size_t c = std::max(pin_need + pin_need / 2, (size_t)1 << 20);
+      if (cudaMallocHost((void**)&l->lat_pin, c) != cudaSuccess) {
+        release();
+        return fail(CTW_ERR_OOM, "lattice: pinned staging allocation failed");
+      }
+      l->lat_pin_cap = c;
+    }
     for (int k = 0; k < m; ++k) {
       const int i = todo[k];
       const CtwLatEntry& e = ent[k];
@@ -1905,26 +1951,30 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       const int lane = lane_ids[i];
       const CtwLane& L = l->h[lane];
       Host& h = hb[k];
-      h.arcs.resize((size_t)e.n_arcs);
-      h.lab.resize((size_t)e.lpool_used);
+      char* b = l->lat_pin;
+      const size_t* o = &hoff[(size_t)k * 5];
+      h.arcs = reinterpret_cast<const CtwLatArc*>(b + o[0]);
+      h.lab = reinterpret_cast<const int32_t*>(b + o[1]);
+      h.seeds = reinterpret_cast<const CtwSrc*>(b + o[2]);
+      h.spend = reinterpret_cast<const int32_t*>(b + o[3]);
+      h.pool = reinterpret_cast<const int32_t*>(b + o[4]);
       const int ns = l->seed_n[lane];
-      h.seeds.resize((size_t)ns);
-      h.spend.resize((size_t)ns);
-      h.pool.resize((size_t)L.pool_used);
       if (e.n_arcs)
-        CUDA_TRY(cudaMemcpyAsync(h.arcs.data(), d_arcs[i], h.arcs.size() * sizeof(CtwLatArc),
-                                 cudaMemcpyDeviceToHost, l->stream));
-      if (e.lpool_used)
-        CUDA_TRY(cudaMemcpyAsync(h.lab.data(), d_lab[i], h.lab.size() * 4, cudaMemcpyDeviceToHost, l->stream));
-      if (ns) {
-        CUDA_TRY(cudaMemcpyAsync(h.seeds.data(), l->seed_src[lane], ns * sizeof(CtwSrc), cudaMemcpyDeviceToHost,
+        CUDA_TRY(cudaMemcpyAsync(b + o[0], d_arcs[i], (size_t)e.n_arcs * sizeof(CtwLatArc), cudaMemcpyDeviceToHost,
                                  l->stream));
-        CUDA_TRY(cudaMemcpyAsync(h.spend.data(), l->seed_pend[lane], ns * 4, cudaMemcpyDeviceToHost, l->stream));
+      if (e.lpool_used)
+        CUDA_TRY(cudaMemcpyAsync(b + o[1], d_lab[i], (size_t)e.lpool_used * 4, cudaMemcpyDeviceToHost, l->stream));
+      if (ns) {
+        CUDA_TRY(cudaMemcpyAsync(b + o[2], l->seed_src[lane], ns * sizeof(CtwSrc), cudaMemcpyDeviceToHost,
+                                 l->stream));
+        CUDA_TRY(cudaMemcpyAsync(b + o[3], l->seed_pend[lane], ns * 4, cudaMemcpyDeviceToHost, l->stream));
       }
-      if (L.pool_used)
-        CUDA_TRY(cudaMemcpyAsync(h.pool.data(), L.pool, h.pool.size() * 4, cudaMemcpyDeviceToHost, l->stream));
+      if (l->seed_pool[lane])
+        CUDA_TRY(cudaMemcpyAsync(b + o[4], L.pool, (size_t)l->seed_pool[lane] * 4, cudaMemcpyDeviceToHost,
+                                 l->stream));
     }
     CUDA_TRY(cudaStreamSynchronize(l->stream));
+    lap("d2h");
     std::vector<int> done;
     for (int k = 0; k < m; ++k) {
       const int i = todo[k];
@@ -1957,12 +2007,12 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
       o.lattice_beam = lattice_beam;
       o.closure_items = e.closure_items;
       o.closure_pruned = e.closure_pruned;
-      Host& hh = hb[k];
-      const std::vector<CtwLatArc>& arcs = hh.arcs;
-      const std::vector<int32_t>& lab = hh.lab;
-      const std::vector<CtwSrc>& seeds = hh.seeds;
-      const std::vector<int32_t>& spend = hh.spend;
-      const std::vector<int32_t>& pool = hh.pool;
+      const Host& hh = hb[k];
+      const CtwLatArc* arcs = hh.arcs;
+      const int32_t* lab = hh.lab;
+      const CtwSrc* seeds = hh.seeds;
+      const int32_t* spend = hh.spend;
+      const int32_t* pool = hh.pool;
       const int ns = l->seed_n[lane];
       o.n_seeds = ns;
       o.seed_state = cmalloc<int32_t>(ns);
@@ -2036,9 +2086,11 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
         });
       for (auto& t : th) t.join();
     }
+    lap("post");
     todo.swap(again);
   }
   release();
+  lap("release");
   return 0;
 }
 

@@ -55,7 +55,7 @@
 #define LAT_QL 128      // local relaxation budget per work item
 #define LAT_CL_BIG 256  // ... of the re-run for items that overflowed
 #define LAT_QL_BIG 1024
-#define LAT_MAP 1024        // shared-memory destination map slots (<= LAT_MAP / 2 entries)
+#define LAT_MAP 2048        // indexed kernel: shared-memory destination map slots (<= LAT_MAP / 2 entries)
 #define CLO_CAP 64          // closure index: largest indexed closure
 #define CLO_QCAP 256        // ... and its relaxation budget
 
@@ -168,27 +168,7 @@ struct __align__(16) LatSmem {
   unsigned long long mb_all;    // cluster-wide minimum
   unsigned long long best;
   unsigned long long items, pruned;
-  int map_tot;            // destination-map entries over all ranks
-  int nput_r[8];          // ... per rank
 };
-
-// Shared-memory copy of the layer's destination map (PRE kernel): state ->
-// node and the node's beta, open addressing over LAT_MAP slots.
-struct LatMapSm {
-  uint32_t st[LAT_MAP];
-  int32_t node[LAT_MAP];
-  unsigned long long beta[LAT_MAP];
-};
-
-__device__ __forceinline__ int map_find(const LatMapSm& mp, uint32_t s) {
-  uint32_t h = lat_hash(s, 32 - 10) & (LAT_MAP - 1);
-  for (;;) {
-    const uint32_t k = mp.st[h];
-    if (k == s) return (int)h;
-    if (k == CTW_EMPTY) return -1;
-    h = (h + 1) & (LAT_MAP - 1);
-  }
-}
 
 #ifndef LAT_MINB
 #define LAT_MINB 4  // 4 CTAs (64 warps) per SM: every lane of a 512-lane batch resident (61 -> 32 registers; lattice stage -32 %)
@@ -314,82 +294,13 @@ __device__ __forceinline__ void lat_item(const LatArgs& a, CtwLatEntry& E, const
   }
 }
 
-// Work item of the indexed kernel: the closure of nextstate(e) comes from
-// the graph's closure index, destinations from the shared-memory map (or
-// the lane table when the layer's map is too large for it).
-__device__ __forceinline__ void lat_item_pre(const LatArgs& a, CtwLatEntry& E, const CtwLane& lane, LatSmem& sm,
-                                             const LatMapSm& mp, bool map_ok, uint32_t shift, uint32_t mask,
-                                             bool cut_ok, double cutoff, double min_beta, int32_t sst, double sc,
-                                             int node, int f, uint32_t ai, long long row0) {
-  const double INF = __longlong_as_double(0x7FF0000000000000LL);
-  const CtwArc arc = a.g.arcs[ai];
-  double x;
-  {
-    const long long idx = row0 + arc.ilabel - 1;
-    x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
-  }
-  double c0 = __dadd_rn(__dmul_rn(-a.acoustic_scale, x), arc.weight);
-  const int32_t ol0 = a.g.olabel[ai];
-  const uint32_t x0 = lat_dest(lane, (uint32_t)sst, ol0, (uint32_t)arc.nextstate, c0);
-  if (!(c0 < INF)) return;
-  if (cut_ok && sc + c0 + min_beta > cutoff) {
-    atomicAdd(&sm.pruned, 1ULL);
-    return;
-  }
-  atomicAdd(&sm.items, 1ULL);
-  const uint32_t s0 = x0 & lane.smask, hi = x0 & ~lane.smask;
-  const uint32_t ob = __ldg(&a.clo_off[s0]);
-  if (ob & CTW_CLO_NONE) {  // closure too large for the index: the host re-runs the lane
-    atomicMax(&E.status, 3);
-    return;
-  }
-  const uint32_t oe = __ldg(&a.clo_off[s0 + 1]) & ~CTW_CLO_NONE;
-  for (uint32_t k = ob; k < oe; ++k) {
-    const ulonglong2 ce = __ldg(reinterpret_cast<const ulonglong2*>(a.clo_ent + k));  // {w, state}
-    const double c = __dadd_rn(c0, __longlong_as_double((long long)ce.x));
-    if (!(c < INF)) continue;
-    if (cut_ok && sc + c + min_beta > cutoff) continue;
-    const uint32_t key = (uint32_t)ce.y | hi;
-    int dn;
-    double bd;
-    if (map_ok) {
-      const int slot = map_find(mp, key);
-      if (slot < 0) continue;
-      dn = mp.node[slot];
-      bd = lat_key2d(mp.beta[slot]);
-    } else {
-      dn = lat_get(lane, shift, mask, key);
-      if (dn < 0) continue;
-      bd = lat_key2d(__ldcg(&E.beta[dn]));
-    }
-    const double tail = __dadd_rn(c, bd);
-    atomicMin(&E.beta[node], lat_d2key(tail));
-    if (__dadd_rn(sc, tail) > cutoff) continue;
-    const int ia = atomicAdd(&E.n_arcs, 1);
-    if (ia >= E.arc_cap) {
-      atomicMax(&E.status, 1);
-      continue;
-    }
-    CtwLatArc la;
-    la.src = node;
-    la.dst = dn;
-    la.w = c;
-    la.code = ol0;
-    la.frame = f;
-    la.dst_state = (int32_t)key;
-    la.src_state = sst;
-    E.arcs[ia] = la;
-  }
-}
-
 // One thread-block cluster of R CTAs ("ranks") per lane: the ranks split
 // every layer's destination records and source tiles and meet at cluster
 // barriers between the steps of a layer; counters live in the entry (global
 // atomics), the layer's minimum beta is exchanged through shared memory.
-template <int CL, int QL, bool PRE>
+template <int CL, int QL>
 __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
   __shared__ LatSmem sm;
-  __shared__ typename std::conditional<PRE, LatMapSm, char>::type mp_;
   cg::cluster_group cl = cg::this_cluster();
   const int R = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const int tid = threadIdx.x;
@@ -451,8 +362,6 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
       sm.nput = 0;
       sm.ac_min = ~0ULL;
     }
-    if constexpr (PRE)
-      for (int i = tid; i < LAT_MAP; i += LAT_BS) mp_.st[i] = CTW_EMPTY;
     __syncthreads();
     {
       // smallest acoustic term of the frame (source-level pruning bound)
@@ -482,39 +391,14 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
     cl.sync();  // the whole layer is in the map; every rank's minimum published
     if (tid < 32) {
       unsigned long long m = tid < R ? cl.map_shared_rank(&sm, tid)->mb_pub : ~0ULL;
-      int np = tid < R ? min(cl.map_shared_rank(&sm, tid)->nput, pcap) : 0;
-      if (tid < 8) sm.nput_r[tid] = np;
       for (int d = 16; d; d >>= 1) {
         const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, m, d);
         if (o < m) m = o;
-        np += __shfl_xor_sync(0xFFFFFFFFu, np, d);
       }
-      if (tid == 0) {
-        sm.mb_all = m;
-        sm.map_tot = np;
-      }
+      if (tid == 0) sm.mb_all = m;
     }
     __syncthreads();
     const double min_beta = sm.mb_all == ~0ULL ? INF : lat_key2d(sm.mb_all);
-    // PRE: every rank copies the whole layer map (all ranks' lists) into its
-    // shared memory, with the nodes' beta (final since the previous layer)
-    const bool map_ok = PRE && sm.map_tot <= LAT_MAP / 2;
-    if constexpr (PRE) {
-      if (map_ok && min_beta != INF) {
-        for (int r = 0; r < R; ++r) {
-          const uint2* pl = lane.front + (size_t)r * pcap;
-          for (int i = tid; i < sm.nput_r[r]; i += LAT_BS) {
-            const uint2 e = __ldcg(&pl[i]);
-            const int32_t nd = (int32_t)__ldcg(&lane.table[e.x].tb);
-            uint32_t h = lat_hash(e.y, 32 - 10) & (LAT_MAP - 1);
-            while (atomicCAS(&mp_.st[h], CTW_EMPTY, e.y) != CTW_EMPTY) h = (h + 1) & (LAT_MAP - 1);
-            mp_.node[h] = nd;
-            mp_.beta[h] = __ldcg(&E.beta[nd]);
-          }
-        }
-      }
-      __syncthreads();
-    }
     // ---- sources: layer f-1 (records) or the seeds, tiles split over the ranks
     const long long s0 = f > 0 ? lane.frame_base[f - 1] : 0;
     const long long s1 = f > 0 ? d0 : S0;
@@ -558,12 +442,8 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
             if (sm.off[mid] <= item) lo = mid;
             else hi = mid - 1;
           }
-          if constexpr (PRE)
-            lat_item_pre(a, E, lane, sm, mp_, map_ok, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo],
-                         sm.node[lo], f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
-          else
-            lat_item<CL, QL>(a, E, lane, sm, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo],
-                             sm.node[lo], f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
+          lat_item<CL, QL>(a, E, lane, sm, shift, mask, cut_ok, cutoff, min_beta, sm.sst[lo], sm.sc[lo], sm.node[lo],
+                           f, sm.beg[lo] + (uint32_t)(item - sm.off[lo]), row0);
         }
         __syncthreads();  // the tile's smem is reused by the next tile
       }
@@ -589,6 +469,284 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
   }
 }
 
+
+// ------------------------------------------------------------ indexed kernel
+// (graphs without labelled epsilon arcs): closures from the closure index,
+// and every rank builds the layer's whole destination map in its own shared
+// memory from the layer's records (8x redundant reads of a few KB instead of
+// two extra cluster barriers and the lane-table map): one cluster barrier
+// per layer.
+
+#ifndef LAT_IBS
+#define LAT_IBS 512  // threads per CTA of the indexed kernel
+#endif
+#ifndef LAT_IMINB
+#define LAT_IMINB 4
+#endif
+
+struct __align__(16) LatIdxSmem {
+  typedef cub::BlockScan<int, LAT_IBS> Scan;
+  typename Scan::TempStorage scan;
+  int off[LAT_IBS + 1];
+  uint32_t beg[LAT_IBS];
+  int32_t sst[LAT_IBS];
+  int32_t node[LAT_IBS];
+  double sc[LAT_IBS];
+  // destination map: state -> node and the node's beta (sortable key)
+  uint32_t mst[LAT_MAP];
+  int32_t mnode[LAT_MAP];
+  unsigned long long mbeta[LAT_MAP];
+  int nmap, final_mode;
+  unsigned long long ac_min, min_beta, best, items, pruned;
+  // per-layer values the work items read at their point of use (fewer live
+  // registers across the item loop: no spills at 32 registers)
+  double cutoff, mb;
+  long long row0;
+  int f, cut_ok;
+  CtwLatEntry* E;
+  const CtwLane* lane;
+  int T, NR, S0;
+  int s0, nsrc;  // the layer's sources
+  int t0;        // first source of the current tile
+};
+
+#define LAT_MAP_LOG2 11
+static_assert((1 << LAT_MAP_LOG2) == LAT_MAP, "LAT_MAP is 2^LAT_MAP_LOG2");
+
+__device__ __forceinline__ int idx_find(const LatIdxSmem& sm, uint32_t s) {
+  uint32_t h = lat_hash(s, 32 - LAT_MAP_LOG2);
+  for (;;) {
+    const uint32_t k = sm.mst[h];
+    if (k == s) return (int)h;
+    if (k == CTW_EMPTY) return -1;
+    h = (h + 1) & (LAT_MAP - 1);
+  }
+}
+
+// Work item: emitting arc ai out of source node `node` (state sst, cost sc).
+__device__ __forceinline__ void lat_item_idx(const LatArgs& a, LatIdxSmem& sm, int lo, uint32_t ai) {
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const CtwArc arc = a.g.arcs[ai];
+  double x;
+  {
+    const long long idx = sm.row0 + arc.ilabel - 1;
+    x = a.is_f64 ? ((const double*)a.loglik)[idx] : (double)((const float*)a.loglik)[idx];
+  }
+  double c0 = __dadd_rn(__dmul_rn(-a.acoustic_scale, x), arc.weight);
+  const int32_t ol0 = a.g.olabel[ai];
+  const uint32_t x0 = lat_dest(*sm.lane, (uint32_t)sm.sst[lo], ol0, (uint32_t)arc.nextstate, c0);
+  if (!(c0 < INF)) return;
+  const double sc = sm.sc[lo];
+  if (sm.cut_ok && sc + c0 + sm.mb > sm.cutoff) {
+    atomicAdd(&sm.pruned, 1ULL);
+    return;
+  }
+  atomicAdd(&sm.items, 1ULL);
+  const uint32_t smask = sm.lane->smask;
+  const uint32_t s0 = x0 & smask, hi = x0 & ~smask;
+  const uint32_t ob = __ldg(&a.clo_off[s0]);
+  if (ob & CTW_CLO_NONE) {  // closure too large for the index: the host re-runs the lane
+    atomicMax(&sm.E->status, 3);
+    return;
+  }
+  const uint32_t oe = __ldg(&a.clo_off[s0 + 1]) & ~CTW_CLO_NONE;
+  for (uint32_t k = ob; k < oe; ++k) {
+    const ulonglong2 ce = __ldg(reinterpret_cast<const ulonglong2*>(a.clo_ent + k));  // {w, state}
+    const double c = __dadd_rn(c0, __longlong_as_double((long long)ce.x));
+    if (!(c < INF)) continue;
+    if (sm.cut_ok && sc + c + sm.mb > sm.cutoff) continue;
+    const uint32_t key = (uint32_t)ce.y | hi;
+    const int slot = idx_find(sm, key);
+    if (slot < 0) continue;
+    const double tail = __dadd_rn(c, lat_key2d(sm.mbeta[slot]));
+    CtwLatEntry& E = *sm.E;
+    atomicMin(&E.beta[sm.node[lo]], lat_d2key(tail));
+    if (__dadd_rn(sc, tail) > sm.cutoff) continue;
+    const int ia = atomicAdd(&E.n_arcs, 1);
+    if (ia >= E.arc_cap) {
+      atomicMax(&E.status, 1);
+      continue;
+    }
+    CtwLatArc la;
+    la.src = sm.node[lo];
+    la.dst = sm.mnode[slot];
+    la.w = c;
+    la.code = ol0;
+    la.frame = sm.f;
+    la.dst_state = (int32_t)key;
+    la.src_state = sm.sst[lo];
+    E.arcs[ia] = la;
+  }
+}
+
+__global__ void __launch_bounds__(LAT_IBS, LAT_IMINB) k_lattice_idx(LatArgs a) {
+  __shared__ LatIdxSmem sm;
+  cg::cluster_group cl = cg::this_cluster();
+  const int R = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  CtwLatEntry& E = a.ent[blockIdx.x / R];
+  const CtwLane& lane = a.lanes[E.lane];
+  const double INF = __longlong_as_double(0x7FF0000000000000LL);
+  const int T = lane.frame_count;
+  const int NR = (int)lane.n_rec;  // node ids are int32 (S0 + NR < 2^31)
+  const int S0 = E.n_seeds;
+  const int stride = R * LAT_IBS;
+  if (tid == 0) {
+    sm.best = ~0ULL;
+    sm.final_mode = 0;
+    sm.items = 0;
+    sm.pruned = 0;
+    sm.E = &E;
+    sm.lane = &lane;
+    sm.T = T;
+    sm.NR = NR;
+    sm.S0 = S0;
+  }
+  for (int i = rank * LAT_IBS + tid; i < S0 + NR; i += stride) E.beta[i] = ~0ULL;
+  cl.sync();  // beta cleared everywhere before any rank sets the last layer's
+  if (T == 0) {
+    if (rank == 0 && tid == 0) E.status = 4;
+    return;
+  }
+  // ---- last layer: beta = final weight (final states if any survive, else 0)
+  const int lf0 = (int)lane.frame_base[T - 1], lf1 = NR;
+  for (int r = lf0 + tid; r < lf1; r += LAT_IBS) {
+    int32_t st;
+    double c;
+    lat_rec(lane, r, &st, &c);
+    if (a.g.final_w[(uint32_t)st & lane.smask] != INF) sm.final_mode = 1;  // benign race: all writers store 1
+  }
+  __syncthreads();
+  const bool fm = sm.final_mode != 0;
+  for (int r = lf0 + tid; r < lf1; r += LAT_IBS) {
+    int32_t st;
+    double c;
+    lat_rec(lane, r, &st, &c);
+    const double fw = fm ? a.g.final_w[(uint32_t)st & lane.smask] : 0.0;
+    if (fm && fw == INF) continue;
+    atomicMin(&sm.best, lat_d2key(c + fw));
+    if ((((r - lf0) / LAT_IBS) % R) == rank) E.beta[S0 + r] = lat_d2key(fw);
+  }
+  cl.sync();  // the last layer's beta set in every rank's share
+  // loop-invariant values live in shared memory (no spills at 32 registers)
+  if (tid == 0) {
+    sm.cutoff = __dadd_rn(lat_key2d(sm.best), a.lattice_beam);
+    sm.cut_ok = lane.prune_ok != 0;  // epsilon continuations never lower a cost
+  }
+  bool ovf = false;
+
+  if (threadIdx.x == 0) sm.f = T - 1;
+  for (;;) {
+    __syncthreads();  // sm.f of this layer
+    if (sm.f < 0) break;  // the layer index lives in shared memory (no register across the layer)
+    const int d0 = (int)sm.lane->frame_base[sm.f], d1 = (sm.f + 1 < sm.T) ? (int)sm.lane->frame_base[sm.f + 1] : sm.NR;
+    if ((int)threadIdx.x == 0) {
+      sm.min_beta = ~0ULL;
+      sm.nmap = 0;
+      sm.ac_min = ~0ULL;
+    }
+    for (int i = (int)threadIdx.x; i < LAT_MAP; i += LAT_IBS) sm.mst[i] = CTW_EMPTY;
+    __syncthreads();
+    {
+      // smallest acoustic term of the frame (source-level pruning bound)
+      const long long rr = sm.E->ll_off + (long long)sm.f * a.width;
+      for (int v = (int)threadIdx.x; v < a.width; v += LAT_IBS) {
+        const double x = a.is_f64 ? ((const double*)a.loglik)[rr + v] : (double)((const float*)a.loglik)[rr + v];
+        atomicMin(&sm.ac_min, lat_d2key(__dmul_rn(-a.acoustic_scale, x)));
+      }
+    }
+    // ---- destination map: nodes of layer f that can lie on a kept path
+    // (beta final since the previous layer's barrier), the whole layer in
+    // every rank
+    for (int r = d0 + (int)threadIdx.x; r < d1; r += LAT_IBS) {
+      const unsigned long long bk = __ldcg(&sm.E->beta[sm.S0 + r]);
+      if (bk == ~0ULL) continue;
+      int32_t st;
+      double c;
+      lat_rec(*sm.lane, r, &st, &c);
+      if (c + lat_key2d(bk) > sm.cutoff) continue;
+      atomicMin(&sm.min_beta, bk);
+      if (atomicAdd(&sm.nmap, 1) >= LAT_MAP / 2) continue;
+      uint32_t h = lat_hash((uint32_t)st, 32 - LAT_MAP_LOG2);
+      while (atomicCAS(&sm.mst[h], CTW_EMPTY, (uint32_t)st) != CTW_EMPTY) h = (h + 1) & (LAT_MAP - 1);
+      sm.mnode[h] = (int32_t)(sm.S0 + r);
+      sm.mbeta[h] = bk;
+    }
+    __syncthreads();
+    if (sm.nmap > LAT_MAP / 2) {  // same decision in every rank (same layer data): all leave together
+      ovf = true;
+      break;
+    }
+    // ---- sources: layer f-1 (records) or the seeds, tiles split over the ranks
+    if ((int)threadIdx.x == 0) {
+      const int s0 = sm.f > 0 ? (int)sm.lane->frame_base[sm.f - 1] : 0;
+      sm.s0 = s0;
+      sm.nsrc = (sm.f > 0 ? d0 : sm.S0) - s0;
+      sm.mb = sm.min_beta == ~0ULL ? INF : lat_key2d(sm.min_beta);
+      sm.row0 = sm.E->ll_off + (long long)sm.f * a.width;
+      sm.t0 = (int)cl.block_rank() * LAT_IBS;
+    }
+    __syncthreads();
+    if (sm.min_beta != ~0ULL) {
+      while (sm.t0 < sm.nsrc) {
+        const int si = sm.t0 + (int)threadIdx.x;
+        int deg = 0;
+        const double step_lb = lat_key2d(sm.ac_min) + sm.E->emit_lb;  // any emitting step costs at least this
+        if (si < sm.nsrc) {
+          int32_t st0;
+          double c0s;
+          int nd;
+          if (sm.f > 0) {
+            lat_rec(*sm.lane, sm.s0 + si, &st0, &c0s);
+            nd = sm.S0 + sm.s0 + si;
+          } else {
+            st0 = sm.E->seeds[si].state;
+            c0s = sm.E->seeds[si].cost;
+            nd = si;
+          }
+          const CtwStateRange rg = a.g.ranges[(uint32_t)st0 & sm.lane->smask];
+          deg = (int)(rg.emit_end - rg.emit_beg);
+          if (sm.cut_ok && c0s + step_lb + sm.mb > sm.cutoff + 1e-9 * fabs(sm.cutoff)) deg = 0;
+          sm.beg[(int)threadIdx.x] = rg.emit_beg;
+          sm.sst[(int)threadIdx.x] = st0;
+          sm.sc[(int)threadIdx.x] = c0s;
+          sm.node[(int)threadIdx.x] = nd;
+        }
+        int ex, tot;
+        LatIdxSmem::Scan(sm.scan).ExclusiveSum(deg, ex, tot);
+        sm.off[(int)threadIdx.x] = ex;
+        __syncthreads();
+        const int nv = min(LAT_IBS, sm.nsrc - sm.t0);
+        for (int item = (int)threadIdx.x; item < tot; item += LAT_IBS) {
+          int lo = 0, hi = nv - 1;  // last source with off <= item
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.off[mid] <= item) lo = mid;
+            else hi = mid - 1;
+          }
+          lat_item_idx(a, sm, lo, sm.beg[lo] + (uint32_t)(item - sm.off[lo]));
+        }
+        __syncthreads();  // the tile's smem is reused by the next tile
+        if (threadIdx.x == 0) sm.t0 += (int)(cl.num_blocks() * LAT_IBS);
+        __syncthreads();
+      }
+    }
+    cl.sync();  // the layer's arcs are out; beta of layer f-1 final in every rank
+    if (threadIdx.x == 0) sm.f -= 1;
+  }
+  if (threadIdx.x == 0) {
+    CtwLatEntry& Ex = *sm.E;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&Ex.closure_items), sm.items);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&Ex.closure_pruned), sm.pruned);
+    if (cl.block_rank() == 0) {
+      if (ovf) atomicMax(&Ex.status, 3);  // a layer map outgrew shared memory: general kernel re-run
+      if (Ex.status == 0 && sm.best == ~0ULL) Ex.status = 4;
+      Ex.final_mode = sm.final_mode;
+      Ex.best = lat_key2d(sm.best);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" int ctw_launch_lattice(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
@@ -598,13 +756,13 @@ extern "C" int ctw_launch_lattice(CtwLane* d_lanes, const CtwStateRange* ranges,
                                   cudaStream_t stream) {
   LatArgs a{d_lanes, LatGraph{ranges, arcs, olabel, final_w}, clo_off, clo_ent, d_ent, loglik, width, is_f64,
             acoustic_scale, lattice_beam};
-  void (*KFN)(LatArgs) = big       ? k_lattice<LAT_CL_BIG, LAT_QL_BIG, false>
-                         : clo_off ? k_lattice<1, 1, true>
-                                   : k_lattice<LAT_CL, LAT_QL, false>;
+  void (*KFN)(LatArgs) = big       ? k_lattice<LAT_CL_BIG, LAT_QL_BIG>
+                         : clo_off ? k_lattice_idx
+                                   : k_lattice<LAT_CL, LAT_QL>;
   (void)cudaGetLastError();
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(n * ranks));
-  lc.blockDim = dim3(LAT_BS);
+  lc.blockDim = dim3(KFN == k_lattice_idx ? LAT_IBS : LAT_BS);
   lc.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;

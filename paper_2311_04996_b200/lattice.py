@@ -48,8 +48,11 @@ class Lattice:
         self.closure_pruned = int(c.closure_pruned)
         ns, na = int(c.n_seeds), int(c.n_arcs)
 
-        def arr(p, n, dt):
-            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True) if n else np.zeros(0, dt)
+        def arr(p, n, dt):  # copy of n elements at a C pointer (the C arrays are freed with the lattice)
+            if not n:
+                return np.zeros(0, dt)
+            nb = n * np.dtype(dt).itemsize
+            return np.frombuffer((C.c_char * nb).from_address(C.cast(p, C.c_void_p).value), dt).copy()
 
         self.seed_state = arr(c.seed_state, ns, np.int32)
         self.seed_cost = arr(c.seed_cost, ns, np.float64)
