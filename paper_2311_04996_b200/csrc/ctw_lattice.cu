@@ -483,6 +483,9 @@ __global__ void __launch_bounds__(LAT_BS, LAT_MINB) k_lattice(LatArgs a) {
 #ifndef LAT_IMINB
 #define LAT_IMINB 4
 #endif
+#ifndef LAT_MU
+#define LAT_MU 4  // destination-map scan: records per thread per round
+#endif
 
 struct __align__(16) LatIdxSmem {
   typedef cub::BlockScan<int, LAT_IBS> Scan;
@@ -507,7 +510,7 @@ struct __align__(16) LatIdxSmem {
   const CtwLane* lane;
   int T, NR, S0;
   int s0, nsrc;  // the layer's sources
-  int t0;        // first source of the current tile
+  int t0, t1;    // first source of the current tile, end of this rank's share
 };
 
 #define LAT_MAP_LOG2 11
@@ -658,41 +661,56 @@ __global__ void __launch_bounds__(LAT_IBS, LAT_IMINB) k_lattice_idx(LatArgs a) {
     // ---- destination map: nodes of layer f that can lie on a kept path
     // (beta final since the previous layer's barrier), the whole layer in
     // every rank
-    for (int r = d0 + (int)threadIdx.x; r < d1; r += LAT_IBS) {
-      const unsigned long long bk = __ldcg(&sm.E->beta[sm.S0 + r]);
-      if (bk == ~0ULL) continue;
-      int32_t st;
-      double c;
-      lat_rec(*sm.lane, r, &st, &c);
-      if (c + lat_key2d(bk) > sm.cutoff) continue;
-      atomicMin(&sm.min_beta, bk);
-      if (atomicAdd(&sm.nmap, 1) >= LAT_MAP / 2) continue;
-      uint32_t h = lat_hash((uint32_t)st, 32 - LAT_MAP_LOG2);
-      while (atomicCAS(&sm.mst[h], CTW_EMPTY, (uint32_t)st) != CTW_EMPTY) h = (h + 1) & (LAT_MAP - 1);
-      sm.mnode[h] = (int32_t)(sm.S0 + r);
-      sm.mbeta[h] = bk;
+    // (the beta words of LAT_MU records per thread are loaded together: most
+    // are +inf and skipped, so the scan costs ~one memory latency)
+    for (int r0 = d0; r0 < d1; r0 += LAT_MU * LAT_IBS) {
+      unsigned long long bk[LAT_MU];
+#pragma unroll
+      for (int u = 0; u < LAT_MU; ++u) {
+        const int r = r0 + u * LAT_IBS + (int)threadIdx.x;
+        bk[u] = r < d1 ? __ldcg(&sm.E->beta[sm.S0 + r]) : ~0ULL;
+      }
+#pragma unroll
+      for (int u = 0; u < LAT_MU; ++u) {
+        if (bk[u] == ~0ULL) continue;
+        const int r = r0 + u * LAT_IBS + (int)threadIdx.x;
+        int32_t st;
+        double c;
+        lat_rec(*sm.lane, r, &st, &c);
+        if (c + lat_key2d(bk[u]) > sm.cutoff) continue;
+        atomicMin(&sm.min_beta, bk[u]);
+        if (atomicAdd(&sm.nmap, 1) >= LAT_MAP / 2) continue;
+        uint32_t h = lat_hash((uint32_t)st, 32 - LAT_MAP_LOG2);
+        while (atomicCAS(&sm.mst[h], CTW_EMPTY, (uint32_t)st) != CTW_EMPTY) h = (h + 1) & (LAT_MAP - 1);
+        sm.mnode[h] = (int32_t)(sm.S0 + r);
+        sm.mbeta[h] = bk[u];
+      }
     }
     __syncthreads();
     if (sm.nmap > LAT_MAP / 2) {  // same decision in every rank (same layer data): all leave together
       ovf = true;
       break;
     }
-    // ---- sources: layer f-1 (records) or the seeds, tiles split over the ranks
+    // ---- sources: layer f-1 (records) or the seeds, split over the ranks
     if ((int)threadIdx.x == 0) {
       const int s0 = sm.f > 0 ? (int)sm.lane->frame_base[sm.f - 1] : 0;
       sm.s0 = s0;
       sm.nsrc = (sm.f > 0 ? d0 : sm.S0) - s0;
       sm.mb = sm.min_beta == ~0ULL ? INF : lat_key2d(sm.min_beta);
       sm.row0 = sm.E->ll_off + (long long)sm.f * a.width;
-      sm.t0 = (int)cl.block_rank() * LAT_IBS;
+      // this rank's share: an equal contiguous slice (tiles of LAT_IBS)
+      const int nsrc = sm.nsrc, rn = (int)cl.num_blocks(), rk = (int)cl.block_rank();
+      const int share = (nsrc + rn - 1) / rn;
+      sm.t0 = min(nsrc, rk * share);
+      sm.t1 = min(nsrc, (rk + 1) * share);
     }
     __syncthreads();
     if (sm.min_beta != ~0ULL) {
-      while (sm.t0 < sm.nsrc) {
+      while (sm.t0 < sm.t1) {
         const int si = sm.t0 + (int)threadIdx.x;
         int deg = 0;
         const double step_lb = lat_key2d(sm.ac_min) + sm.E->emit_lb;  // any emitting step costs at least this
-        if (si < sm.nsrc) {
+        if (si < sm.t1) {
           int32_t st0;
           double c0s;
           int nd;
@@ -716,7 +734,7 @@ __global__ void __launch_bounds__(LAT_IBS, LAT_IMINB) k_lattice_idx(LatArgs a) {
         LatIdxSmem::Scan(sm.scan).ExclusiveSum(deg, ex, tot);
         sm.off[(int)threadIdx.x] = ex;
         __syncthreads();
-        const int nv = min(LAT_IBS, sm.nsrc - sm.t0);
+        const int nv = min(LAT_IBS, sm.t1 - sm.t0);
         for (int item = (int)threadIdx.x; item < tot; item += LAT_IBS) {
           int lo = 0, hi = nv - 1;  // last source with off <= item
           while (lo < hi) {
@@ -727,7 +745,7 @@ __global__ void __launch_bounds__(LAT_IBS, LAT_IMINB) k_lattice_idx(LatArgs a) {
           lat_item_idx(a, sm, lo, sm.beg[lo] + (uint32_t)(item - sm.off[lo]));
         }
         __syncthreads();  // the tile's smem is reused by the next tile
-        if (threadIdx.x == 0) sm.t0 += (int)(cl.num_blocks() * LAT_IBS);
+        if (threadIdx.x == 0) sm.t0 += LAT_IBS;
         __syncthreads();
       }
     }
