@@ -313,6 +313,7 @@ def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cor
                                  sync=torch.cuda.synchronize)
         k1 = lp.stats()
         ht = lp.host_timing()
+        gi = lp.graph_info()
         pool.close()
     st = res.stats()
     if not reference:
@@ -321,6 +322,7 @@ def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cor
         st["breakdown_s"]["frame_kernel_launches"] = k1["decode_launches"] - k0["decode_launches"]
         st["breakdown_s"]["advance_host"] = {k: (round(v, 4) if isinstance(v, float) else v)
                                              for k, v in ht.items()}
+        st["breakdown_s"]["step_graphs"] = gi
     st.update(streams=n_streams, audio_s_per_stream=frames * FRAME_S, chunk_s=12 * FRAME_S,
               arrivals_per_stream_per_s=2.0)
     return st, res.finals, utts

@@ -144,6 +144,11 @@ int ctw_lanes_reserve(ctw_lanes* l, int32_t n);
  * ctw_lanes_search_info: out3 = {mode, fast launches, decode launches}. */
 int ctw_lanes_set_search(ctw_lanes* l, int32_t mode);
 int ctw_lanes_search_info(ctw_lanes* l, int64_t* out3);
+/* ctw_lanes_graph_info: out3 = {CUDA-graph step launches, graphs captured,
+ * 1 if step graphs were turned off (CTW_NO_GRAPH or a capture failure)}.
+ * ctw_advance_best runs a step's first round (parameter uploads, frame
+ * kernel, partial best paths, result copies) as one graph launch. */
+int ctw_lanes_graph_info(ctw_lanes* l, int64_t* out3);
 
 /* Seed lanes: fresh channel = start token + epsilon closure, zero frames, empty
  * history (decoder.py:173-229). boosts[i] is a host f64 vector of

@@ -83,6 +83,7 @@ _SIGS = {
     "ctw_lanes_host_timing": (I32, [P, P]),
     "ctw_lanes_set_search": (I32, [P, I32]),
     "ctw_lanes_search_info": (I32, [P, P]),
+    "ctw_lanes_graph_info": (I32, [P, P]),
     "ctw_lanes_stream": (P, [P]),
     "ctw_lane_lattice": (I32, [P, P, I32, P, I32, I32, P, I32, F64, P]),
     "ctw_lattice_free": (None, [C.POINTER(CtwLattice)]),

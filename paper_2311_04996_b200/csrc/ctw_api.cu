@@ -209,6 +209,16 @@ struct ctw_lanes {
   int32_t search = 0;         // 0 exact (reference histories), 1 fast (words-exact)
   int64_t fast_launches = 0;  // decode launches that ran the fast mode
   uint32_t tlog2_hint = 0;  // largest token-table size any lane of this set grew to
+  // CUDA graphs of a streaming step (ctw_advance_best's first round: the
+  // parameter uploads, the frame kernel, the partial best paths and the
+  // result copies as one graph launch), keyed by launch shape and buffers
+  struct StepGraph {
+    uintptr_t key[12];
+    cudaGraphExec_t exec;
+  };
+  std::vector<StepGraph> step_graphs;
+  bool graphs_off = false;
+  int64_t graph_launches = 0, graph_builds = 0;
   std::mutex mu;
 };
 
@@ -820,6 +830,8 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   for (void* p : {(void*)l->h_ids, (void*)l->h_nframes, (void*)l->h_lloff, (void*)l->h_out, (void*)l->h_woff,
                   (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus, (void*)l->h_words})
     if (p) cudaFreeHost(p);
+  for (auto& sg : l->step_graphs) cudaGraphExecDestroy(sg.exec);
+  l->step_graphs.clear();
   if (l->ev0) cudaEventDestroy(l->ev0);
   if (l->ev1) cudaEventDestroy(l->ev1);
   if (l->own_stream) cudaStreamDestroy(l->stream);
@@ -1007,8 +1019,9 @@ int best_prepare(ctw_lanes* l, int n) {
 // Enqueue k_best_path over the n lanes whose ids are in l->d_ids (uploaded
 // from l->h_ids when `upload_ids`) with word windows caps[], and the copies
 // of its results into the pinned mirrors. No synchronisation.
-int best_enqueue(ctw_lanes* l, int n, const std::vector<int>& caps, bool upload_ids) {
-  ctw_graph* g = l->g;
+// host half of best_enqueue: buffers sized, word windows in the pinned
+// mirrors; *tot_out = total window
+int best_host(ctw_lanes* l, int n, const std::vector<int>& caps, long long* tot_out) {
   if (int r = best_prepare(l, n)) return r;
   long long tot = 0;
   for (int i = 0; i < n; ++i) {
@@ -1027,19 +1040,38 @@ int best_enqueue(ctw_lanes* l, int n, const std::vector<int>& caps, bool upload_
     CUDA_TRY(cudaMallocHost((void**)&l->h_words, ((size_t)tot + tot / 2) * sizeof(int32_t)));
     l->h_words_cap = (size_t)tot + tot / 2;
   }
+  *tot_out = tot;
+  return 0;
+}
+
+// device half: window uploads, k_best_path, the per-lane result copies
+// (graph-capturable: fixed sizes for a given n)
+int best_device(ctw_lanes* l, int n, bool upload_ids) {
+  ctw_graph* g = l->g;
   if (upload_ids) CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
   CUDA_TRY(cudaMemcpyAsync(l->d_woff, l->h_woff, n * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
   CUDA_TRY(cudaMemcpyAsync(l->d_wcap, l->h_wcap, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
   if (ctw_launch_best(l->d, g->ranges, g->arcs, g->olabel, g->final_w, l->d_ids, n, l->d_words, l->d_woff,
                       l->d_wcap, l->d_nwords, l->d_tcost, l->d_bstatus, l->stream))
     return fail(-1, std::string("best-path launch: ") + cudaGetErrorString(cudaGetLastError()));
-  l->launches++;
   CUDA_TRY(cudaMemcpyAsync(l->h_nwords, l->d_nwords, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
   CUDA_TRY(cudaMemcpyAsync(l->h_tcost, l->d_tcost, n * sizeof(double), cudaMemcpyDeviceToHost, l->stream));
   CUDA_TRY(cudaMemcpyAsync(l->h_bstatus, l->d_bstatus, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
+  return 0;
+}
+
+int best_words(ctw_lanes* l, long long tot) {
   if (tot) CUDA_TRY(cudaMemcpyAsync(l->h_words, l->d_words, (size_t)tot * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                     l->stream));
   return 0;
+}
+
+int best_enqueue(ctw_lanes* l, int n, const std::vector<int>& caps, bool upload_ids) {
+  long long tot = 0;
+  if (int r = best_host(l, n, caps, &tot)) return r;
+  if (int r = best_device(l, n, upload_ids)) return r;
+  l->launches++;
+  return best_words(l, tot);
 }
 
 // Results of a completed best_enqueue in the reference layout (status 2 = no
@@ -1159,28 +1191,89 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
       l->h_nframes[k] = frames[i];
       l->h_lloff[k] = (long long)ll_offsets[i];
     }
-    CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(l->d_nframes, l->h_nframes, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
-    CUDA_TRY(cudaMemcpyAsync(l->d_lloff, l->h_lloff, m * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
-    CUDA_TRY(cudaEventRecord(l->ev0, l->stream));
     int any_fsa = 0;
     for (int k = 0; k < m; ++k) any_fsa |= l->h[todo[k]].fsa_next != nullptr;
     const bool fast = fast_launch(l, l->h_ids, m);
     l->fast_launches += fast;
-    if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
-                          l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, fast ? 1 : 0, (int)g->ebits,
-                          g->eps_olabel ? 1 : 0, l->stream))
-      return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
-    CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
-    l->launches++;
-    l->decode_launches++;
-    if (bp && round == 0) {
+    // the device work of this round (capturable: fixed sizes for a given m)
+    auto device_round = [&](bool with_best) -> int {
+      CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+      CUDA_TRY(cudaMemcpyAsync(l->d_nframes, l->h_nframes, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
+      CUDA_TRY(cudaMemcpyAsync(l->d_lloff, l->h_lloff, m * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
+      CUDA_TRY(cudaEventRecord(l->ev0, l->stream));
+      if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
+                            l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, fast ? 1 : 0, (int)g->ebits,
+                            g->eps_olabel ? 1 : 0, l->stream))
+        return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
+      CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
       // partial best paths behind the decode (lane ids already on the device)
+      if (with_best)
+        if (int r = best_device(l, m, false)) return r;
+      CUDA_TRY(cudaMemcpyAsync(l->h_out, l->d_out, m * sizeof(CtwLaneOut), cudaMemcpyDeviceToHost, l->stream));
+      return 0;
+    };
+    const bool with_best = bp && round == 0;
+    long long btot = 0;
+    if (with_best) {
       bp->resize(m);
       for (int k = 0; k < m; ++k) (*bp)[k] = l->h[todo[k]].frame_count + l->h_nframes[k] + 8;
-      if (int r = best_enqueue(l, m, *bp, false)) return r;
+      if (int r = best_host(l, m, *bp, &btot)) return r;
     }
-    CUDA_TRY(cudaMemcpyAsync(l->h_out, l->d_out, m * sizeof(CtwLaneOut), cudaMemcpyDeviceToHost, l->stream));
+    // a streaming step (the first round of ctw_advance_best) runs as one CUDA
+    // graph launch: the graph of this launch shape is captured once and
+    // replayed (parameters live in the pinned mirrors it copies from)
+    cudaGraphExec_t exec = nullptr;
+    if (with_best && !l->graphs_off && m <= 64 && getenv("CTW_NO_GRAPH") == nullptr) {
+      {
+        const uintptr_t key[12] = {(uintptr_t)m, (uintptr_t)(fast ? 1 : 0) | (uintptr_t)any_fsa << 1,
+                                   (uintptr_t)dtype, (uintptr_t)width, (uintptr_t)dev_ll, (uintptr_t)l->d,
+                                   (uintptr_t)l->d_ids, (uintptr_t)l->h_ids, (uintptr_t)l->d_woff,
+                                   (uintptr_t)l->h_woff, (uintptr_t)l->d_words, (uintptr_t)l->h_out};
+        for (auto& sg : l->step_graphs)
+          if (std::equal(key, key + 12, sg.key)) exec = sg.exec;
+        if (!exec) {
+          cudaGraph_t graph = nullptr;
+          int rc = (int)cudaStreamBeginCapture(l->stream, cudaStreamCaptureModeThreadLocal);
+          if (rc == 0) {
+            rc = device_round(true);
+            cudaGraph_t gr = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(l->stream, &gr);
+            graph = gr;
+            if (rc == 0 && ec != cudaSuccess) rc = (int)ec;
+          }
+          if (rc == 0 && graph && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+            exec = nullptr;
+            rc = -1;
+          }
+          if (graph) cudaGraphDestroy(graph);
+          (void)cudaGetLastError();
+          if (rc != 0 || !exec) {
+            l->graphs_off = true;  // capture not possible here: plain stream launches from now on
+            exec = nullptr;
+          } else {
+            if (l->step_graphs.size() >= 32) {
+              cudaGraphExecDestroy(l->step_graphs.front().exec);
+              l->step_graphs.erase(l->step_graphs.begin());
+            }
+            ctw_lanes::StepGraph sg;
+            std::copy(key, key + 12, sg.key);
+            sg.exec = exec;
+            l->step_graphs.push_back(sg);
+            l->graph_builds++;
+          }
+        }
+      }
+    }
+    if (exec) {
+      CUDA_TRY(cudaGraphLaunch(exec, l->stream));
+      l->graph_launches++;
+    } else {
+      if (int r = device_round(with_best)) return r;
+    }
+    if (with_best)
+      if (int r = best_words(l, btot)) return r;
+    l->launches += with_best ? 2 : 1;
+    l->decode_launches++;
     CUDA_TRY(cudaStreamSynchronize(l->stream));
     const clk::time_point tw = clk::now();
     l->h_wait += secs(tl, tw);
@@ -1292,6 +1385,14 @@ int ctw_lanes_search_info(ctw_lanes* l, int64_t* out3) {
   out3[0] = l->search;
   out3[1] = l->fast_launches;
   out3[2] = l->decode_launches;
+  return 0;
+}
+
+int ctw_lanes_graph_info(ctw_lanes* l, int64_t* out3) {
+  std::lock_guard<std::mutex> lk(l->mu);
+  out3[0] = l->graph_launches;
+  out3[1] = l->graph_builds;
+  out3[2] = l->graphs_off ? 1 : 0;
   return 0;
 }
 

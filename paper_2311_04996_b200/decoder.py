@@ -368,6 +368,12 @@ class LanePool:
         _lib.load().ctw_lanes_search_info(self.handle, _lib.ptr(v))
         return {"search": SEARCH_MODES[int(v[0])], "fast_launches": int(v[1]), "decode_launches": int(v[2])}
 
+    def graph_info(self) -> dict:
+        """Streaming steps launched as one CUDA graph (ctw_lanes_graph_info)."""
+        v = np.zeros(3, np.int64)
+        _lib.load().ctw_lanes_graph_info(self.handle, _lib.ptr(v))
+        return {"graph_launches": int(v[0]), "graphs_captured": int(v[1]), "graphs_off": bool(v[2])}
+
 
 # ---------------------------------------------------- loglik marshalling ---
 

@@ -488,3 +488,35 @@ def test_stream_partials_equal_offline_prefix_decodes(search):
         want = decode_batch(s.graph, cfg, [utts[k][:h.frame_count]], search=search)[0]
         assert h == want
     assert len(partials) == 4 * 6
+
+
+@pytest.mark.parametrize("search", ["exact", "fast"])
+def test_stream_step_graph_equals_stream_launches(monkeypatch, search):
+    """A streaming step's first round runs as one CUDA graph launch (uploads,
+    frame kernel, partial best paths, result copies). The graph path is the
+    one taken, and its partial hypotheses equal those of plain stream
+    launches (CTW_NO_GRAPH=1), chunk for chunk."""
+    from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, StreamPool, synth
+
+    s = _system(num_units=30, num_words=50, order=2, seed=2)
+    utts = synth.planted_utterances(s, 5, 48, seed=3)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    out = {}
+    for mode in ("graph", "plain"):
+        if mode == "plain":
+            monkeypatch.setenv("CTW_NO_GRAPH", "1")
+        pool = StreamPool(s.graph, cfg, BatcherConfig(max_batch=5), search=search)
+        lp = s.graph.device_graph(0).pool(cfg, s.graph.num_states, search)
+        g0 = lp.graph_info()
+        sids = [pool.create_stream() for _ in utts]
+        got = []
+        for i in range(0, 48, 6):
+            for sid, u in zip(sids, utts):
+                pool.push_chunk(Chunk(sid, u[i:i + 6], is_last=i + 6 >= 48))
+            got.append(sorted((sids.index(sid), h.words, h.total_cost, h.frame_count) for sid, h in pool.step()))
+        g1 = lp.graph_info()
+        out[mode] = (got, g1["graph_launches"] - g0["graph_launches"])
+        pool.close()
+    assert not lp.graph_info()["graphs_off"]
+    assert out["graph"][1] >= 6 and out["plain"][1] == 0
+    assert out["graph"][0] == out["plain"][0]
