@@ -137,10 +137,12 @@ def check(rc: int, what: str) -> int:
     return rc
 
 
-def ptr(a) -> C.c_void_p | None:
+def ptr(a) -> int | None:
+    """Address of a numpy array's data (c_void_p arguments take the int:
+    ~10x cheaper than ctypes.data_as on the per-chunk streaming path)."""
     if a is None:
         return None
-    return a.ctypes.data_as(C.c_void_p)
+    return a.ctypes.data
 
 
 def take_export(e: CtwExport, free: bool = True) -> dict:

@@ -1196,16 +1196,19 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
     const bool fast = fast_launch(l, l->h_ids, m);
     l->fast_launches += fast;
     // the device work of this round (capturable: fixed sizes for a given m)
-    auto device_round = [&](bool with_best) -> int {
+    // (under stream capture the timing events must be external event nodes:
+    // a plain record only orders the capture)
+    auto device_round = [&](bool with_best, bool capture) -> int {
+      const unsigned evf = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
       CUDA_TRY(cudaMemcpyAsync(l->d_ids, l->h_ids, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
       CUDA_TRY(cudaMemcpyAsync(l->d_nframes, l->h_nframes, m * sizeof(int), cudaMemcpyHostToDevice, l->stream));
       CUDA_TRY(cudaMemcpyAsync(l->d_lloff, l->h_lloff, m * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
-      CUDA_TRY(cudaEventRecord(l->ev0, l->stream));
+      CUDA_TRY(cudaEventRecordWithFlags(l->ev0, l->stream, evf));
       if (ctw_launch_decode(l->d, g->ranges, g->arcs, g->olabel, g->final_w, dev_ll, dtype, width, l->d_lloff,
                             l->d_nframes, l->d_ids, m, &l->dcfg, l->d_out, any_fsa, fast ? 1 : 0, (int)g->ebits,
                             g->eps_olabel ? 1 : 0, l->stream))
         return fail(-1, std::string("decode launch: ") + cudaGetErrorString(cudaGetLastError()));
-      CUDA_TRY(cudaEventRecord(l->ev1, l->stream));
+      CUDA_TRY(cudaEventRecordWithFlags(l->ev1, l->stream, evf));
       // partial best paths behind the decode (lane ids already on the device)
       if (with_best)
         if (int r = best_device(l, m, false)) return r;
@@ -1235,7 +1238,7 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
           cudaGraph_t graph = nullptr;
           int rc = (int)cudaStreamBeginCapture(l->stream, cudaStreamCaptureModeThreadLocal);
           if (rc == 0) {
-            rc = device_round(true);
+            rc = device_round(true, true);
             cudaGraph_t gr = nullptr;
             const cudaError_t ec = cudaStreamEndCapture(l->stream, &gr);
             graph = gr;
@@ -1268,7 +1271,7 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
       CUDA_TRY(cudaGraphLaunch(exec, l->stream));
       l->graph_launches++;
     } else {
-      if (int r = device_round(with_best)) return r;
+      if (int r = device_round(with_best, false)) return r;
     }
     if (with_best)
       if (int r = best_words(l, btot)) return r;

@@ -679,40 +679,44 @@ def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: 
     without re-copying it. ``with_best``: ctw_advance_best -- the partial
     best paths come back from the same call; returns (errors, hypotheses)."""
     n = len(states)
-    ids = np.asarray([s._lane for s in states], np.int32)
-    frames = np.asarray([m.shape[0] for m in mats], np.int32)
+    frame_list = [m.shape[0] for m in mats]
     width = int(mats[0].shape[1])
-    status = np.zeros(n, np.int32)
-    err = np.zeros(n, np.int32)
-    buf, offs, base, dcode, loc = _pack_rows(mats, on_dev, packed, frames, width)
-    keep = buf
     L = _lib.load()
     if with_best:
-        cap = int(sum(s.frame_count for s in states) + int(frames.sum()) + 8 * n) + 16
-        words = np.zeros(cap, np.int32)
-        woff = np.zeros(n + 1, np.int64)
-        cost = np.zeros(n, np.float64)
-        fc = np.zeros(n, np.int64)
-        bst = np.zeros(n, np.int32)
-        rc = L.ctw_advance_best(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc, _lib.ptr(offs),
-                                _lib.ptr(frames), width, _lib.ptr(status), _lib.ptr(err), _lib.ptr(words), cap,
-                                _lib.ptr(woff), _lib.ptr(cost), _lib.ptr(fc), _lib.ptr(bst))
+        cap = int(sum(s.frame_count for s in states) + sum(frame_list) + 8 * n) + 16
+        ids = np.asarray([s._lane for s in states], np.int32)
+        frames = np.asarray(frame_list, np.int32)
+        status, err, bst = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int32)
+        woff, fc, cost = np.empty(n + 1, np.int64), np.empty(n, np.int64), np.empty(n, np.float64)
+        words = np.empty(cap, np.int32)
+        buf, offs, base, dcode, loc = _pack_rows(mats, on_dev, packed, frames, width)
+        keep = buf
+        p = _lib.ptr
+        rc = L.ctw_advance_best(pool.handle, p(ids), n, base, dcode, loc, p(offs), p(frames), width, p(status),
+                                p(err), p(words), cap, p(woff), p(cost), p(fc), p(bst))
         if rc != -2:
             _lib.check(rc, "advance")
     else:
+        ids = np.asarray([s._lane for s in states], np.int32)
+        frames = np.asarray(frame_list, np.int32)
+        status = np.zeros(n, np.int32)
+        err = np.zeros(n, np.int32)
+        buf, offs, base, dcode, loc = _pack_rows(mats, on_dev, packed, frames, width)
+        keep = buf
         _lib.check(L.ctw_advance(pool.handle, _lib.ptr(ids), n, C.c_void_p(base), dcode, loc,
                                  _lib.ptr(offs), _lib.ptr(frames), width, _lib.ptr(status),
                                  _lib.ptr(err)), "advance")
     del keep
     errors = []
+    st_l, er_l = status.tolist(), err.tolist()
     for i, s in enumerate(states):
         s._cache = None
-        if status[i] == _lib.OK:
-            s.frame_count += int(frames[i])
+        if st_l[i] == _lib.OK:
+            s.frame_count += frame_list[i]
             errors.append(None)
         else:
             try:
-                _raise_status(int(status[i]), s.frame_count + int(err[i]))
+                _raise_status(st_l[i], s.frame_count + er_l[i])
             except (DecodeError, MemoryError) as e:
                 errors.append(e)
     if raise_first:
@@ -728,14 +732,15 @@ def _advance_lanes(pool: LanePool, states: Sequence[DecodeState], mats, on_dev: 
 
 def _hyps_from(n, words, woff, cost, fc, st) -> list:
     out = []
+    # (one conversion to Python objects per array, then plain list slicing)
+    wl, ol, cl, fl, sl = words[:int(woff[n])].tolist(), woff.tolist(), cost.tolist(), fc.tolist(), st.tolist()
     for i in range(n):
-        if st[i] == 2:
+        if sl[i] == 2:
             out.append(DecodeError("no frames decoded"))
-        elif st[i] == 1:
+        elif sl[i] == 1:
             out.append(DecodeError("no surviving hypotheses"))
         else:
-            out.append(Hypothesis(words=tuple(int(w) for w in words[woff[i]:woff[i + 1]]),
-                                  total_cost=float(cost[i]), frame_count=int(fc[i])))
+            out.append(Hypothesis(words=tuple(wl[ol[i]:ol[i + 1]]), total_cost=cl[i], frame_count=fl[i]))
     return out
 
 
