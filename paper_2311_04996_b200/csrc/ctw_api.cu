@@ -43,7 +43,7 @@ extern "C" int ctw_launch_seed(CtwLane*, const CtwStateRange*, const CtwArc*, co
                                cudaStream_t);
 extern "C" int ctw_launch_best(const CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*,
                                const double*, const int*, int, int32_t*, const long long*, const int*,
-                               int*, double*, int*, cudaStream_t);
+                               int*, double*, int*, CtwBpCache, cudaStream_t);
 extern "C" int ctw_launch_clear(CtwTok*, uint32_t, cudaStream_t);
 extern "C" int ctw_launch_hist_mark(const CtwLane*, const int*, uint32_t* const*, int, cudaStream_t);
 extern "C" int ctw_launch_hist_compact(CtwLane*, const int*, uint32_t* const*, int32_t* const*,
@@ -213,10 +213,14 @@ struct ctw_lanes {
   // parameter uploads, the frame kernel, the partial best paths and the
   // result copies as one graph launch), keyed by launch shape and buffers
   struct StepGraph {
-    uintptr_t key[12];
+    uintptr_t key[13];
     cudaGraphExec_t exec;
   };
   std::vector<StepGraph> step_graphs;
+  // best-path caches of the streaming path (allocated on first use, for
+  // bpc_lanes lanes; see CtwBpCache)
+  CtwBpCache bpc{nullptr, nullptr, nullptr, nullptr, 0};
+  int bpc_lanes = 0;
   bool graphs_off = false;
   int64_t graph_launches = 0, graph_builds = 0;
   std::mutex mu;
@@ -404,6 +408,34 @@ int ensure_scratch(ctw_lanes* l, int n) {
   CUDA_TRY(cudaMallocHost((void**)&l->h_lloff, c * sizeof(long long)));
   CUDA_TRY(cudaMallocHost((void**)&l->h_out, c * sizeof(CtwLaneOut)));
   l->scratch_cap = c;
+  return 0;
+}
+
+// Best-path caches for every lane of the set (streaming path): allocated on
+// first use, re-allocated (all empty) when the set grew.
+int bpc_ensure(ctw_lanes* l) {
+  if (l->bpc_lanes >= l->n) return 0;
+  dfree(l->bpc.n);
+  dfree(l->bpc.rec);
+  dfree(l->bpc.cum);
+  dfree(l->bpc.words);
+  l->bpc_lanes = 0;
+  l->bpc.lanes = 0;
+  const size_t c = (size_t)l->cap;
+  CUDA_TRY(dalloc(&l->bpc.n, c));
+  CUDA_TRY(dalloc(&l->bpc.rec, c * CTW_BPC_REC));
+  CUDA_TRY(dalloc(&l->bpc.cum, c * CTW_BPC_REC));
+  CUDA_TRY(dalloc(&l->bpc.words, c * CTW_BPC_WORDS));
+  CUDA_TRY(cudaMemsetAsync(l->bpc.n, 0, c * sizeof(int32_t), l->stream));
+  l->bpc_lanes = l->cap;
+  l->bpc.lanes = l->cap;
+  return 0;
+}
+
+// Empty a lane's best-path cache (its history was reset or renumbered).
+int bpc_clear(ctw_lanes* l, int lane) {
+  if (l->bpc.n && lane < l->bpc_lanes)
+    CUDA_TRY(cudaMemsetAsync(l->bpc.n + lane, 0, sizeof(int32_t), l->stream));
   return 0;
 }
 
@@ -830,6 +862,10 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   for (void* p : {(void*)l->h_ids, (void*)l->h_nframes, (void*)l->h_lloff, (void*)l->h_out, (void*)l->h_woff,
                   (void*)l->h_wcap, (void*)l->h_nwords, (void*)l->h_tcost, (void*)l->h_bstatus, (void*)l->h_words})
     if (p) cudaFreeHost(p);
+  dfree(l->bpc.n);
+  dfree(l->bpc.rec);
+  dfree(l->bpc.cum);
+  dfree(l->bpc.words);
   for (auto& sg : l->step_graphs) cudaGraphExecDestroy(sg.exec);
   l->step_graphs.clear();
   if (l->ev0) cudaEventDestroy(l->ev0);
@@ -882,6 +918,7 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
     L.n_rec = 0;
     L.pend_valid = 0;
     l->compacted[lane] = 0;
+    if (int r = bpc_clear(l, lane)) return r;
     trim_hist(l, lane);
     if (int r = sync_lane(l, lane)) return r;
   }
@@ -1052,7 +1089,7 @@ int best_device(ctw_lanes* l, int n, bool upload_ids) {
   CUDA_TRY(cudaMemcpyAsync(l->d_woff, l->h_woff, n * sizeof(long long), cudaMemcpyHostToDevice, l->stream));
   CUDA_TRY(cudaMemcpyAsync(l->d_wcap, l->h_wcap, n * sizeof(int), cudaMemcpyHostToDevice, l->stream));
   if (ctw_launch_best(l->d, g->ranges, g->arcs, g->olabel, g->final_w, l->d_ids, n, l->d_words, l->d_woff,
-                      l->d_wcap, l->d_nwords, l->d_tcost, l->d_bstatus, l->stream))
+                      l->d_wcap, l->d_nwords, l->d_tcost, l->d_bstatus, l->bpc, l->stream))
     return fail(-1, std::string("best-path launch: ") + cudaGetErrorString(cudaGetLastError()));
   CUDA_TRY(cudaMemcpyAsync(l->h_nwords, l->d_nwords, n * sizeof(int), cudaMemcpyDeviceToHost, l->stream));
   CUDA_TRY(cudaMemcpyAsync(l->h_tcost, l->d_tcost, n * sizeof(double), cudaMemcpyDeviceToHost, l->stream));
@@ -1218,6 +1255,7 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
     const bool with_best = bp && round == 0;
     long long btot = 0;
     if (with_best) {
+      if (int r = bpc_ensure(l)) return r;
       bp->resize(m);
       for (int k = 0; k < m; ++k) (*bp)[k] = l->h[todo[k]].frame_count + l->h_nframes[k] + 8;
       if (int r = best_host(l, m, *bp, &btot)) return r;
@@ -1228,12 +1266,13 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
     cudaGraphExec_t exec = nullptr;
     if (with_best && !l->graphs_off && m <= 64 && getenv("CTW_NO_GRAPH") == nullptr) {
       {
-        const uintptr_t key[12] = {(uintptr_t)m, (uintptr_t)(fast ? 1 : 0) | (uintptr_t)any_fsa << 1,
+        const uintptr_t key[13] = {(uintptr_t)m, (uintptr_t)(fast ? 1 : 0) | (uintptr_t)any_fsa << 1,
                                    (uintptr_t)dtype, (uintptr_t)width, (uintptr_t)dev_ll, (uintptr_t)l->d,
                                    (uintptr_t)l->d_ids, (uintptr_t)l->h_ids, (uintptr_t)l->d_woff,
-                                   (uintptr_t)l->h_woff, (uintptr_t)l->d_words, (uintptr_t)l->h_out};
+                                   (uintptr_t)l->h_woff, (uintptr_t)l->d_words, (uintptr_t)l->h_out,
+                                   (uintptr_t)l->bpc.n};
         for (auto& sg : l->step_graphs)
-          if (std::equal(key, key + 12, sg.key)) exec = sg.exec;
+          if (std::equal(key, key + 13, sg.key)) exec = sg.exec;
         if (!exec) {
           cudaGraph_t graph = nullptr;
           int rc = (int)cudaStreamBeginCapture(l->stream, cudaStreamCaptureModeThreadLocal);
@@ -1259,7 +1298,7 @@ int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* l
               l->step_graphs.erase(l->step_graphs.begin());
             }
             ctw_lanes::StepGraph sg;
-            std::copy(key, key + 12, sg.key);
+            std::copy(key, key + 13, sg.key);
             sg.exec = exec;
             l->step_graphs.push_back(sg);
             l->graph_builds++;
@@ -1493,6 +1532,7 @@ int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* 
     L.rcap = (int64_t)l->hpages[lane].size() * CTW_PAGE;
     L.n_rec = kv[i];
     l->compacted[lane] = 1;
+    if (int r = bpc_clear(l, lane)) return r;
     if (kept) kept[i] = kv[i];
     if (int r = sync_lane(l, lane)) return r;
     sfree(marks[i], st);

@@ -186,6 +186,21 @@ struct CtwLatArc {
   int32_t src_state;
 };
 
+// Best-path cache (streaming partial hypotheses): per lane the labelled
+// records of the previous best path (ascending), the word count through each
+// and its words, in fixed-size per-lane slices of three slabs; n[lane] = 0
+// means empty. Written by k_best_path only; the host empties a lane's cache
+// when its history is reset or renumbered.
+#define CTW_BPC_REC 2048
+#define CTW_BPC_WORDS 8192
+struct CtwBpCache {
+  int32_t* n;      // [lanes]
+  int32_t* rec;    // [lanes * CTW_BPC_REC]
+  int32_t* cum;    // [lanes * CTW_BPC_REC]
+  int32_t* words;  // [lanes * CTW_BPC_WORDS]
+  int32_t lanes;   // lanes covered (a lane id >= lanes has no cache)
+};
+
 // Epsilon-closure index entry (lattice kernel): for every state s, the
 // states reachable from s over epsilon arcs (s itself first) with the
 // minimum path weight from s. Built on the device once per graph when no

@@ -2159,11 +2159,15 @@ __global__ void __launch_bounds__(CTW_BS) k_seed(CtwLane* lanes, GraphDev g, con
 // records. Words are written oldest-first into words[woff[b] .. + cap[b]);
 // nwords[b] always receives the true length (host retries when too small).
 #define CTW_BPB 256  // best path: threads per lane (the argmin over up to max_active tokens)
+#define CTW_BPC_NEW 512  // best-path cache: records walked per call that can be cached
+#define CTW_BPU 4  // best path: tokens per thread per round of the argmin
 __global__ void __launch_bounds__(CTW_BPB) k_best_path(const CtwLane* lanes, GraphDev g, const int* lane_ids, int n,
                                                       int32_t* words, const long long* woff, const int* wcap,
-                                                      int* nwords, double* total_cost, int* status) {
+                                                      int* nwords, double* total_cost, int* status, CtwBpCache bc) {
   __shared__ double s_best[CTW_BPB / 32];
   __shared__ int s_state[CTW_BPB / 32], s_i[CTW_BPB / 32];
+  __shared__ int32_t s_crec[CTW_BPC_REC];             // the lane's cached best path (record indices, ascending)
+  __shared__ int32_t s_new[CTW_BPC_NEW], s_cnt[CTW_BPC_NEW];  // records walked this time (newest first), words each
   const int warp = blockIdx.x;  // (the batch entry)
   const int ln = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (warp >= n) return;
@@ -2176,22 +2180,39 @@ __global__ void __launch_bounds__(CTW_BPB) k_best_path(const CtwLane* lanes, Gra
   auto better = [](double ob, int os, int oi, double b, int bs, int bi) {
     return oi >= 0 && (bi < 0 || ob < b || (ob == b && os < bs));
   };
+  const int nsrc = lane.n_src;
   for (int pass = 0; pass < 2 && best_i < 0; ++pass) {
-    for (int i = threadIdx.x; i < lane.n_src; i += CTW_BPB) {
-      const CtwSrc t = src[i];
-      double tot;
-      if (pass == 0) {
-        const double fw = g.final_w[(uint32_t)t.state & lane.smask];
-        if (fw == INF) continue;
-        tot = t.cost + fw;
-      } else {
-        tot = t.cost;
-        if (!(tot < INF)) continue;
+    // CTW_BPU tokens per thread per round, their loads issued together (the
+    // scan is a few dependent round trips instead of one per token)
+    for (int i0 = threadIdx.x; i0 < nsrc; i0 += CTW_BPB * CTW_BPU) {
+      int st[CTW_BPU];
+      double c[CTW_BPU], fw[CTW_BPU];
+#pragma unroll
+      for (int u = 0; u < CTW_BPU; ++u) {
+        const int i = i0 + u * CTW_BPB;
+        st[u] = i < nsrc ? src[i].state : 0;
+        c[u] = i < nsrc ? src[i].cost : INF;
       }
-      if (tot < best || (tot == best && t.state < best_state)) {
-        best = tot;
-        best_state = t.state;
-        best_i = i;
+#pragma unroll
+      for (int u = 0; u < CTW_BPU; ++u)
+        fw[u] = (pass == 0 && i0 + u * CTW_BPB < nsrc) ? g.final_w[(uint32_t)st[u] & lane.smask] : 0.0;
+#pragma unroll
+      for (int u = 0; u < CTW_BPU; ++u) {
+        const int i = i0 + u * CTW_BPB;
+        if (i >= nsrc) continue;
+        double tot;
+        if (pass == 0) {
+          if (fw[u] == INF) continue;
+          tot = c[u] + fw[u];
+        } else {
+          tot = c[u];
+          if (!(tot < INF)) continue;
+        }
+        if (tot < best || (tot == best && st[u] < best_state)) {
+          best = tot;
+          best_state = st[u];
+          best_i = i;
+        }
       }
     }
     for (int o = 16; o; o >>= 1) {
@@ -2230,47 +2251,105 @@ __global__ void __launch_bounds__(CTW_BPB) k_best_path(const CtwLane* lanes, Gra
     }
     return;
   }
-  // one walk of the prev chain (lane 0): words are written newest-first from
-  // the end of the lane's window, then the warp moves them to its start
+  // one walk of the labelled-record chain (lane 0): words are written
+  // newest-first at the end of the lane's window, then the warp moves them
+  // into place. With a best-path cache (streaming: ctw_advance_best), the
+  // walk stops at the first record on the lane's previous best path -- its
+  // ancestry is that path's prefix, whose words are copied from the cache --
+  // so a step costs one hop per new word instead of one per word so far.
+  const int lid = lane_ids[warp];
+  const bool cached = bc.n != nullptr && lid < bc.lanes;
+  const int cn = cached ? bc.n[lid] : 0;
+  const int32_t* crec = cached ? bc.rec + (size_t)lid * CTW_BPC_REC : nullptr;
+  for (int k = ln; k < cn; k += 32) s_crec[k] = crec[k];
+  __syncwarp();
   const int cap = wcap[warp];
   int32_t* w = words + woff[warp];
-  int pos = cap, count = 0;
+  int pos = cap, count = 0, hit = -1, nnew = 0, pre = 0;
   if (ln == 0) {
     status[warp] = 0;
     total_cost[warp] = best;
     // labelled records only: anc / plab skip the frames without output labels
     for (int r = src[best_i].anc; r >= 0;) {
+      if (cn > 0 && r <= s_crec[cn - 1]) {
+        int lo = 0, hi = cn - 1;  // binary search of r in the cached path
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_crec[mid] < r) lo = mid + 1;
+          else hi = mid;
+        }
+        if (s_crec[lo] == r) {
+          hit = lo;
+          break;
+        }
+      }
       const CtwRecPage* pg = lane.pages[r >> CTW_PAGE_LOG2];
       const int2 lk = pg->link[r & (CTW_PAGE - 1)];
       const int nxt = pg->plab[r & (CTW_PAGE - 1)];
       const int c = lk.y;
+      int m = 0;
       if (c > 0) {
         if (pos > 0) w[pos - 1] = c;
         --pos;
-        ++count;
+        m = 1;
       } else if (c < 0) {
         const int32_t* seg = lane.pool + (-c - 1);
-        const int m = seg[0];
+        m = seg[0];
         for (int j = m - 1; j >= 0; --j) {
           if (pos > 0) w[pos - 1] = seg[1 + j];
           --pos;
         }
-        count += m;
       }
+      count += m;
+      if (nnew < CTW_BPC_NEW) {
+        s_new[nnew] = r;
+        s_cnt[nnew] = m;
+      }
+      ++nnew;
       r = nxt;
     }
-    nwords[warp] = count;  // > cap: the host retries with a bigger window
+    pre = hit >= 0 ? bc.cum[(size_t)lid * CTW_BPC_REC + hit] : 0;
+    nwords[warp] = pre + count;  // > cap: the host retries with a bigger window
   }
   count = __shfl_sync(0xFFFFFFFFu, count, 0);
   pos = __shfl_sync(0xFFFFFFFFu, pos, 0);
-  if (count > cap || pos == 0) return;
+  pre = __shfl_sync(0xFFFFFFFFu, pre, 0);
+  hit = __shfl_sync(0xFFFFFFFFu, hit, 0);
+  nnew = __shfl_sync(0xFFFFFFFFu, nnew, 0);
+  if (pre + count > cap) return;
   __syncwarp();
-  for (int k = 0; k < count; k += 32) {
-    const int32_t v = (k + ln < count) ? w[pos + k + ln] : 0;
-    __syncwarp();
-    if (k + ln < count) w[k + ln] = v;
-    __syncwarp();
+  // new words to [pre, pre + count) (forward, chunk read before written:
+  // the destination never overtakes the unread source)
+  if (pos != pre)
+    for (int k = 0; k < count; k += 32) {
+      const int32_t v = (k + ln < count) ? w[pos + k + ln] : 0;
+      __syncwarp();
+      if (k + ln < count) w[pre + k + ln] = v;
+      __syncwarp();
+    }
+  if (!cached) return;
+  int32_t* cw = bc.words + (size_t)lid * CTW_BPC_WORDS;
+  for (int k = ln; k < pre; k += 32) w[k] = cw[k];
+  // the new path into the cache: the kept prefix, then the walked records
+  // oldest first (a path too long for the cache leaves it empty)
+  const int base = hit + 1;
+  const bool fits = nnew <= CTW_BPC_NEW && base + nnew <= CTW_BPC_REC && pre + count <= CTW_BPC_WORDS;
+  if (fits) {
+    int32_t* rec = bc.rec + (size_t)lid * CTW_BPC_REC;
+    int32_t* cum = bc.cum + (size_t)lid * CTW_BPC_REC;
+    if (ln == 0) {
+      int acc = pre;
+      for (int j = 0; j < nnew; ++j) {
+        const int k = nnew - 1 - j;
+        acc += s_cnt[k];
+        rec[base + j] = s_new[k];
+        cum[base + j] = acc;
+      }
+    }
+    for (int k = ln; k < count; k += 32) cw[pre + k] = w[pre + k];
   }
+  __syncwarp();
+  if (ln == 0) bc.n[lid] = fits ? base + nnew : 0;
 }
 
 __global__ void k_clear_table(CtwTok* T, uint32_t n) {
@@ -2381,10 +2460,10 @@ extern "C" int ctw_launch_seed(CtwLane* d_lanes, const CtwStateRange* ranges, co
 extern "C" int ctw_launch_best(const CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                const int32_t* olabel, const double* final_w, const int* lane_ids, int n,
                                int32_t* words, const long long* woff, const int* wcap, int* nwords, double* total_cost,
-                               int* status, cudaStream_t stream) {
+                               int* status, CtwBpCache bc, cudaStream_t stream) {
   GraphDev g{ranges, arcs, olabel, final_w};
   (void)cudaGetLastError();
-  k_best_path<<<n, CTW_BPB, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap, nwords, total_cost, status);
+  k_best_path<<<n, CTW_BPB, 0, stream>>>(d_lanes, g, lane_ids, n, words, woff, wcap, nwords, total_cost, status, bc);
   return (int)cudaGetLastError();
 }
 

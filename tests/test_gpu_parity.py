@@ -520,3 +520,44 @@ def test_stream_step_graph_equals_stream_launches(monkeypatch, search):
     assert not lp.graph_info()["graphs_off"]
     assert out["graph"][1] >= 6 and out["plain"][1] == 0
     assert out["graph"][0] == out["plain"][0]
+
+
+@pytest.mark.parametrize("chunk", [1, 5])
+def test_stream_partials_with_best_path_cache(chunk):
+    """Streaming partial hypotheses come from k_best_path with the per-lane
+    best-path cache (the walk stops where it meets the previous step's best
+    path and copies that prefix's words). On a random graph whose epsilon
+    and emitting arcs both carry output labels (multi-label records), every
+    partial equals the offline decode of the same prefix (fresh lanes: a
+    full walk), with 1-frame chunks that reuse the cache on every step."""
+    from paper_2311_04996_b200 import BatcherConfig, Chunk, DecoderConfig, FlatGraph, StreamPool, decode_batch
+
+    rng = np.random.default_rng(11)
+    S, V, W = 60, 6, 25
+    src, il, ol, w, ns = [], [], [], [], []
+    for s_ in range(S):
+        for _ in range(int(rng.integers(1, 4))):  # emitting arcs
+            src.append(s_); il.append(int(rng.integers(1, V + 1)))
+            ol.append(int(rng.integers(1, W + 1)) if rng.random() < 0.4 else 0)
+            w.append(float(rng.uniform(0.0, 2.0))); ns.append(int(rng.integers(0, S)))
+        if rng.random() < 0.5:  # a labelled or unlabelled epsilon arc to a later state
+            src.append(s_); il.append(0); ol.append(int(rng.integers(1, W + 1)) if rng.random() < 0.5 else 0)
+            w.append(float(rng.uniform(0.1, 1.0))); ns.append(int(rng.integers(s_ + 1, S + 1)) % S if s_ + 1 < S else 0)
+    final = np.where(rng.random(S) < 0.3, rng.uniform(0, 1, S), np.inf)
+    fg = FlatGraph.from_arrays(S, 0, src, il, ol, w, ns, final)
+    utts = [rng.normal(-2.0, 1.0, size=(60, V)) for _ in range(3)]
+    cfg = DecoderConfig(beam=8.0, max_active=200)
+    pool = StreamPool(fg, cfg, BatcherConfig(max_batch=3), search="exact")
+    sids = [pool.create_stream() for _ in utts]
+    partials = []
+    for i in range(0, 60, chunk):
+        for sid, u in zip(sids, utts):
+            pool.push_chunk(Chunk(sid, u[i:i + chunk], is_last=i + chunk >= 60))
+        partials += [(sids.index(sid), h) for sid, h in pool.step()]
+    pool.close()
+    multi = 0
+    for k, h in partials:
+        want = decode_batch(fg, cfg, [utts[k][:h.frame_count]])[0]
+        assert h == want
+        multi += len(h.words) > 1
+    assert multi > 10
