@@ -5,4 +5,4 @@ timeout 1200 python bench.py > gpurun_out/final_c2.json 2> gpurun_out/final_c2.e
 timeout 1200 python bench.py --config c3 --streams 0 --lattice 0 > gpurun_out/final_c3.json 2> gpurun_out/final_c3.err
 timeout 1200 python bench.py --config c5 --streams 0 --lattice 0 > gpurun_out/final_c5.json 2> gpurun_out/final_c5.err
 timeout 900 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err
-bash tools/prof.sh r2c fast
+[ "${SKIP_PROF:-0}" = 1 ] || bash tools/prof.sh r2c fast
