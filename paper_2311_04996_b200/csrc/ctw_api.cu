@@ -1963,7 +1963,8 @@ int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const voi
     if (g->clo_state == 0) {
       const int rc = ctw_build_closure_index(g->ranges, g->arcs, g->S, &g->clo_off, &g->clo_ent, &g->clo_n,
                                              l->stream);
-      if (rc > 0) return fail(-100 - rc, std::string("closure index: ") + cudaGetErrorString((cudaError_t)rc));
+      if (rc == (int)cudaErrorMemoryAllocation) (void)cudaGetLastError();  // no room for the index: general kernel
+      else if (rc > 0) return fail(-100 - rc, std::string("closure index: ") + cudaGetErrorString((cudaError_t)rc));
       g->clo_state = rc == 0 ? 1 : -1;
     }
   }
