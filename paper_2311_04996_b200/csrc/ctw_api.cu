@@ -45,6 +45,7 @@ extern "C" int ctw_launch_best(const CtwLane*, const CtwStateRange*, const CtwAr
                                const double*, const int*, int, int32_t*, const long long*, const int*,
                                int*, double*, int*, CtwBpCache, cudaStream_t);
 extern "C" int ctw_launch_clear(CtwTok*, uint32_t, cudaStream_t);
+extern "C" int ctw_launch_copy_seeds(const CtwSeedCopy*, int, cudaStream_t);
 extern "C" int ctw_launch_hist_mark(const CtwLane*, const int*, uint32_t* const*, int, cudaStream_t);
 extern "C" int ctw_launch_hist_compact(CtwLane*, const int*, uint32_t* const*, int32_t* const*,
                                        CtwRecPage* const* const*, long long*, int, cudaStream_t);
@@ -160,6 +161,9 @@ struct ctw_lanes {
   std::vector<int32_t> seed_pool;  // label-pool prefix written by the seeding (seed label codes)
   char* lat_pin = nullptr;         // pinned staging of lattice results (grow-only)
   size_t lat_pin_cap = 0;
+  CtwSeedCopy* seedjob_h = nullptr;  // batched seed copies of a reset (pinned / device, grow-only)
+  CtwSeedCopy* seedjob_d = nullptr;
+  int seedjob_cap = 0;
   // phrase automata (ctw_lane_set_fsa), device copies per lane
   std::vector<uint16_t*> fsa_next;
   std::vector<double*> fsa_cost;
@@ -847,6 +851,8 @@ void ctw_lanes_destroy(ctw_lanes* l) {
   cudaStreamSynchronize(l->stream);
   if (l->h) cudaFreeHost(l->h);
   if (l->lat_pin) cudaFreeHost(l->lat_pin);
+  if (l->seedjob_h) cudaFreeHost(l->seedjob_h);
+  dfree(l->seedjob_d);
   dfree(l->d);
   dfree(l->d_ids);
   dfree(l->d_nframes);
@@ -918,17 +924,45 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
     L.n_rec = 0;
     L.pend_valid = 0;
     l->compacted[lane] = 0;
-    if (int r = bpc_clear(l, lane)) return r;
     trim_hist(l, lane);
-    if (int r = sync_lane(l, lane)) return r;
+  }
+  // descriptor uploads and cache clears per run of consecutive lane ids
+  {
+    std::vector<int> sorted(ids);
+    std::sort(sorted.begin(), sorted.end());
+    sorted.erase(std::unique(sorted.begin(), sorted.end()), sorted.end());
+    for (size_t a = 0; a < sorted.size();) {
+      size_t b = a + 1;
+      while (b < sorted.size() && sorted[b] == sorted[b - 1] + 1) ++b;
+      const int lo = sorted[a], cnt = (int)(b - a);
+      CUDA_TRY(cudaMemcpyAsync(&l->d[lo], &l->h[lo], cnt * sizeof(CtwLane), cudaMemcpyHostToDevice, l->stream));
+      if (l->bpc.n && lo + cnt <= l->bpc_lanes)
+        CUDA_TRY(cudaMemsetAsync(l->bpc.n + lo, 0, cnt * sizeof(int32_t), l->stream));
+      else
+        for (int k = lo; k < lo + cnt; ++k)
+          if (int r = bpc_clear(l, k)) return r;
+      a = b;
+    }
   }
   std::vector<int> st;
   if (int r = run_seed(l, ids, st)) return r;
+  // keep the seed tokens (device copies, stream-ordered) for lattices: one
+  // batched copy kernel (run_seed synchronised, so the pinned job list is free)
+  if (n > l->seedjob_cap) {
+    const int c = std::max(n, 2 * l->seedjob_cap);
+    if (l->seedjob_h) cudaFreeHost(l->seedjob_h);
+    dfree(l->seedjob_d);
+    l->seedjob_h = nullptr;
+    l->seedjob_cap = 0;
+    CUDA_TRY(cudaMallocHost((void**)&l->seedjob_h, c * sizeof(CtwSeedCopy)));
+    CUDA_TRY(dalloc(&l->seedjob_d, (size_t)c));
+    l->seedjob_cap = c;
+  }
+  int njobs = 0;
   for (int i = 0; i < n; ++i) {
     status[i] = st[i];
     l->seeded[ids[i]] = st[i] == CTW_OK;
     if (st[i] != CTW_OK) continue;
-    // keep the seed tokens (device copy, stream-ordered) for lattices
     const int lane = ids[i];
     const CtwLane& L = l->h[lane];
     if (L.n_src > l->seed_cap[lane]) {
@@ -941,12 +975,18 @@ int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const doubl
     }
     l->seed_n[lane] = L.n_src;
     l->seed_pool[lane] = L.pool_used;
-    if (L.n_src) {
-      CUDA_TRY(cudaMemcpyAsync(l->seed_src[lane], L.src[L.src_buf], (size_t)L.n_src * sizeof(CtwSrc),
-                               cudaMemcpyDeviceToDevice, l->stream));
-      CUDA_TRY(cudaMemcpyAsync(l->seed_pend[lane], L.pend, (size_t)L.n_src * sizeof(int32_t),
-                               cudaMemcpyDeviceToDevice, l->stream));
-    }
+    if (L.n_src)
+      l->seedjob_h[njobs++] = CtwSeedCopy{l->seed_src[lane], L.src[L.src_buf], l->seed_pend[lane], L.pend,
+                                          L.n_src, 0};
+  }
+  if (njobs) {
+    CUDA_TRY(cudaMemcpyAsync(l->seedjob_d, l->seedjob_h, njobs * sizeof(CtwSeedCopy), cudaMemcpyHostToDevice,
+                             l->stream));
+    if (ctw_launch_copy_seeds(l->seedjob_d, njobs, l->stream))
+      return fail(-1, std::string("seed copy launch: ") + cudaGetErrorString(cudaGetLastError()));
+    // (the job list is pinned host memory read by the copy: the next reset
+    // must not overwrite it before the copy ran)
+    CUDA_TRY(cudaStreamSynchronize(l->stream));
   }
   return 0;
 }

@@ -186,6 +186,16 @@ struct CtwLatArc {
   int32_t src_state;
 };
 
+// One lane's seed-token copy (kept for lattices) in a batched reset.
+struct CtwSeedCopy {
+  CtwSrc* dst_src;
+  const CtwSrc* src_src;
+  int32_t* dst_pend;
+  const int32_t* src_pend;
+  int32_t n;
+  int32_t pad;
+};
+
 // Best-path cache (streaming partial hypotheses): per lane the labelled
 // records of the previous best path (ascending), the word count through each
 // and its words, in fixed-size per-lane slices of three slabs; n[lane] = 0

@@ -111,7 +111,23 @@ __global__ void __launch_bounds__(HG_BS) k_hist_compact(CtwLane* lanes, const in
   if (tid == 0) kept[blockIdx.x] = nk;
 }
 
+// Seed tokens of the lanes of a reset, one CTA per lane (a batch reset
+// would otherwise issue two copies per lane).
+__global__ void k_copy_seeds(const CtwSeedCopy* jobs) {
+  const CtwSeedCopy j = jobs[blockIdx.x];
+  for (int i = threadIdx.x; i < j.n; i += blockDim.x) {
+    j.dst_src[i] = j.src_src[i];
+    j.dst_pend[i] = j.src_pend[i];
+  }
+}
+
 }  // namespace
+
+extern "C" int ctw_launch_copy_seeds(const CtwSeedCopy* d_jobs, int n, cudaStream_t stream) {
+  (void)cudaGetLastError();
+  if (n > 0) k_copy_seeds<<<n, 256, 0, stream>>>(d_jobs);
+  return (int)cudaGetLastError();
+}
 
 extern "C" int ctw_launch_hist_mark(const CtwLane* d_lanes, const int* d_ids, uint32_t* const* d_marks, int n,
                                     cudaStream_t stream) {
