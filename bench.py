@@ -651,6 +651,9 @@ def main():
     if nfile.exists():
         try:
             ncu = json.loads(nfile.read_text())
+            # a capture of another workload is context, not this run's kernel
+            ncu["captured_on"] = "C2 (512 x 250 / 512 x 80), search " + str(ncu.get("search", "fast"))
+            ncu["applies_to_this_run"] = args.config == "c2" and n == 512 and F == 250 and args.search == "fast"
         except ValueError:
             ncu = None
 
