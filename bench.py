@@ -500,9 +500,16 @@ def reference_arm(args):
     for _ in range(args.warmup if args.warmup < 1 else 1):
         cpu_decode(utts[: max(1, cores)], fg, cores, None if boosts is None else boosts[: max(1, cores)])
     times = []
-    for _ in range(args.steps):
-        _, dt = cpu_decode(utts, fg, cores, boosts)
-        times.append(dt)
+    import gc
+
+    gc.collect()
+    gc.disable()  # (the same timing convention as the GPU arm's e2e loop)
+    try:
+        for _ in range(args.steps):
+            _, dt = cpu_decode(utts, fg, cores, boosts)
+            times.append(dt)
+    finally:
+        gc.enable()
     audio = n * args.frames * FRAME_S
     value = audio * len(times) / sum(times)
     k1 = args.ref_w1_sample
