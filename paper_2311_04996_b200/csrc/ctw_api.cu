@@ -31,6 +31,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ctcwfst_b200.h"
 #include "ctw_common.h"
 
@@ -58,6 +60,15 @@ extern "C" int ctw_build_closure_index(const CtwStateRange*, const CtwArc*, long
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around a C-ABI operation (nsys / ncu --nvtx timelines; free
+// when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -634,6 +645,7 @@ int ctw_graph_create(const int64_t* off, const int64_t* eps_end, const int32_t* 
                      const int32_t* olabel, const double* weight, const int32_t* nextstate,
                      const double* final_w, int64_t num_states, int64_t num_arcs, int64_t start,
                      int32_t device, ctw_graph** out) {
+  NvtxRange nvtx_("ctw_graph_create");
   *out = nullptr;
   if (num_states <= 0) return fail(-1, "empty graph");
   if (num_arcs < 0 || num_arcs >= 0x7FFFFFFFLL) return fail(-1, "arc count must be < 2^31");
@@ -891,6 +903,7 @@ int ctw_lanes_reserve(ctw_lanes* l, int32_t n) {
 
 int ctw_lane_reset(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const double* const* boosts,
                    const int64_t* boost_lens, int32_t* status) {
+  NvtxRange nvtx_("ctw_lane_reset");
   std::lock_guard<std::mutex> lk(l->mu);
   CUDA_TRY(cudaSetDevice(l->g->device));
   if (int r = check_ids(l, lane_ids, n)) return r;
@@ -1180,6 +1193,7 @@ int best_finish(ctw_lanes* l, const int32_t* lane_ids, int n, int32_t* words, in
 
 int best_path_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* words, int64_t words_cap,
                    int64_t* word_off, double* total_cost, int64_t* frame_count, int32_t* status) {
+  NvtxRange nvtx_("ctw_best_path");
   ctw_graph* g = l->g;
   CUDA_TRY(cudaSetDevice(g->device));
   if (n <= 0) {
@@ -1215,6 +1229,7 @@ int best_path_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wo
 int advance_impl(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
                  int32_t location, const int64_t* ll_offsets, const int32_t* frames, int32_t width,
                  int32_t* status, int32_t* err_frame, std::vector<int>* bp, bool* bp_valid) {
+  NvtxRange nvtx_("ctw_advance");
   ctw_graph* g = l->g;
   if (bp_valid) *bp_valid = false;
   CUDA_TRY(cudaSetDevice(g->device));
@@ -1497,6 +1512,7 @@ int ctw_best_path(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int32_t* wor
 }
 
 int ctw_lane_compact(ctw_lanes* l, const int32_t* lane_ids, int32_t n, int64_t* kept) {
+  NvtxRange nvtx_("ctw_lane_compact");
   std::lock_guard<std::mutex> lk(l->mu);
   CUDA_TRY(cudaSetDevice(l->g->device));
   if (n <= 0) return 0;
@@ -1962,6 +1978,7 @@ void ctw_lattice_free(ctw_lattice* lat) {
 int ctw_lane_lattice(ctw_lanes* l, const int32_t* lane_ids, int32_t n, const void* loglik, int32_t dtype,
                 int32_t location, const int64_t* ll_offsets, int32_t width, double lattice_beam,
                 ctw_lattice* out) {
+  NvtxRange nvtx_("ctw_lane_lattice");
   std::lock_guard<std::mutex> lk(l->mu);
   ctw_graph* g = l->g;
   CUDA_TRY(cudaSetDevice(g->device));
