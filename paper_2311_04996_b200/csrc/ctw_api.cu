@@ -329,7 +329,11 @@ int grow_hist(ctw_lanes* l, int i, int64_t need) {
     return fail(-1, "channel history would exceed 2^31 records: compact it (DecodeState.compact_history, "
                     "StreamPool(gc_every=...)) or start a new channel");
   auto& pg = l->hpages[i];
-  while ((int64_t)pg.size() * CTW_PAGE < need) {
+  // two pages of headroom beyond the request: a channel that grows by a
+  // chunk at a time (streaming) re-uploads its page table every few chunks
+  // instead of on every one
+  const int64_t want = std::min<int64_t>(need + 2 * (int64_t)CTW_PAGE, (int64_t)INT32_MAX);
+  while ((int64_t)pg.size() * CTW_PAGE < want) {
     CtwRecPage* p = nullptr;
     if (l->free_pages.empty()) {
       // pages come in slabs: one allocation per CTW_SLAB pages
