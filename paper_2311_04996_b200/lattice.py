@@ -19,13 +19,27 @@ distinct word sequences (A* over the kept arcs with exact remaining costs).
 from __future__ import annotations
 
 import ctypes as C
-import weakref
 from typing import Sequence
 
 import numpy as np
 
 from . import _lib
 from .decoder import DecodeFailure, Hypothesis, decode_batch
+
+
+class _CArrays:
+    """Owner of one ctw_lattice's C arrays (freed with the last reference)."""
+
+    __slots__ = ("c", "__weakref__")
+
+    def __init__(self, c: _lib.CtwLattice):
+        self.c = c
+
+    def __del__(self):
+        try:
+            _lib.load().ctw_lattice_free(C.byref(self.c))
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class Lattice:
@@ -36,8 +50,12 @@ class Lattice:
     dst, weight)."""
 
     def __init__(self, c: _lib.CtwLattice, best_path: Hypothesis):
-        self._c = c
-        self._fin = weakref.finalize(self, _lib.load().ctw_lattice_free, C.byref(c))
+        # the arrays below are zero-copy views of the C arrays; one owner
+        # object frees them (ctw_lattice_free) once the lattice and every
+        # array taken from it are gone
+        owner = _CArrays(c)
+        self._owner = owner
+        self._c = owner.c
         self.best_path = best_path
         self.status = int(c.status)
         self.final_mode = bool(c.final_mode)
@@ -48,11 +66,13 @@ class Lattice:
         self.closure_pruned = int(c.closure_pruned)
         ns, na = int(c.n_seeds), int(c.n_arcs)
 
-        def arr(p, n, dt):  # copy of n elements at a C pointer (the C arrays are freed with the lattice)
+        def arr(p, n, dt):  # n elements at a C pointer, kept alive by the owner
             if not n:
                 return np.zeros(0, dt)
             nb = n * np.dtype(dt).itemsize
-            return np.frombuffer((C.c_char * nb).from_address(C.cast(p, C.c_void_p).value), dt).copy()
+            buf = (C.c_char * nb).from_address(C.cast(p, C.c_void_p).value)
+            buf._owner = owner
+            return np.frombuffer(buf, dt)
 
         self.seed_state = arr(c.seed_state, ns, np.int32)
         self.seed_cost = arr(c.seed_cost, ns, np.float64)

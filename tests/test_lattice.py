@@ -348,3 +348,24 @@ def test_closure_index_overflow_reruns_general_kernel():
     inner = lo.kept(ora, beam, -1e-7)
     outer = lo.kept(ora, beam, +1e-7)
     assert len(inner) <= lat.num_arcs <= len(outer)
+
+
+def test_lattice_arrays_are_views_that_outlive_the_lattice():
+    """Lattice arrays are zero-copy views of the C result arrays: they stay
+    valid after the Lattice object is gone (the C arrays are freed with the
+    last view), and equal a copy taken while the lattice was alive."""
+    import gc
+
+    from paper_2311_04996_b200 import DecoderConfig, decode_lattices, synth
+
+    s = _system(num_units=12, num_words=40, order=3, seed=4, min_pron=1, max_pron=4)
+    utts = synth.planted_utterances(s, 3, 30, seed=5, gap=3.0, noise=1.0)
+    lats = decode_lattices(s.graph, DecoderConfig(beam=14.0, max_active=300), utts, lattice_beam=4.0)
+    kept = [(lat.weight, lat.src, lat.label_pool) for lat in lats]
+    copies = [(w.copy(), sr.copy(), lp.copy()) for w, sr, lp in kept]
+    del lats
+    gc.collect()
+    junk = [np.full(1 << 16, 7.0) for _ in range(64)]  # reuse freed heap memory if any was freed early
+    for (w, sr, lp), (w0, sr0, lp0) in zip(kept, copies):
+        assert np.array_equal(w, w0) and np.array_equal(sr, sr0) and np.array_equal(lp, lp0)
+    del junk
