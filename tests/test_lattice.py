@@ -369,3 +369,28 @@ def test_lattice_arrays_are_views_that_outlive_the_lattice():
     for (w, sr, lp), (w0, sr0, lp0) in zip(kept, copies):
         assert np.array_equal(w, w0) and np.array_equal(sr, sr0) and np.array_equal(lp, lp0)
     del junk
+
+
+def test_closure_index_with_phrase_automaton_matches_general_kernel(monkeypatch):
+    """In-search phrase automata put the automaton state in the token key's
+    high bits; the indexed lattice kernel carries them through the closure
+    (epsilon arcs have no labels, so the automaton state is constant along a
+    closure). Its lattices equal the general kernel's arc for arc."""
+    from paper_2311_04996_b200 import DecoderConfig, PhraseBoost, decode_batch, decode_lattices, synth
+
+    s = synth.build_system(synth.SystemSpec(num_units=10, num_words=25, order=2, seed=12, min_pron=1, max_pron=3))
+    utts = synth.planted_utterances(s, 4, 30, seed=8, gap=4.0, noise=1.0)
+    cfg = DecoderConfig(beam=14.0, max_active=500)
+    plain = decode_batch(s.graph, cfg, utts)
+    pb = PhraseBoost({tuple(h.words[:2]): 2.5 for h in plain if len(h.words) >= 2})
+    out = {}
+    for mode in ("pre", "general"):
+        if mode == "general":
+            monkeypatch.setenv("CTW_LAT_NOPRE", "1")
+        out[mode] = decode_lattices(s.graph, cfg, utts, lattice_beam=4.0, boost=[pb] * 4)
+    for a, b in zip(out["pre"], out["general"]):
+        assert a.status == b.status == 0 and a.num_arcs == b.num_arcs > 0
+        ca, cb = _canon(a), _canon(b)
+        assert [x[:4] for x in ca] == [x[:4] for x in cb]
+        assert all(abs(x[4] - y[4]) <= W_TOL * max(1.0, abs(y[4])) for x, y in zip(ca, cb))
+        assert a.best_path == b.best_path
