@@ -31,7 +31,7 @@
 // depend on the lane (boosts and phrase automata only act on labelled arcs):
 // they are computed once per graph into an index (k_closure_index: per state
 // the epsilon-reachable states and their minimum path weight), and the work
-// item of the indexed kernel (PRE) reads its closure as one contiguous run of
+// item of the indexed kernel (k_lattice_idx) reads its closure as one contiguous run of
 // 16-byte entries and probes a shared-memory copy of the layer's destination
 // map -- no per-thread closure arrays, no local memory, ~4 dependent memory
 // round trips per item instead of ~50. Arc weights are then c0 + (w1 + w2 +
@@ -107,7 +107,7 @@ namespace {
 struct LatArgs {
   CtwLane* lanes;
   LatGraph g;
-  const uint32_t* clo_off;  // closure index (PRE kernel): per state offset | CTW_CLO_NONE
+  const uint32_t* clo_off;  // closure index (k_lattice_idx): per state offset | CTW_CLO_NONE
   const CtwClo* clo_ent;
   CtwLatEntry* ent;
   const void* loglik;
