@@ -19,13 +19,16 @@ for _ in range(2):
     decode_batch(s.graph, cfg, host, search="fast")
 lp = s.graph.device_graph(0).pool(cfg, s.graph.num_states, "fast")
 for _ in range(3):
+    h0 = lp.host_timing()
     k0 = lp.stats()["decode_ms"]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     decode_batch(s.graph, cfg, host, search="fast")
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    print(f"wall {1e3 * (t1 - t0):.1f} ms, frame kernel {lp.stats()['decode_ms'] - k0:.1f} ms")
+    h1 = lp.host_timing()
+    print(f"wall {1e3 * (t1 - t0):.1f} ms, frame kernel {lp.stats()['decode_ms'] - k0:.1f} ms,",
+          {k: round(1e3 * (h1[k] - h0[k]), 2) for k in h1 if isinstance(h1[k], float)})
 pr = cProfile.Profile()
 pr.enable()
 decode_batch(s.graph, cfg, host, search="fast")
