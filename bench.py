@@ -284,10 +284,21 @@ def streaming_run(s, n_streams, seconds, seed, device=None, reference=False, cor
     the reference's stream-sim scheduler (cli.py:209-297) through the public
     StreamPool API. Returns latency stats (p50/p99 per the reference's
     order-statistic convention) and the final hypotheses."""
-    from paper_2311_04996_b200 import streamsim
-
     frames = int(round(seconds / FRAME_S))
     utts = list(workload(s, n_streams, frames, 7000 + seed))
+    import gc
+
+    gc.collect()
+    gc.disable()  # (both arms: a cyclic-GC pause of the driving script is not a decoder latency)
+    try:
+        return _streaming_run(s, n_streams, seconds, seed, device, reference, cores, search, frames, utts)
+    finally:
+        gc.enable()
+
+
+def _streaming_run(s, n_streams, seconds, seed, device, reference, cores, search, frames, utts):
+    from paper_2311_04996_b200 import streamsim
+
     if reference:
         ctcwfst = ref_module()
         from ctcwfst.streaming import BatcherConfig, Chunk, StreamPool

@@ -2397,9 +2397,46 @@ static int launch_decode_r(CtwLane* d_lanes, const CtwStateRange* ranges, const 
 }
 
 #ifdef CTW_WIDE
+#ifndef CTW_WIDE_FN
+#define CTW_WIDE_FN ctw_launch_decode_wide
+#define CTW_WIDE_MAXC ctw_wide_max_clusters
+#else
+#define CTW_WIDE_MAXC ctw_wide64_max_clusters
+#endif
+// How many 16-CTA clusters of this build can be resident at once (a lane is
+// one cluster: a launch of more lanes than this runs in waves), for a
+// launch of the given frame width.
+extern "C" int CTW_WIDE_MAXC(int width) {
+  static int last_dyn = -1, last = 0;
+  const size_t dyn = (width <= CTW_MAX_SMEM_WIDTH ? (size_t)width : 0) * sizeof(double);
+  if ((int)dyn == last_dyn) return last;
+  void (*KFN)(CtwLane*, GraphDev, ChunkArgs, CtwLaneOut*) = k_decode_chunk<false, true>;
+  if (dyn + sizeof(Smem) > 48 * 1024)
+    cudaFuncSetAttribute(KFN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  cudaFuncSetAttribute(KFN, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(16 * 64);
+  lc.blockDim = dim3(CTW_BS);
+  lc.dynamicSmemBytes = dyn;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 16;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int m = 0;
+  if (cudaOccupancyMaxActiveClusters(&m, (void*)KFN, &lc) != cudaSuccess) {
+    (void)cudaGetLastError();
+    m = 0;
+  }
+  last = m;
+  last_dyn = (int)dyn;
+  return m;
+}
 // 1024-thread CTAs, 16 per lane: twice the threads of a 512 x 16 lane, for
 // launches too small to fill the GPU (streaming steps: per-lane latency)
-extern "C" int ctw_launch_decode_wide(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
+extern "C" int CTW_WIDE_FN(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                       const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
                                       int width, const long long* ll_off, const int* nframes, const int* lane_ids,
                                       int n, const CtwDecodeCfg* cfg, CtwLaneOut* out, int any_fsa, int fast,
@@ -2411,13 +2448,20 @@ extern "C" int ctw_launch_decode_wide(CtwLane* d_lanes, const CtwStateRange* ran
 extern "C" int ctw_launch_decode_wide(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
                                       const void*, int, int, const long long*, const int*, const int*, int,
                                       const CtwDecodeCfg*, CtwLaneOut*, int, int, int, int, cudaStream_t);
+extern "C" int ctw_launch_decode_wide64(CtwLane*, const CtwStateRange*, const CtwArc*, const int32_t*, const double*,
+                                        const void*, int, int, const long long*, const int*, const int*, int,
+                                        const CtwDecodeCfg*, CtwLaneOut*, int, int, int, int, cudaStream_t);
+extern "C" int ctw_wide_max_clusters(int);
+extern "C" int ctw_wide64_max_clusters(int);
 
 // Ranks (CTAs) per lane for a launch of n lanes: CTW_CLUSTER overrides.
 // Otherwise 8 x 512 threads (best throughput when lanes fill the GPU: 74
 // clusters resident); launches too small to fill the GPU -- streaming steps,
 // where per-lane latency is the metric -- take 16 CTAs per lane, of 1024
-// threads while 16 x 1024-thread clusters still fit (C4: p50 2.79 -> 2.30 ms,
-// p99 4.13 -> 3.34 ms against 512-thread CTAs), else of 512.
+// threads while all its 16 x 1024-thread clusters can be resident at once
+// (C4: p50 2.79 -> 2.30 ms, p99 4.13 -> 3.34 ms against 512-thread CTAs),
+// else of 512; while the clusters of the build with 64 registers per thread
+// (one CTA per SM, no spills) all fit, that build (C4 p50 -1.8 %).
 extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, const CtwArc* arcs,
                                  const int32_t* olabel, const double* final_w, const void* loglik, int is_f64,
                                  int width, const long long* ll_off, const int* nframes, const int* lane_ids, int n,
@@ -2438,7 +2482,10 @@ extern "C" int ctw_launch_decode(CtwLane* d_lanes, const CtwStateRange* ranges, 
   int R = CTW_DEFAULT_CLUSTER;
   if (env) {
     R = env;
-  } else if ((long long)n * 16 <= (long long)sms * (2048 / 1024) && !getenv("CTW_NO_WIDE")) {
+  } else if (n <= ctw_wide64_max_clusters(width) && !getenv("CTW_NO_WIDE") && !getenv("CTW_NO_WIDE64")) {
+    return ctw_launch_decode_wide64(d_lanes, ranges, arcs, olabel, final_w, loglik, is_f64, width, ll_off, nframes,
+                                    lane_ids, n, cfg, out, any_fsa, fast, ebits, eps_lab, stream);
+  } else if (n <= ctw_wide_max_clusters(width) && !getenv("CTW_NO_WIDE")) {
     return ctw_launch_decode_wide(d_lanes, ranges, arcs, olabel, final_w, loglik, is_f64, width, ll_off, nframes,
                                   lane_ids, n, cfg, out, any_fsa, fast, ebits, eps_lab, stream);
   } else if ((long long)n * 16 <= (long long)sms * CTW_MINB) {

@@ -251,19 +251,23 @@ def test_bench_scale_fast_equals_exact():
 
 @pytest.mark.parametrize("search", ["exact", "fast"])
 def test_wide_and_narrow_launch_shapes_agree(monkeypatch, search):
-    """Small launches run the frame kernel with 1024-thread CTAs (16 per lane),
-    full batches with 512-thread CTAs (8 per lane): same hypotheses and, in
-    the exact mode, the same histories."""
+    """Small launches run the frame kernel with 1024-thread CTAs (16 per lane;
+    the 64-register build while its clusters all fit, else the 32-register
+    one), full batches with 512-thread CTAs (8 per lane): same hypotheses
+    and, in the exact mode, the same histories."""
     from paper_2311_04996_b200 import DecoderConfig, DecodeState, decode_batch, synth
 
     s = _system(num_units=129, blank_id=128, num_words=300, order=3, seed=13, min_pron=1, max_pron=4,
                 followers=15)
     utts = list(synth.conformer_logprobs(s, 6, 60, seed=4, delta=5.0, sigma=1.5, dtype=np.float32))
     cfg = DecoderConfig(beam=15.0, max_active=400)
-    wide = decode_batch(s.graph, cfg, utts, search=search)
+    wide = decode_batch(s.graph, cfg, utts, search=search)  # 6 lanes: the 64-register wide build
+    monkeypatch.setenv("CTW_NO_WIDE64", "1")
+    wide32 = decode_batch(s.graph, cfg, utts, search=search)
+    monkeypatch.delenv("CTW_NO_WIDE64")
     monkeypatch.setenv("CTW_NO_WIDE", "1")
     narrow = decode_batch(s.graph, cfg, utts, search=search)
-    assert wide == narrow
+    assert wide == wide32 == narrow
     if search == "exact":
         monkeypatch.delenv("CTW_NO_WIDE")
         a = DecodeState(s.graph, cfg)
